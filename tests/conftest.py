@@ -1,0 +1,39 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+    config.addinivalue_line("markers", "slow: long-running parity case")
+
+
+@pytest.fixture(scope="session")
+def orc():
+    """The restatement oracle (always available)."""
+    from oracle.oracle import Oracle
+    return Oracle.restatement()
+
+
+@pytest.fixture(scope="session")
+def ref():
+    """The reference's own compiled sources (None when oracle/_ref was not built)."""
+    from oracle.oracle import Oracle
+    return Oracle.reference()
+
+
+@pytest.fixture(scope="session")
+def golden():
+    import json
+
+    import numpy as np
+    d = os.path.join(ROOT, "tests", "golden")
+    with open(os.path.join(d, "golden.json")) as f:
+        meta = json.load(f)
+    arrays = dict(np.load(os.path.join(d, "golden.npz")))
+    return meta, arrays
