@@ -1,0 +1,363 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 GaBP hot path (BASELINE.json metric: GaBP edge-message updates/s and
+achieved HBM GB/s; time to residual 1e-8).
+
+Default workload = BASELINE.json config 2: poisson5(2048, 2048), b ~ U[-1,1] seed 1, synchronous
+(flood) GaBP solve with the reference's stop rule (rel. residual 1e-8, 20000-sweep cap).  One
+"step" = one solve iteration exactly as GabpEngine::solve runs it (gabp.cpp:187-218): a flood sweep,
+the residual check ||b - A x||_inf and the stop test.  value = edge-message updates/s over the
+whole job = n_gpus * E * K / (max over ranks of the device time of K steps).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--workload mg]
+
+With --impl reference, rank 0 times the reference's own CPU implementation (oracle/_ref, the
+reference sources compiled here; else the restatement) on the same workload and prints the same
+line with "impl": "reference"; other ranks exit 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GaBP edge-message updates/sec"
+UNIT = "edge-updates/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.p:
+            time.sleep(0.1)
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (self.out or "").strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = max(smax, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        import torch
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------------------------------------
+# CPU baseline: the reference's own GabpEngine::solve on the host cores
+# ------------------------------------------------------------------------------------------------
+def cpu_reference_rate(P, iters):
+    """Time `iters` iterations of the reference's solve loop (sweep + residual) on config 2."""
+    from oracle.oracle import Oracle, Csr, Schedule as OSched
+    o = Oracle.reference()
+    kind = "reference"
+    if o is None:
+        o, kind = Oracle.restatement(), "port"
+    A = Csr(P.A.n, P.A.row_offsets, P.A.col_indices, P.A.values)
+    eng = o.engine(A)
+    E = eng.num_edges
+    tol = 1e-8 * float(np.abs(P.b).max())
+    eng.solve(P.b, OSched.parallel_flood(), tol=tol, max_iter=1)  # warm-up (page-in, allocator)
+    t0 = time.perf_counter()
+    rep = eng.solve(P.b, OSched.parallel_flood(), tol=tol, max_iter=iters)
+    dt = time.perf_counter() - t0
+    assert rep.iterations == iters
+    return {"value": E * iters / dt, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"{iters} solve iterations (flood sweep + residual, gabp.cpp:187-218) of the full config-2 "
+                      f"system, 1 thread (the reference is single-threaded), best of 1 after 1 warm-up iteration",
+            "seconds": dt, "cpu": _cpu_name(), "nproc": os.cpu_count()}
+
+
+def _cpu_name():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference_arm(args, world, rank):
+    if rank != 0:
+        return
+    import paper_1904_04093_b200 as g  # input generation only (host code, no device work)
+    P = g.config_problem(2)
+    iters = max(1, min(args.steps, args.ref_iters))
+    cb = cpu_reference_rate(P, iters)
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
+            "steps": iters, "warmup": 1, "ms_per_step": cb["seconds"] * 1e3 / iters, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE.json config 2)",
+            "config": workload_config(P, args),
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(P, args, eng_info=None):
+    n = P.A.n
+    E = int(P.A.nnz - n)
+    cfg = {"workload": "config2: poisson5 2048x2048, flood GaBP solve loop (sweep + residual + stop test per step)",
+           "n": n, "nnz": int(P.A.nnz), "edges": E, "tol": "1e-8*||b||_inf", "max_iter": 20000,
+           "l2": "inputs larger than L2: %.0f MB moved per sweep vs 126 MB L2" % ((40 * E + 24 * n) / 1e6),
+           "parallelism": f"{args.gpus} independent replicas (one system per GPU)"}
+    if eng_info:
+        cfg["layout"] = {1: "DIA", 2: "CSR"}[eng_info["layout"]]
+    return cfg
+
+
+# ------------------------------------------------------------------------------------------------
+# GPU arm
+# ------------------------------------------------------------------------------------------------
+def run_gpu(args, world, rank, local):
+    import torch
+
+    import paper_1904_04093_b200 as g
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    P = g.config_problem(2)
+    n = P.A.n
+    eng = g.GabpEngine(P.A)
+    E = eng.num_edges
+    info = eng.info
+    stream = torch.cuda.ExternalStream(eng.stream(), device=dev)
+    b_host = torch.from_numpy(P.b).pin_memory()
+    b_dev = b_host.to(dev)
+    tol = 1e-8 * float(np.abs(P.b).max())
+    max_iter = max(20000, args.warmup + args.steps + 2)
+    opt = g.GabpOptions(tol=tol, max_iter=max_iter)
+    sched = g.Schedule.parallel_flood()
+
+    # ---- headline: K solve iterations with b resident in HBM -----------------------------------
+    eng.solve_device_begin(b_dev.data_ptr(), sched, opt)
+    eng.solve_device_steps(args.warmup)
+    torch.cuda.synchronize()
+    barrier(world)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        eng.solve_device_steps(args.steps)
+        ev1.record(stream)
+        ev1.synchronize()
+        torch.cuda.synchronize()
+    barrier(world)
+    ms = ev0.elapsed_time(ev1)
+    status, its, _, _ = eng.solve_device_end()
+    assert int(status) == 2 and its >= args.warmup + args.steps - 1, (status, its)  # no early stop in the window
+    ms_max = max_over_ranks(ms, world)
+    value = world * E * args.steps / (ms_max / 1e3)
+
+    # ---- dominant kernel alone: K bare flood sweeps, CUDA events on the launching stream -------
+    eng.flood_sweeps_device(b_dev.data_ptr(), 3)
+    torch.cuda.synchronize()
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k0.record(stream)
+    eng.flood_sweeps_device(b_dev.data_ptr(), args.steps)
+    k1.record(stream)
+    k1.synchronize()
+    t_sweep = k0.elapsed_time(k1) / args.steps / 1e3
+    bytes_sweep = float(info["bytes_per_sweep"])
+    peak, peak_src = peaks()
+    achieved = bytes_sweep / t_sweep / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "flood_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- end to end through the public C-ABI with host buffers -----------------------------------
+    e2e_sweeps = args.e2e_sweeps
+    e2e_opt = g.GabpOptions(tol=tol, max_iter=e2e_sweeps)
+    b_np = b_host.numpy()
+    eng.solve(b_np, sched, g.GabpOptions(tol=tol, max_iter=2))  # warm path
+    torch.cuda.synchronize()
+    barrier(world)
+    t0 = time.perf_counter()
+    reps = []
+    for _ in range(args.e2e_calls):
+        reps.append(eng.solve(b_np, sched, e2e_opt))
+    t_e2e = max_over_ranks(time.perf_counter() - t0, world)
+    assert all(r.iterations == e2e_sweeps for r in reps)
+    e2e_value = world * E * e2e_sweeps * args.e2e_calls / t_e2e
+    h2d = 8 * n  # b per solve call
+    d2h = 8 * n + 8 * (e2e_sweeps + 1)  # x + residual history per call
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE.json config 2: b ~ U[-1,1], seed 1)",
+            "config": workload_config(P, args, info),
+            "roofline": {"bound": "hbm", "kernel": "k_flood_dia<4> (K1 fused flood sweep)", "achieved": achieved,
+                         "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": peak_src, "bytes_per_launch": bytes_sweep,
+                         "bytes_formula": "40*E + 24*n (SURVEY.md 8(d))", "us_per_launch": t_sweep * 1e6,
+                         "frac_of_8TBs": achieved / 8000.0, "share_of_step": t_sweep * 1e3 / (ms_max / args.steps)},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / e2e_sweeps,
+                    "d2h_bytes_per_step": d2h / e2e_sweeps,
+                    "how": f"{args.e2e_calls} x bgabp_solve(host b, max_iter={e2e_sweeps}) incl. H2D b, D2H x + history"},
+            "gpu_launches": 3 * args.steps, "clocks": clk.summary()}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cb = cpu_reference_rate(P, args.ref_iters)
+            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as ex:  # the oracle is test infrastructure; its absence must not hide the GPU number
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "unavailable", "sample": str(ex)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------------
+# config 5: multigrid V(2,2) time to 1e-8 (secondary line, --workload mg)
+# ------------------------------------------------------------------------------------------------
+def run_mg(args, world, rank, local):
+    import torch
+
+    import paper_1904_04093_b200 as g
+    torch.cuda.set_device(local)
+    J = args.mg_J
+    levels, nxs = [], []
+    for k in range(J - 4):  # down to 31 x 31 (J = 5)
+        p = g.config5_level(J, k)
+        levels.append(p.A)
+        nxs.append(p.nx)
+        if k == 0:
+            b = p.b
+    out = {"metric": "multigrid V(2,2) time to rel. residual 1e-8", "unit": "s", "higher_is_better": False,
+           "config": {"workload": f"config5: var-coeff 2D diffusion {nxs[0]}^2, K=exp(N(0,2^2)), {len(levels)} levels"},
+           "dtype": "f64", "data": "synthetic (BASELINE.json config 5, seed 4)", "results": {}}
+    bd = torch.tensor(b, device="cuda")
+    xd = torch.zeros_like(bd)
+    tol = 1e-8 * float(np.abs(b).max())
+    for name, sm in (("gabp_red_black", g.MgSmoother.GabpRedBlack), ("gs_red_black", g.MgSmoother.GsRedBlack),
+                     ("gabp_flood", g.MgSmoother.GabpFlood)):
+        t0 = time.perf_counter()
+        h = g.Hierarchy.from_levels(levels, nxs, sm)
+        setup = time.perf_counter() - t0
+        spec = g.CycleSpec(2, 2, sm)
+        cap = args.mg_cycles if sm != g.MgSmoother.GabpFlood else min(args.mg_cycles, 30)
+        g.mg_solve_device(h, spec, bd.data_ptr(), xd.data_ptr(), g.MgSolveOptions(tol=tol, max_cycles=2))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep = g.mg_solve_device(h, spec, bd.data_ptr(), xd.data_ptr(), g.MgSolveOptions(tol=tol, max_cycles=cap))
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        out["results"][name] = {"status": rep.status.name, "cycles": rep.iterations, "seconds": dt,
+                                "setup_seconds": setup, "levels": h.num_levels(),
+                                "final_rel_residual": float(rep.residual_history[-1] / np.abs(b).max())}
+        del h
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="config2", choices=["config2", "mg"])
+    ap.add_argument("--e2e-sweeps", type=int, default=500)
+    ap.add_argument("--e2e-calls", type=int, default=3)
+    ap.add_argument("--ref-iters", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mg-J", type=int, default=12)
+    ap.add_argument("--mg-cycles", type=int, default=100)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        run_reference_arm(args, world, rank)
+        return
+    world, rank, local = dist_setup()
+    if args.workload == "mg":
+        run_mg(args, world, rank, local)
+    else:
+        run_gpu(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

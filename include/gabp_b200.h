@@ -1,0 +1,222 @@
+/*
+ * gabp_b200.h — C-ABI of the B200 (sm_100a) GaBP hot path.
+ *
+ * This is the drop-in boundary for the reference's solver and smoother entry points in
+ * proj/core (paths below are relative to /root/reference/proj/core).  Plain pointers and sizes,
+ * no exceptions, no C++ or torch types.  A handle owns its device copy of the matrix, the
+ * device message layout, the message buffers and one CUDA stream; it is not re-entrant, but
+ * separate handles may be used concurrently from different threads.
+ *
+ * Host buffers are used by every call that has no `_device` suffix; those calls copy inputs to
+ * the device, run, and copy results back before returning.  `_device` calls take device
+ * pointers, enqueue on the handle's stream and return without synchronising unless stated.
+ *
+ * Return codes: BGABP_OK (0), BGABP_EINVAL (1, the reference throws std::invalid_argument),
+ * BGABP_EPIVOT (2, the reference returns false / Diverged with the same message text),
+ * BGABP_ECUDA (3), BGABP_ERUNTIME (4, the reference throws std::runtime_error).
+ * Every call taking (err, errlen) writes the reference's message text there.
+ */
+#ifndef GABP_B200_H
+#define GABP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { BGABP_OK = 0, BGABP_EINVAL = 1, BGABP_EPIVOT = 2, BGABP_ECUDA = 3, BGABP_ERUNTIME = 4 };
+
+/* ScheduleKind (schedule.hpp:9-15) + constructor used (schedule.cpp:51-103) */
+enum {
+    BGABP_SCHED_FLOOD = 0,           /* Schedule::parallel_flood()                         */
+    BGABP_SCHED_SEQUENTIAL = 1,      /* Schedule::sequential(n)                            */
+    BGABP_SCHED_RED_BLACK_GRID = 2,  /* Schedule::red_black_grid(nx, ny)                   */
+    BGABP_SCHED_FOUR_COLOR_GRID = 3, /* Schedule::four_color_grid(nx, ny)                  */
+    BGABP_SCHED_CUSTOM = 4,          /* Schedule::custom(order)                            */
+    BGABP_SCHED_RED_BLACK = 5,       /* Schedule::red_black(A)  (greedy)                   */
+    BGABP_SCHED_FOUR_COLOR = 6       /* Schedule::four_color(A) (greedy)                   */
+};
+
+/* SolveStatus (report.hpp:10) and StopCriterion (gabp.hpp:37) */
+enum { BGABP_CONVERGED = 0, BGABP_DIVERGED = 1, BGABP_MAX_ITER = 2 };
+enum { BGABP_STOP_RESIDUAL = 0, BGABP_STOP_MESSAGE_DELTA = 1 };
+
+/* device message layout chosen at create time */
+enum { BGABP_LAYOUT_AUTO = 0, BGABP_LAYOUT_DIA = 1, BGABP_LAYOUT_CSR = 2 };
+
+typedef struct {
+    int kind;
+    int nx, ny;       /* grid kinds */
+    const int* order; /* BGABP_SCHED_CUSTOM: permutation of 0..n-1 (host) */
+} bgabp_schedule;
+
+/* GabpOptions (gabp.hpp:39-45); pivot_floor is not a field: the reference never reads it
+ * (gabp.hpp:43 vs the engine's private 1e-300, gabp.hpp:110) */
+typedef struct {
+    double tol;               /* absolute inf-norm tolerance (reference default 2e-4) */
+    int max_iter;             /* reference default 20000 */
+    int stop;                 /* BGABP_STOP_* */
+    double divergence_factor; /* reference default 1e12 */
+} bgabp_options;
+
+/* SolveReport (report.hpp:21-28) minus the vectors, which are caller buffers */
+typedef struct {
+    int status;
+    int iterations;
+    double flop_estimate;
+} bgabp_report;
+
+typedef struct {
+    int n;
+    long long nnz;
+    long long num_edges;          /* MessageGraph::num_edges (gabp.cpp:22) */
+    int layout;                   /* BGABP_LAYOUT_DIA or BGABP_LAYOUT_CSR */
+    int num_slots;                /* DIA: slots (distinct neighbour offsets) per node */
+    int symmetric_values;         /* 1 if A == A^T bit for bit (residual reuses the sweep coefficients) */
+    double bytes_per_sweep;       /* algorithmic B_sweep = 40 E + 24 n */
+    double bytes_per_residual;    /* algorithmic B_res = 8 nnz + 16 n */
+    long long device_bytes;       /* device memory held by the handle */
+} bgabp_info;
+
+typedef struct bgabp_engine bgabp_engine;
+
+/* ---- engine lifetime: GabpEngine::GabpEngine(const SparseMatrix&) (gabp.cpp:29-33) ----------
+ * Input is canonical CSR (sparse.hpp:10-27: strictly increasing columns per row).  The reverse
+ * edge index (SparseMatrix::transpose_pos, sparse.cpp:70-74) is rebuilt internally.
+ * EINVAL "gabp: matrix has a structurally zero diagonal entry" as gabp.cpp:30-32. */
+int bgabp_create(int n, const int* row_offsets, const int* col_indices, const double* values,
+                 int layout, bgabp_engine** out, char* err, size_t errlen);
+void bgabp_destroy(bgabp_engine* e);
+int bgabp_get_info(const bgabp_engine* e, bgabp_info* info);
+/* the handle's CUDA stream (cudaStream_t), for callers that time or order work around it */
+void* bgabp_stream(bgabp_engine* e);
+
+/* ---- message state: MessageState (gabp.hpp:31-35) ----------------------------------------------
+ * CSR-position indexed arrays of length nnz; diagonal slots read back as 0. */
+int bgabp_reset_state(bgabp_engine* e); /* make_state(): zeros (gabp.cpp:35-40) */
+int bgabp_set_state(bgabp_engine* e, const double* lambda_tilde, const double* m);
+int bgabp_get_state(bgabp_engine* e, double* lambda_tilde, double* m);
+
+/* ---- one sweep: GabpEngine::sweep(b, sched, state, x, &err) (gabp.cpp:42-47) ------------------
+ * Advances the handle's state.  x is in/out (n): the sequential and coloured schedules write
+ * every node they visit, flood writes all of x from the new messages (gabp.cpp:141-160).
+ * EPIVOT with "zero pivot on edge j->i" / "zero pivot at node i" as gabp.cpp:71-74,83-87,126-130,
+ * 155-158 (state contents after a breakdown are not contractual). */
+int bgabp_sweep(bgabp_engine* e, const double* b, const bgabp_schedule* sched, double* x,
+                char* err, size_t errlen);
+
+/* node_precisions(state) (gabp.cpp:403-419) of the handle's current state */
+int bgabp_node_precisions(bgabp_engine* e, double* beta);
+double bgabp_sweep_flops(const bgabp_engine* e); /* gabp.cpp:165-172 */
+
+/* ---- solve(b, sched, opt) (gabp.cpp:174-219) ------------------------------------------------------
+ * Starts from make_state() and leaves the handle's state at the last sweep run.  x_out (n) gets
+ * the solution, history (max_iter+1, nullable) the residual history; detail gets
+ * SolveReport::detail.  Iteration counts, statuses and details follow the reference exactly. */
+int bgabp_solve(bgabp_engine* e, const double* b, const bgabp_schedule* sched,
+                const bgabp_options* opt, bgabp_report* rep, double* x_out, double* history,
+                char* detail, size_t detaillen);
+
+/* Device-resident stepping form of bgabp_solve for drivers that keep b and x in HBM:
+ *   begin: reset state, r0 = ||b||_inf (device b), arm the stop logic;
+ *   steps: enqueue `nsteps` solve iterations (sweep + residual check + stop test) without
+ *          synchronising; iterations after the stop decision are no-ops on the device;
+ *   end:   synchronise and fill the report; x_dev (n) receives the solution, history_dev
+ *          (max_iter+1) the residual history (both device pointers, nullable). */
+int bgabp_solve_device_begin(bgabp_engine* e, const double* b_dev, const bgabp_schedule* sched,
+                             const bgabp_options* opt);
+int bgabp_solve_device_steps(bgabp_engine* e, int nsteps);
+int bgabp_solve_device_end(bgabp_engine* e, bgabp_report* rep, double* x_dev, double* history_dev,
+                           char* detail, size_t detaillen);
+/* `nsweeps` bare flood sweeps on device b (no residual, no stop logic): the hot kernel alone,
+ * for timing it with events on bgabp_stream(). */
+int bgabp_flood_sweeps_device(bgabp_engine* e, const double* b_dev, int nsweeps);
+
+/* residual_inf_norm(A, x, b) (sparse.cpp:104-115) on the handle's matrix */
+int bgabp_residual_inf_norm(bgabp_engine* e, const double* x, const double* b, double* out);
+
+/* ---- frozen-precision path (gabp.cpp:221-401) ------------------------------------------------------
+ * precompute_lambda keeps the result on the device for the correction calls; lambda_out (nnz,
+ * CSR order) and sigma_out (n) are nullable host copies.  set_frozen loads a FrozenLambda. */
+int bgabp_precompute_lambda(bgabp_engine* e, const bgabp_schedule* sched, double tol, int max_iter,
+                            double* lambda_out, double* sigma_out, int* converged, int* iterations);
+int bgabp_set_frozen(bgabp_engine* e, const double* lambda_tilde, const double* sigma);
+int bgabp_correction_sweeps(bgabp_engine* e, const double* r, const bgabp_schedule* sched,
+                            int sweeps, double* e_out);
+int bgabp_error_correction_apply(bgabp_engine* e, const double* b, const double* x0, int sweeps,
+                                 const bgabp_schedule* sched, int use_frozen, double* x_out,
+                                 char* err, size_t errlen);
+int bgabp_solve_error_correction(bgabp_engine* e, const double* b, const bgabp_schedule* sched,
+                                 int sweeps, const bgabp_options* opt, bgabp_report* rep,
+                                 double* x_out, double* history, char* detail, size_t detaillen);
+
+/* ---- multigrid with the GaBP smoother (multigrid.hpp:17-103, multigrid.cpp:54-318) ----------------
+ * Levels are supplied by the caller finest first (the reference rediscretises a named problem per
+ * level, multigrid.cpp:79-83; bgmg_create_named does that with the built-in assembly).  Smoother
+ * numbering = MgSmoother (multigrid.hpp:17-31): 0 GabpSequential 1 GabpRedBlack 2 GabpFourColor
+ * 3 GabpFlood 5 Jacobi 6 GsLex 7 GsRedBlack 8 GsFourColor.  Coarsening stops where the
+ * sweeps_expand probe fires (multigrid.cpp:54-70, 89-93); the coarsest level is solved directly. */
+typedef struct bgmg bgmg;
+typedef struct {
+    int pre, post; /* CycleSpec (multigrid.hpp:33-40) */
+    int frozen;
+} bgmg_cycle;
+typedef struct {
+    double tol;               /* MgSolveOptions (multigrid.hpp:96-100): absolute, default 2e-4 */
+    int max_cycles;           /* default 200 */
+    double divergence_factor; /* default 1e6 */
+} bgmg_options;
+
+int bgmg_create(int nlevels, const int* n, const int* const* row_offsets,
+                const int* const* col_indices, const double* const* values, const int* nx,
+                int smoother, bgmg** out, char* err, size_t errlen);
+int bgmg_create_named(const char* problem, int J1, int J2, int nparam, const char* const* keys,
+                      const double* vals, int smoother, bgmg** out, char* err, size_t errlen);
+void bgmg_destroy(bgmg* h);
+int bgmg_num_levels(const bgmg* h);
+int bgmg_level_frozen_ok(const bgmg* h, int k);
+int bgmg_level_n(const bgmg* h, int k);
+/* fine-level right-hand side of a named hierarchy (Hierarchy::fine_rhs, multigrid.hpp:62) */
+int bgmg_fine_rhs(const bgmg* h, double* b_out);
+int bgmg_vcycle(bgmg* h, const bgmg_cycle* spec, const double* b, double* x, char* err,
+                size_t errlen);
+int bgmg_solve(bgmg* h, const bgmg_cycle* spec, const double* b, const bgmg_options* opt,
+               bgabp_report* rep, double* x_out, double* history, char* detail, size_t detaillen);
+/* device-resident mg_solve: b_dev / x_dev device pointers; synchronises at every cycle's stop test */
+int bgmg_solve_device(bgmg* h, const bgmg_cycle* spec, const double* b_dev,
+                      const bgmg_options* opt, bgabp_report* rep, double* x_dev, double* history,
+                      char* detail, size_t detaillen);
+void* bgmg_stream(bgmg* h);
+/* transfer operators on host buffers, run on the device (multigrid.cpp:111-161) */
+int bgmg_restrict(const double* fine, int mf, double* coarse_out);
+int bgmg_prolong(const double* coarse, int mc, double* fine_out);
+
+/* ---- problem assembly (input generation; host only, no device work) ----------------------------
+ * Named problems restate assemble(name, J, params) (problems.cpp:161-226); the config generators
+ * are the BASELINE.json workloads the reference cannot assemble. */
+typedef struct bgabp_problem bgabp_problem;
+bgabp_problem* bgabp_problem_named(const char* name, int J, int nparam, const char* const* keys,
+                                   const double* vals, char* err, size_t errlen);
+bgabp_problem* bgabp_problem_poisson5(int nx, int ny);          /* tests/oracles.hpp:140-152 */
+bgabp_problem* bgabp_problem_config(int config, int size, unsigned seed); /* configs 2..5 */
+/* config-5 coarse level: same K field rule, level `k` below the finest (k=0 finest) */
+bgabp_problem* bgabp_problem_config5_level(int J_fine, int k, unsigned seed);
+void bgabp_problem_free(bgabp_problem* p);
+int bgabp_problem_n(const bgabp_problem* p);
+long long bgabp_problem_nnz(const bgabp_problem* p);
+int bgabp_problem_nx(const bgabp_problem* p);
+const int* bgabp_problem_row_offsets(const bgabp_problem* p);
+const int* bgabp_problem_col_indices(const bgabp_problem* p);
+const double* bgabp_problem_values(const bgabp_problem* p);
+const double* bgabp_problem_rhs(const bgabp_problem* p);   /* b (n) */
+const double* bgabp_problem_exact(const bgabp_problem* p); /* manufactured solution or NULL */
+
+/* library build tag (sm arch, git-independent) */
+const char* bgabp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,1188 @@
+// Host side of the B200 GaBP engine behind include/gabp_b200.h.
+//
+// Replaces GabpEngine (proj/core/include/belief/gabp.hpp:58-111, src/gabp.cpp) with a handle that
+// owns the device layout of the message graph, the message buffers and a CUDA stream.  Setup is
+// host C++ (layout build, schedule dependency levels); every sweep, residual and reduction runs in
+// the kernels of kernels.cuh.  There is no CPU fallback: a failed CUDA call is BGABP_ECUDA.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "engine.h"
+
+namespace bgabp {
+
+const char* kVersion = "gabp_b200 sm_100a";
+
+// ---------------------------------------------------------------------------------------------
+// helpers
+// ---------------------------------------------------------------------------------------------
+void put_err(char* err, size_t len, const std::string& s) {
+    if (err && len) std::snprintf(err, len, "%s", s.c_str());
+}
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void* Engine::dalloc(size_t bytes) {
+    void* p = nullptr;
+    if (bytes == 0) bytes = 16;
+    ck(cudaMalloc(&p, bytes), "cudaMalloc");
+    allocs.push_back(p);
+    device_bytes += (long long)bytes;
+    return p;
+}
+
+template <class T>
+T* Engine::upload(const std::vector<T>& v) {
+    T* d = static_cast<T*>(dalloc(sizeof(T) * v.size()));
+    if (!v.empty()) ck(cudaMemcpyAsync(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, st), "H2D");
+    return d;
+}
+
+Engine::~Engine() {
+    if (st) cudaStreamSynchronize(st);
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    for (void* p : allocs) cudaFree(p);
+    if (h_ctrl) cudaFreeHost(h_ctrl);
+    if (st && own_stream) cudaStreamDestroy(st);
+}
+
+// ---------------------------------------------------------------------------------------------
+// construction: validate CSR, rebuild transpose_pos, choose and build the device layout
+// ---------------------------------------------------------------------------------------------
+void Engine::build(int n_, const int* ro_, const int* ci_, const double* v_, int want_layout,
+                   cudaStream_t shared_stream) {
+    if (n_ < 0) throw InvalidArg("gabp: negative dimension");
+    n = n_;
+    ro.assign(ro_, ro_ + n + 1);
+    if (ro[0] != 0) throw InvalidArg("gabp: row_offsets[0] must be 0");
+    for (int i = 0; i < n; ++i)
+        if (ro[i + 1] < ro[i]) throw InvalidArg("gabp: row_offsets not monotone");
+    nnz = ro[n];
+    ci.assign(ci_, ci_ + nnz);
+    val.assign(v_, v_ + nnz);
+    std::vector<int> diag_pos(n, -1);
+    for (int i = 0; i < n; ++i)
+        for (int p = ro[i]; p < ro[i + 1]; ++p) {
+            if (ci[p] < 0 || ci[p] >= n) throw InvalidArg("gabp: column index out of range");
+            if (p > ro[i] && ci[p] <= ci[p - 1]) throw InvalidArg("gabp: CSR is not canonical (columns must increase)");
+            if (ci[p] == i) diag_pos[i] = p;
+        }
+    for (int i = 0; i < n; ++i)  // gabp.cpp:29-33
+        if (diag_pos[i] < 0) throw InvalidArg("gabp: matrix has a structurally zero diagonal entry");
+    num_edges = nnz - n;
+
+    // transpose partner of every entry (sparse.cpp:70-74)
+    tpos.assign(nnz, -1);
+    auto find = [&](int r, int c) -> long long {
+        const int* lo = ci.data() + ro[r];
+        const int* hi = ci.data() + ro[r + 1];
+        const int* it = std::lower_bound(lo, hi, c);
+        return (it != hi && *it == c) ? (long long)(it - ci.data()) : -1;
+    };
+    symmetric = true;
+    for (int i = 0; i < n; ++i)
+        for (int p = ro[i]; p < ro[i + 1]; ++p) {
+            tpos[p] = find(ci[p], i);
+            if (tpos[p] < 0 || val[tpos[p]] != val[p] ||
+                std::memcmp(&val[tpos[p]], &val[p], sizeof(double)) != 0)
+                symmetric = false;
+        }
+
+    // union neighbour lists (row j and column j, sorted): the dependency graph of the schedules
+    std::vector<int> ucount(n + 1, 0);
+    for (int i = 0; i < n; ++i)
+        for (int p = ro[i]; p < ro[i + 1]; ++p) {
+            const int j = ci[p];
+            if (j == i) continue;
+            ucount[i + 1]++;                 // i has neighbour j (in-edge j->i)
+            if (tpos[p] < 0) ucount[j + 1]++;  // j has neighbour i only through the out-edge j->i
+        }
+    uptr.assign(n + 1, 0);
+    for (int i = 0; i < n; ++i) uptr[i + 1] = uptr[i] + ucount[i + 1];
+    const long long U = uptr[n];
+    unbr.assign(U, 0);
+    std::vector<int> fill(uptr.begin(), uptr.end() - 1);
+    for (int i = 0; i < n; ++i)
+        for (int p = ro[i]; p < ro[i + 1]; ++p) {
+            const int j = ci[p];
+            if (j == i) continue;
+            unbr[fill[i]++] = j;
+            if (tpos[p] < 0) unbr[fill[j]++] = i;
+        }
+    for (int i = 0; i < n; ++i) std::sort(unbr.begin() + uptr[i], unbr.begin() + uptr[i + 1]);
+
+    // offsets of the union structure decide the layout
+    std::vector<int> offs;
+    {
+        std::map<int, int> seen;
+        for (int i = 0; i < n && (int)seen.size() <= kMaxDia; ++i)
+            for (long long s = uptr[i]; s < uptr[i + 1]; ++s) seen[unbr[s] - i] = 1;
+        for (auto& kv : seen) offs.push_back(kv.first);
+    }
+    const bool dia_ok = !offs.empty() && (int)offs.size() <= kMaxDia && offs.size() % 2 == 0;
+    if (want_layout == BGABP_LAYOUT_DIA && !dia_ok)
+        throw InvalidArg("gabp: DIA layout needs 1..8 symmetric neighbour offsets");
+    layout = (want_layout == BGABP_LAYOUT_CSR || !dia_ok) ? BGABP_LAYOUT_CSR : BGABP_LAYOUT_DIA;
+
+    if (shared_stream) {
+        st = shared_stream;
+        own_stream = false;
+    } else {
+        ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+    }
+    ck(cudaMallocHost((void**)&h_ctrl, sizeof(Ctrl)), "cudaMallocHost");
+    d_ctrl = static_cast<Ctrl*>(dalloc(sizeof(Ctrl)));
+
+    std::vector<double> diag(n);
+    for (int i = 0; i < n; ++i) diag[i] = val[diag_pos[i]];
+    csr2slot.assign(nnz, -1);
+
+    if (layout == BGABP_LAYOUT_DIA) {
+        S = (int)offs.size();
+        std::memset(&dia, 0, sizeof(dia));
+        dia.n = n;
+        dia.S = S;
+        dia.nneg = (int)(std::lower_bound(offs.begin(), offs.end(), 0) - offs.begin());
+        std::map<int, int> slot_of;
+        for (int s = 0; s < S; ++s) {
+            dia.off[s] = offs[s];
+            slot_of[offs[s]] = s;
+        }
+        for (int s = 0; s < S; ++s) dia.rev[s] = slot_of.at(-offs[s]);
+        nslots = (long long)S * n;
+        std::vector<uint32_t> mask(n, 0u);
+        std::vector<double> c((size_t)nslots, 0.0), rowv;
+        if (!symmetric) rowv.assign((size_t)nslots, 0.0);
+        for (int i = 0; i < n; ++i)
+            for (int p = ro[i]; p < ro[i + 1]; ++p) {
+                const int j = ci[p];
+                if (j == i) continue;
+                // entry A_ij: in-edge j->i of node i (slot off=j-i), out-edge j->i of node j (slot off=i-j)
+                const int si = slot_of.at(j - i), sj = slot_of.at(i - j);
+                mask[i] |= 1u << si;
+                mask[j] |= 1u << (16 + sj);
+                c[(size_t)sj * n + j] = val[p];
+                if (!symmetric) rowv[(size_t)si * n + i] = val[p];
+                csr2slot[p] = (long long)si * n + i;
+            }
+        dia.mask = upload(mask);
+        dia.c = upload(c);
+        dia.rowv = symmetric ? dia.c : upload(rowv);
+        dia.diag = upload(diag);
+    } else {
+        S = 0;
+        nslots = U;
+        std::vector<uint8_t> flg(U, 0);
+        std::vector<double> uc(U, 0.0);
+        std::vector<int> urev(U, -1), undiag(n, 0);
+        auto slot = [&](int j, int k) -> long long {  // slot of neighbour k in j's sorted list
+            auto b = unbr.begin() + uptr[j], e = unbr.begin() + uptr[j + 1];
+            return (long long)(std::lower_bound(b, e, k) - unbr.begin());
+        };
+        for (int j = 0; j < n; ++j) {
+            undiag[j] = (int)(std::lower_bound(unbr.begin() + uptr[j], unbr.begin() + uptr[j + 1], j) -
+                              (unbr.begin() + uptr[j]));
+            for (long long s = uptr[j]; s < uptr[j + 1]; ++s) urev[s] = (int)slot(unbr[s], j);
+        }
+        for (int i = 0; i < n; ++i)
+            for (int p = ro[i]; p < ro[i + 1]; ++p) {
+                const int j = ci[p];
+                if (j == i) continue;
+                const long long si = slot(i, j), sj = slot(j, i);
+                flg[si] |= 1;
+                flg[sj] |= 2;
+                uc[sj] = val[p];
+                csr2slot[p] = si;
+            }
+        std::memset(&csr, 0, sizeof(csr));
+        csr.n = n;
+        csr.uptr = upload(uptr);
+        csr.unbr = upload(unbr);
+        csr.uflg = upload(flg);
+        csr.uc = upload(uc);
+        csr.urev = upload(urev);
+        csr.undiag = upload(undiag);
+        csr.diag = upload(diag);
+        csr.ro = upload(ro);
+        csr.ci = upload(ci);
+        csr.val = upload(val);
+    }
+    d_csr2slot = upload(csr2slot);
+    for (int k = 0; k < 2; ++k) {
+        d_msg[k] = static_cast<double2*>(dalloc(sizeof(double2) * (size_t)std::max<long long>(nslots, 1)));
+        ck(cudaMemsetAsync(d_msg[k], 0, sizeof(double2) * (size_t)std::max<long long>(nslots, 1), st), "memset");
+    }
+    const size_t vb = sizeof(double) * (size_t)std::max(n, 1);
+    d_b = static_cast<double*>(dalloc(vb));
+    d_x = static_cast<double*>(dalloc(vb));
+    d_r = static_cast<double*>(dalloc(vb));
+    d_e = static_cast<double*>(dalloc(vb));
+    d_aux = static_cast<double*>(dalloc(vb));
+    cur = 0;
+    ck(cudaStreamSynchronize(st), "setup sync");
+}
+
+// ---------------------------------------------------------------------------------------------
+// schedules: node order (schedule.cpp) -> dependency levels over the union graph
+// ---------------------------------------------------------------------------------------------
+std::vector<int> Engine::schedule_order(const bgabp_schedule& s) const {
+    std::vector<int> order;
+    auto grouped = [&](std::vector<int> colour) {  // schedule.cpp:11-22 (stable, ascending in colour)
+        std::vector<int> o(colour.size());
+        std::iota(o.begin(), o.end(), 0);
+        std::stable_sort(o.begin(), o.end(), [&](int a, int b) { return colour[a] < colour[b]; });
+        return o;
+    };
+    switch (s.kind) {
+        case BGABP_SCHED_SEQUENTIAL:
+            order.resize(n);
+            std::iota(order.begin(), order.end(), 0);
+            break;
+        case BGABP_SCHED_RED_BLACK_GRID:
+        case BGABP_SCHED_FOUR_COLOR_GRID: {
+            if (s.nx < 0 || s.ny < 0) throw InvalidArg("gabp: bad grid shape");
+            std::vector<int> col((size_t)s.nx * s.ny);
+            for (int iy = 0; iy < s.ny; ++iy)
+                for (int ix = 0; ix < s.nx; ++ix)
+                    col[(size_t)iy * s.nx + ix] =
+                        s.kind == BGABP_SCHED_RED_BLACK_GRID ? (ix + iy) % 2 : 2 * (iy % 2) + (ix % 2);
+            order = grouped(std::move(col));
+            break;
+        }
+        case BGABP_SCHED_CUSTOM: {  // schedule.cpp:65-76
+            if (!s.order && n > 0) throw InvalidArg("Schedule::custom: order is not a permutation");
+            order.assign(s.order, s.order + n);
+            std::vector<char> seen(n, 0);
+            for (int v : order) {
+                if (v < 0 || v >= n || seen[v]) throw InvalidArg("Schedule::custom: order is not a permutation");
+                seen[v] = 1;
+            }
+            break;
+        }
+        case BGABP_SCHED_RED_BLACK:
+        case BGABP_SCHED_FOUR_COLOR: {  // greedy first fit over the undirected structure (schedule.cpp:25-47)
+            std::vector<std::vector<int>> adj(n);
+            for (int i = 0; i < n; ++i)
+                for (int p = ro[i]; p < ro[i + 1]; ++p) {
+                    const int j = ci[p];
+                    if (j == i) continue;
+                    adj[i].push_back(j);
+                    adj[j].push_back(i);
+                }
+            std::vector<int> col(n, -1);
+            int nc = 1;
+            std::vector<char> used;
+            for (int i = 0; i < n; ++i) {
+                used.assign(nc + 1, 0);
+                for (int j : adj[i])
+                    if (col[j] >= 0 && col[j] < (int)used.size()) used[col[j]] = 1;
+                int c = 0;
+                while (c < (int)used.size() && used[c]) ++c;
+                col[i] = c;
+                nc = std::max(nc, c + 1);
+            }
+            order = grouped(std::move(col));
+            break;
+        }
+        default:
+            throw InvalidArg("gabp: unknown schedule kind " + std::to_string(s.kind));
+    }
+    if ((int)order.size() != n) throw InvalidArg("gabp: schedule order does not cover every node");
+    return order;
+}
+
+const Levels& Engine::levels_for(const bgabp_schedule& s) {
+    std::string key = std::to_string(s.kind) + ":" + std::to_string(s.nx) + "x" + std::to_string(s.ny);
+    std::vector<int> order = schedule_order(s);
+    if (s.kind == BGABP_SCHED_CUSTOM) {
+        key += ":";
+        for (int v : order) key += std::to_string(v) + ",";
+    }
+    auto it = level_cache.find(key);
+    if (it != level_cache.end()) return *it->second;
+    std::vector<int> pos(n), lev(n, 0);
+    for (int q = 0; q < n; ++q) pos[order[q]] = q;
+    int nlev = 0;
+    for (int q = 0; q < n; ++q) {
+        const int j = order[q];
+        int L = 0;
+        for (long long s2 = uptr[j]; s2 < uptr[j + 1]; ++s2) {
+            const int k = unbr[s2];
+            if (pos[k] < q) L = std::max(L, lev[k] + 1);
+        }
+        lev[j] = L;
+        nlev = std::max(nlev, L + 1);
+    }
+    auto lv = std::make_unique<Levels>();
+    lv->ptr.assign(nlev + 1, 0);
+    for (int j = 0; j < n; ++j) lv->ptr[lev[j] + 1]++;
+    for (int l = 0; l < nlev; ++l) lv->ptr[l + 1] += lv->ptr[l];
+    std::vector<int> nodes(n), npos(n);
+    std::vector<int> fillp(lv->ptr.begin(), lv->ptr.end() - 1);
+    for (int q = 0; q < n; ++q) {  // visit order kept within each level
+        const int j = order[q];
+        const int at = fillp[lev[j]]++;
+        nodes[at] = j;
+        npos[at] = q;
+    }
+    lv->order = order;
+    lv->d_nodes = upload(nodes);
+    lv->d_npos = upload(npos);
+    ck(cudaStreamSynchronize(st), "levels sync");
+    auto& ref = *lv;
+    level_cache[key] = std::move(lv);
+    return ref;
+}
+
+// ---------------------------------------------------------------------------------------------
+// kernel launchers
+// ---------------------------------------------------------------------------------------------
+#define DIA_SWITCH(S_, ...)                                   \
+    switch (S_) {                                             \
+        case 2: { constexpr int SS = 2; __VA_ARGS__; } break; \
+        case 4: { constexpr int SS = 4; __VA_ARGS__; } break; \
+        case 6: { constexpr int SS = 6; __VA_ARGS__; } break; \
+        case 8: { constexpr int SS = 8; __VA_ARGS__; } break; \
+        default: throw InvalidArg("gabp: unsupported DIA slot count"); \
+    }
+
+unsigned nblk_host(long long n, int t) { return (unsigned)std::max<long long>(1, (n + t - 1) / t); }
+static inline unsigned nblk(long long n, int t = 256) { return nblk_host(n, t); }
+
+void Engine::launch_flood(const double* b, double2* m0, double2* m1, double* x, int mode, bool delta) {
+    if (n == 0) return;
+    const unsigned g = nblk(n);
+    if (layout == BGABP_LAYOUT_DIA) {
+        DIA_SWITCH(S, if (delta) k_flood_dia<SS, true><<<g, 256, 0, st>>>(dia, b, m0, m1, x, d_ctrl, mode);
+                   else k_flood_dia<SS, false><<<g, 256, 0, st>>>(dia, b, m0, m1, x, d_ctrl, mode));
+    } else {
+        if (delta)
+            k_flood_csr<true><<<g, 256, 0, st>>>(csr, b, m0, m1, x, d_ctrl, mode);
+        else
+            k_flood_csr<false><<<g, 256, 0, st>>>(csr, b, m0, m1, x, d_ctrl, mode);
+    }
+}
+
+void Engine::launch_aggregate(const double* b, const double2* msg, double* x, double* beta,
+                              unsigned long long* npiv) {
+    if (n == 0) return;
+    const unsigned g = nblk(n);
+    if (layout == BGABP_LAYOUT_DIA) {
+        DIA_SWITCH(S, k_aggregate_dia<SS><<<g, 256, 0, st>>>(dia, b, msg, x, beta, npiv));
+    } else {
+        k_aggregate_csr<<<g, 256, 0, st>>>(csr, b, msg, x, beta, npiv);
+    }
+}
+
+void Engine::launch_residual(const double* b, const double* x, double* r, unsigned long long* rmax, int mode) {
+    if (n == 0) return;
+    const unsigned g = nblk(n);
+    if (layout == BGABP_LAYOUT_DIA) {
+        DIA_SWITCH(S, k_residual_dia<SS><<<g, 256, 0, st>>>(dia, b, x, r, rmax, d_ctrl, mode));
+    } else {
+        k_residual_csr<<<g, 256, 0, st>>>(csr, b, x, r, rmax, d_ctrl, mode);
+    }
+}
+
+void Engine::launch_levels(const Levels& L, const double* b, double2* msg, double* x, bool delta,
+                           unsigned long long* dslot, int mode) {
+    for (size_t l = 0; l + 1 < L.ptr.size(); ++l) {
+        const int cnt = L.ptr[l + 1] - L.ptr[l];
+        const int* nodes = L.d_nodes + L.ptr[l];
+        const int* npos = L.d_npos + L.ptr[l];
+        const unsigned g = nblk(cnt);
+        if (layout == BGABP_LAYOUT_DIA) {
+            DIA_SWITCH(S, if (delta) k_level_dia<SS, true><<<g, 256, 0, st>>>(dia, b, msg, x, nodes, npos, cnt, d_ctrl, dslot, mode);
+                       else k_level_dia<SS, false><<<g, 256, 0, st>>>(dia, b, msg, x, nodes, npos, cnt, d_ctrl, dslot, mode));
+        } else {
+            if (delta)
+                k_level_csr<true><<<g, 256, 0, st>>>(csr, b, msg, x, nodes, npos, cnt, d_ctrl, dslot, mode);
+            else
+                k_level_csr<false><<<g, 256, 0, st>>>(csr, b, msg, x, nodes, npos, cnt, d_ctrl, dslot, mode);
+        }
+    }
+}
+
+void Engine::launch_gs_levels(const Levels& L, const double* b, double* x) {
+    for (size_t l = 0; l + 1 < L.ptr.size(); ++l) {
+        const int cnt = L.ptr[l + 1] - L.ptr[l];
+        const int* nodes = L.d_nodes + L.ptr[l];
+        const int* npos = L.d_npos + L.ptr[l];
+        if (layout == BGABP_LAYOUT_DIA) {
+            DIA_SWITCH(S, k_gs_level_dia<SS><<<nblk(cnt), 256, 0, st>>>(dia, b, x, nodes, npos, cnt, d_ctrl));
+        } else {
+            k_gs_level_csr<<<nblk(cnt), 256, 0, st>>>(csr, b, x, nodes, npos, cnt, d_ctrl);
+        }
+    }
+}
+
+void Engine::launch_jacobi(const double* b, const double* x, double* xn) {
+    if (n == 0) return;
+    if (layout == BGABP_LAYOUT_DIA) {
+        DIA_SWITCH(S, k_jacobi_dia<SS><<<nblk(n), 256, 0, st>>>(dia, b, x, xn, d_ctrl));
+    } else {
+        k_jacobi_csr<<<nblk(n), 256, 0, st>>>(csr, b, x, xn, d_ctrl);
+    }
+}
+
+void Engine::reset_ctrl() {
+    Ctrl c;
+    std::memset(&c, 0, sizeof(c));
+    for (int q = 0; q < 4; ++q) {
+        c.epiv[q] = kNone;
+        c.npiv[q] = kNone;
+    }
+    c.opiv = kNone;
+    ck(cudaMemcpyAsync(d_ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, st), "ctrl reset");
+    ck(cudaStreamSynchronize(st), "ctrl sync");
+}
+
+void Engine::read_ctrl() {
+    ck(cudaMemcpyAsync(h_ctrl, d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st), "ctrl D2H");
+    ck(cudaStreamSynchronize(st), "ctrl sync");
+}
+
+std::string Engine::ordered_detail(const std::vector<int>& order, unsigned long long key) const {
+    const int pos = (int)(key >> 32);
+    const unsigned sub = (unsigned)(key & 0xffffffffu);
+    const int j = order[pos];
+    if (sub == 0) return "zero pivot at node " + std::to_string(j);
+    return "zero pivot on edge " + std::to_string(j) + "->" + std::to_string((int)sub - 1);
+}
+
+// ---------------------------------------------------------------------------------------------
+// one sweep (gabp.cpp:42-47)
+// ---------------------------------------------------------------------------------------------
+int Engine::sweep(const double* b, const bgabp_schedule& s, double* x, std::string& err) {
+    if (s.kind == BGABP_SCHED_FLOOD) {
+        if (n == 0) return BGABP_OK;
+        reset_ctrl();
+        ck(cudaMemcpyAsync(d_b, b, sizeof(double) * n, cudaMemcpyHostToDevice, st), "H2D b");
+        launch_flood(d_b, d_msg[cur], d_msg[cur ^ 1], nullptr, MODE_PLAIN, false);
+        cur ^= 1;
+        launch_aggregate(d_b, d_msg[cur], d_x, nullptr, &d_ctrl->npiv[0]);
+        ck(cudaGetLastError(), "flood launch");
+        read_ctrl();
+        if (h_ctrl->epiv[1] != kNone) {  // edge stage failed: x untouched (gabp.cpp:126-130)
+            const unsigned long long k = h_ctrl->epiv[1];
+            err = "zero pivot on edge " + std::to_string(k >> 32) + "->" + std::to_string(k & 0xffffffffu);
+            return BGABP_EPIVOT;
+        }
+        ck(cudaMemcpyAsync(x, d_x, sizeof(double) * n, cudaMemcpyDeviceToHost, st), "D2H x");
+        ck(cudaStreamSynchronize(st), "sync");
+        if (h_ctrl->npiv[0] != kNone) {
+            err = "zero pivot at node " + std::to_string(h_ctrl->npiv[0]);
+            return BGABP_EPIVOT;
+        }
+        return BGABP_OK;
+    }
+    const Levels& L = levels_for(s);
+    if (n == 0) return BGABP_OK;
+    reset_ctrl();
+    ck(cudaMemcpyAsync(d_b, b, sizeof(double) * n, cudaMemcpyHostToDevice, st), "H2D b");
+    ck(cudaMemcpyAsync(d_x, x, sizeof(double) * n, cudaMemcpyHostToDevice, st), "H2D x");
+    launch_levels(L, d_b, d_msg[cur], d_x, false, nullptr, MODE_PLAIN);
+    ck(cudaGetLastError(), "level launch");
+    ck(cudaMemcpyAsync(x, d_x, sizeof(double) * n, cudaMemcpyDeviceToHost, st), "D2H x");
+    read_ctrl();
+    if (h_ctrl->opiv != kNone) {
+        err = ordered_detail(L.order, h_ctrl->opiv);
+        return BGABP_EPIVOT;
+    }
+    return BGABP_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// solve (gabp.cpp:174-219): device-resident loop, stop logic in k_solve_finalize*
+// ---------------------------------------------------------------------------------------------
+void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bgabp_options& o) {
+    solve_flood = s.kind == BGABP_SCHED_FLOOD;
+    solve_levels = solve_flood ? nullptr : &levels_for(s);
+    solve_b = b_dev;
+    solve_stop = o.stop;
+    solve_max_iter = o.max_iter;
+    if (hist_cap < (long long)std::max(o.max_iter, 0) + 2) {
+        hist_cap = (long long)std::max(o.max_iter, 0) + 2;
+        d_hist = static_cast<double*>(dalloc(sizeof(double) * hist_cap));
+    }
+    Ctrl c;
+    std::memset(&c, 0, sizeof(c));
+    c.tol = o.tol;
+    c.divergence = o.divergence_factor;
+    c.stop = o.stop;
+    c.max_iter = o.max_iter;
+    ck(cudaMemcpyAsync(d_ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, st), "ctrl");
+    for (int k = 0; k < 2; ++k)
+        ck(cudaMemsetAsync(d_msg[k], 0, sizeof(double2) * (size_t)std::max<long long>(nslots, 1), st), "memset");
+    ck(cudaMemsetAsync(d_x, 0, sizeof(double) * std::max(n, 1), st), "memset x");
+    cur = 0;
+    if (n > 0) k_inf_norm<<<std::min<unsigned>(nblk(n), 1184), 256, 0, st>>>(b_dev, n, &d_ctrl->red[0]);
+    k_solve_arm<<<1, 1, 0, st>>>(d_ctrl, d_hist);
+    ck(cudaGetLastError(), "solve arm");
+    steps_enqueued = 0;
+}
+
+void Engine::enqueue_step() {
+    if (solve_flood) {
+        launch_flood(solve_b, d_msg[0], d_msg[1], d_x, MODE_SOLVE, solve_stop == BGABP_STOP_MESSAGE_DELTA);
+        launch_residual(solve_b, d_x, nullptr, nullptr, MODE_SOLVE);
+        k_solve_finalize<<<1, 1, 0, st>>>(d_ctrl, d_hist);
+    } else {
+        launch_levels(*solve_levels, solve_b, d_msg[0], d_x, solve_stop == BGABP_STOP_MESSAGE_DELTA,
+                      &d_ctrl->delta[0], MODE_SOLVE);
+        launch_residual(solve_b, d_x, nullptr, nullptr, MODE_SOLVE_ORDERED);
+        k_solve_finalize_ordered<<<1, 1, 0, st>>>(d_ctrl, d_hist);
+    }
+}
+
+void Engine::solve_steps(int nsteps) {
+    if (nsteps <= 0) return;
+    // graph-replay chunks of iterations: the kernels read their step index from the device,
+    // so one captured chunk is valid for any position in the loop
+    const size_t per_step = solve_flood ? 3 : solve_levels->ptr.size() + 1;
+    const bool use_graph = per_step * 16 <= 4096 && n > 0;
+    int left = nsteps;
+    while (left > 0) {
+        const int chunk = use_graph ? std::min(left, 16) : left;
+        if (use_graph && chunk == 16) {
+            const std::string key = std::string(solve_flood ? "f" : "o") + std::to_string(solve_stop) + ":" +
+                                    std::to_string((long long)(uintptr_t)solve_b) + ":" +
+                                    std::to_string((long long)(uintptr_t)solve_levels);
+            auto it = graphs.find(key);
+            if (it == graphs.end()) {
+                cudaGraph_t g;
+                ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture");
+                for (int k = 0; k < 16; ++k) enqueue_step();
+                ck(cudaStreamEndCapture(st, &g), "capture end");
+                cudaGraphExec_t ge;
+                ck(cudaGraphInstantiate(&ge, g, 0), "graph instantiate");
+                cudaGraphDestroy(g);
+                it = graphs.emplace(key, ge).first;
+            }
+            ck(cudaGraphLaunch(it->second, st), "graph launch");
+        } else {
+            for (int k = 0; k < chunk; ++k) enqueue_step();
+        }
+        left -= chunk;
+        steps_enqueued += chunk;
+    }
+    ck(cudaGetLastError(), "solve steps");
+}
+
+bool Engine::solve_done() {
+    read_ctrl();
+    return h_ctrl->done != 0;
+}
+
+void Engine::solve_run_to_end() {
+    // enqueue growing chunks until the device has decided (at most max_iter + 1 iterations)
+    int chunk = 16;
+    while (!solve_done()) {
+        const long long cap = (long long)solve_max_iter + 1 - steps_enqueued;
+        if (cap <= 0) throw CudaError("solve loop did not terminate");
+        solve_steps((int)std::min<long long>(chunk, cap));
+        chunk = std::min(chunk * 2, 512);
+    }
+}
+
+void Engine::solve_report(bgabp_report& rep, std::string& detail) {
+    read_ctrl();
+    const Ctrl& c = *h_ctrl;
+    rep.status = c.status;
+    rep.iterations = c.iterations;
+    detail.clear();
+    bool pivot = false;
+    if (c.status == BGABP_DIVERGED) {
+        switch (c.detail_kind) {
+            case 1: detail = "zero pivot at node " + std::to_string(c.detail_key); pivot = true; break;
+            case 2:
+                detail = "zero pivot on edge " + std::to_string(c.detail_key >> 32) + "->" +
+                         std::to_string(c.detail_key & 0xffffffffu);
+                pivot = true;
+                break;
+            case 3: detail = "residual blowup"; break;
+            case 4: detail = ordered_detail(solve_levels->order, c.detail_key); pivot = true; break;
+        }
+    }
+    const double per_iter = sweep_flops() + 2.0 * (double)nnz;  // gabp.cpp:200-202
+    rep.flop_estimate = 0.0;
+    for (int k = 0; k < c.iterations - (pivot ? 1 : 0); ++k) rep.flop_estimate += per_iter;
+}
+
+double Engine::sweep_flops() const {  // gabp.cpp:165-172
+    const double e = (double)num_edges;
+    return n + 3.0 * e + 4.0 * e;
+}
+
+// ---------------------------------------------------------------------------------------------
+// frozen-precision path (gabp.cpp:221-401)
+// ---------------------------------------------------------------------------------------------
+void Engine::ensure_frozen_buffers() {
+    if (d_lam) return;
+    const size_t sb = sizeof(double) * (size_t)std::max<long long>(nslots, 1);
+    d_lam = static_cast<double*>(dalloc(sb));
+    d_lsrc = static_cast<double*>(dalloc(sb));
+    d_sigma = static_cast<double*>(dalloc(sizeof(double) * std::max(n, 1)));
+}
+
+void Engine::frozen_finish() {  // sigma and the source-major lambda copy from d_lam
+    if (n == 0) return;
+    const unsigned g = nblk(n);
+    if (layout == BGABP_LAYOUT_DIA) {
+        DIA_SWITCH(S, k_sigma_dia<SS><<<g, 256, 0, st>>>(dia, d_lam, d_sigma);
+                   k_lambda_by_source_dia<SS><<<g, 256, 0, st>>>(dia, d_lam, d_lsrc));
+    } else {
+        k_sigma_csr<<<g, 256, 0, st>>>(csr, d_lam, d_sigma);
+        k_lambda_by_source_csr<<<g, 256, 0, st>>>(csr, d_lam, d_lsrc);
+    }
+    has_frozen = true;
+}
+
+void Engine::precompute_lambda(const bgabp_schedule& s, double tol, int max_iter, int& converged, int& iters) {
+    const bool flood = s.kind == BGABP_SCHED_FLOOD;
+    const Levels* L = flood ? nullptr : &levels_for(s);
+    ensure_frozen_buffers();
+    const size_t sb = sizeof(double) * (size_t)std::max<long long>(nslots, 1);
+    double* lb[2] = {d_lam, reinterpret_cast<double*>(d_msg[0])};  // flood ping-pong scratch
+    ck(cudaMemsetAsync(lb[0], 0, sb, st), "memset");
+    ck(cudaMemsetAsync(lb[1], 0, sb, st), "memset");
+    converged = 0;
+    iters = 0;
+    int curb = 0;
+    const unsigned g = nblk(n);
+    for (int it = 1; it <= max_iter; ++it) {
+        reset_ctrl();
+        unsigned long long* ds = &d_ctrl->red[1];
+        if (n > 0) {
+            if (flood) {
+                if (layout == BGABP_LAYOUT_DIA) {
+                    DIA_SWITCH(S, k_lambda_flood_dia<SS><<<g, 256, 0, st>>>(dia, lb[curb], lb[curb ^ 1], d_ctrl, ds));
+                } else {
+                    k_lambda_flood_csr<<<g, 256, 0, st>>>(csr, lb[curb], lb[curb ^ 1], d_ctrl, ds);
+                }
+                curb ^= 1;
+            } else {
+                for (size_t l = 0; l + 1 < L->ptr.size(); ++l) {
+                    const int cnt = L->ptr[l + 1] - L->ptr[l];
+                    const int* nodes = L->d_nodes + L->ptr[l];
+                    if (layout == BGABP_LAYOUT_DIA) {
+                        DIA_SWITCH(S, k_lambda_level_dia<SS><<<nblk(cnt), 256, 0, st>>>(dia, lb[0], nodes, cnt, d_ctrl, ds));
+                    } else {
+                        k_lambda_level_csr<<<nblk(cnt), 256, 0, st>>>(csr, lb[0], nodes, cnt, d_ctrl, ds);
+                    }
+                }
+            }
+        }
+        ck(cudaGetLastError(), "lambda sweep");
+        read_ctrl();
+        iters = it;
+        if (h_ctrl->opiv != kNone) {  // breakdown: not converged, no sigma (gabp.cpp:238-243)
+            if (curb) ck(cudaMemcpyAsync(d_lam, lb[1], sb, cudaMemcpyDeviceToDevice, st), "copy");
+            ck(cudaMemsetAsync(d_sigma, 0, sizeof(double) * std::max(n, 1), st), "memset");
+            converged = 0;
+            has_frozen = false;
+            cudaMemsetAsync(d_msg[0], 0, sb, st);
+            return;
+        }
+        const double delta = bits2d(h_ctrl->red[1]);
+        if (delta <= tol) {
+            converged = 1;
+            break;
+        }
+        if (!std::isfinite(delta)) break;
+    }
+    if (curb) ck(cudaMemcpyAsync(d_lam, lb[1], sb, cudaMemcpyDeviceToDevice, st), "copy");
+    ck(cudaMemsetAsync(d_msg[0], 0, sizeof(double2) * (size_t)std::max<long long>(nslots, 1), st), "memset");
+    frozen_finish();
+    ck(cudaStreamSynchronize(st), "sync");
+}
+
+void Engine::correction_sweeps_dev(const double* r_dev, const bgabp_schedule& s, int sweeps, double* e_dev) {
+    // mean-only sweeps (gabp.cpp:289-325), cold messages, frozen lambda/sigma on the device
+    const bool flood = s.kind == BGABP_SCHED_FLOOD;
+    const Levels* L = flood ? nullptr : &levels_for(s);
+    const size_t sb = sizeof(double) * (size_t)std::max<long long>(nslots, 1);
+    double* mb[2] = {reinterpret_cast<double*>(d_msg[0]), reinterpret_cast<double*>(d_msg[1])};
+    ck(cudaMemsetAsync(mb[0], 0, sb, st), "memset");
+    ck(cudaMemsetAsync(e_dev, 0, sizeof(double) * std::max(n, 1), st), "memset");
+    if (n == 0) return;
+    const unsigned g = nblk(n);
+    int curb = 0;
+    for (int k = 0; k < sweeps; ++k) {
+        if (flood) {
+            if (layout == BGABP_LAYOUT_DIA) {
+                DIA_SWITCH(S, k_corr_flood_dia<SS><<<g, 256, 0, st>>>(dia, r_dev, d_lsrc, mb[curb], mb[curb ^ 1]));
+            } else {
+                k_corr_flood_csr<<<g, 256, 0, st>>>(csr, r_dev, d_lsrc, mb[curb], mb[curb ^ 1]);
+            }
+            curb ^= 1;
+        } else {
+            for (size_t l = 0; l + 1 < L->ptr.size(); ++l) {
+                const int cnt = L->ptr[l + 1] - L->ptr[l];
+                const int* nodes = L->d_nodes + L->ptr[l];
+                if (layout == BGABP_LAYOUT_DIA) {
+                    DIA_SWITCH(S, k_corr_level_dia<SS><<<nblk(cnt), 256, 0, st>>>(dia, r_dev, d_lsrc, d_sigma, mb[0], e_dev, nodes, cnt));
+                } else {
+                    k_corr_level_csr<<<nblk(cnt), 256, 0, st>>>(csr, r_dev, d_lsrc, d_sigma, mb[0], e_dev, nodes, cnt);
+                }
+            }
+        }
+    }
+    if (flood) {
+        if (layout == BGABP_LAYOUT_DIA) {
+            DIA_SWITCH(S, k_corr_final_dia<SS><<<g, 256, 0, st>>>(dia, r_dev, d_sigma, mb[curb], e_dev));
+        } else {
+            k_corr_final_csr<<<g, 256, 0, st>>>(csr, r_dev, d_sigma, mb[curb], e_dev);
+        }
+    }
+    ck(cudaGetLastError(), "correction sweeps");
+}
+
+// cold sweeps on A e = r from zero messages (gabp.cpp:343-361, multigrid.cpp:180-187).  Failures
+// are promoted on the device (k_plain_check) so a multigrid cycle never synchronises; with
+// check=true the call synchronises and returns BGABP_EPIVOT with the reference's message.
+int Engine::cold_sweeps_dev(const double* r_dev, const bgabp_schedule& s, int sweeps, double* e_dev,
+                            std::string& err, bool check, int seq) {
+    const bool flood = s.kind == BGABP_SCHED_FLOOD;
+    const Levels* L = flood ? nullptr : &levels_for(s);
+    if (check) reset_ctrl();
+    k_plain_reset<<<1, 1, 0, st>>>(d_ctrl);
+    for (int k = 0; k < 2; ++k)
+        ck(cudaMemsetAsync(d_msg[k], 0, sizeof(double2) * (size_t)std::max<long long>(nslots, 1), st), "memset");
+    ck(cudaMemsetAsync(e_dev, 0, sizeof(double) * std::max(n, 1), st), "memset");
+    cur = 0;
+    if (n == 0 || sweeps <= 0) return BGABP_OK;
+    if (flood) {
+        for (int k = 0; k < sweeps; ++k) {
+            launch_flood(r_dev, d_msg[cur], d_msg[cur ^ 1], nullptr, k == 0 ? MODE_PLAIN : MODE_PLAIN_X, false);
+            cur ^= 1;
+            k_plain_check<<<1, 1, 0, st>>>(d_ctrl, seq, 4);
+        }
+        launch_aggregate(r_dev, d_msg[cur], e_dev, nullptr, &d_ctrl->npiv[0]);
+    } else {
+        for (int k = 0; k < sweeps; ++k) launch_levels(*L, r_dev, d_msg[cur], e_dev, false, nullptr, MODE_PLAIN);
+    }
+    k_plain_check<<<1, 1, 0, st>>>(d_ctrl, seq, 4);
+    ck(cudaGetLastError(), "cold sweeps");
+    if (!check) return BGABP_OK;
+    read_ctrl();
+    if (h_ctrl->halt) {
+        err = decode_failure(*h_ctrl, L ? &L->order : nullptr);
+        return BGABP_EPIVOT;
+    }
+    return BGABP_OK;
+}
+
+// sweeps_expand (multigrid.cpp:54-70): 30 cold sweeps on r = 1; expand if any sweep breaks down,
+// if max|m| is non-finite after any sweep, or if it grows more than 6.19x from sweep 20 to 30.
+bool Engine::sweeps_expand(const bgabp_schedule& s) {
+    if (n == 0) return false;
+    const bool flood = s.kind == BGABP_SCHED_FLOOD;
+    const Levels* L = flood ? nullptr : &levels_for(s);
+    unsigned long long* d_norms = static_cast<unsigned long long*>(dalloc(sizeof(unsigned long long) * 32));
+    ck(cudaMemsetAsync(d_norms, 0, sizeof(unsigned long long) * 32, st), "memset");
+    std::vector<double> ones(n, 1.0);
+    double* d_ones = upload(ones);
+    reset_ctrl();
+    for (int k = 0; k < 2; ++k)
+        ck(cudaMemsetAsync(d_msg[k], 0, sizeof(double2) * (size_t)std::max<long long>(nslots, 1), st), "memset");
+    ck(cudaMemsetAsync(d_e, 0, sizeof(double) * n, st), "memset");
+    cur = 0;
+    const unsigned gr = std::min<unsigned>(nblk(nslots), 1184);
+    for (int k = 0; k < 30; ++k) {
+        if (flood) {
+            launch_flood(d_ones, d_msg[cur], d_msg[cur ^ 1], nullptr, k == 0 ? MODE_PLAIN : MODE_PLAIN_X, false);
+            cur ^= 1;
+        } else {
+            launch_levels(*L, d_ones, d_msg[cur], d_e, false, nullptr, MODE_PLAIN);
+        }
+        k_plain_check<<<1, 1, 0, st>>>(d_ctrl, k, 4);
+        if (flood) {  // the x-stage of this sweep belongs to this sweep (gabp.cpp:141-160)
+            launch_aggregate(d_ones, d_msg[cur], d_e, nullptr, &d_ctrl->npiv[0]);
+            k_plain_check<<<1, 1, 0, st>>>(d_ctrl, k, 4);
+        }
+        k_max_abs_m<<<gr, 256, 0, st>>>(d_msg[cur], nslots, d_norms + k);
+    }
+    ck(cudaGetLastError(), "probe");
+    unsigned long long hn[32];
+    ck(cudaMemcpyAsync(hn, d_norms, sizeof(hn), cudaMemcpyDeviceToHost, st), "D2H");
+    read_ctrl();
+    for (int k = 0; k < 2; ++k)
+        ck(cudaMemsetAsync(d_msg[k], 0, sizeof(double2) * (size_t)std::max<long long>(nslots, 1), st), "memset");
+    ck(cudaStreamSynchronize(st), "sync");
+    if (h_ctrl->halt) return true;
+    for (int k = 0; k < 30; ++k)
+        if (!std::isfinite(bits2d(hn[k]))) return true;
+    const double mid = bits2d(hn[19]), end = bits2d(hn[29]);
+    return mid > 0.0 && end > 6.19 * mid;
+}
+
+std::string Engine::decode_failure(const Ctrl& c, const std::vector<int>* order) const {
+    switch (c.detail_kind) {
+        case 1: return "zero pivot at node " + std::to_string(c.detail_key);
+        case 2:
+            return "zero pivot on edge " + std::to_string(c.detail_key >> 32) + "->" +
+                   std::to_string(c.detail_key & 0xffffffffu);
+        case 3: return "residual blowup";
+        case 4: return order ? ordered_detail(*order, c.detail_key) : "zero pivot";
+        case 5: {  // relax: gs_pass / jacobi_pass (classic.cpp:27,43)
+            const int pos = (int)(c.detail_key >> 32);
+            return "relax: zero diagonal at " + std::to_string(order ? (*order)[pos] : pos);
+        }
+    }
+    return "breakdown";
+}
+
+}  // namespace bgabp
+
+// =============================================================================================
+// C-ABI
+// =============================================================================================
+using namespace bgabp;
+
+struct bgabp_engine {
+    Engine E;
+};
+
+#define ABI_GUARD(ERRBUF, ERRLEN, ...)                           \
+    try {                                                        \
+        __VA_ARGS__                                              \
+    } catch (const InvalidArg& ex) {                             \
+        put_err(ERRBUF, ERRLEN, ex.what());                      \
+        return BGABP_EINVAL;                                     \
+    } catch (const CudaError& ex) {                              \
+        put_err(ERRBUF, ERRLEN, ex.what());                      \
+        return BGABP_ECUDA;                                      \
+    } catch (const std::exception& ex) {                         \
+        put_err(ERRBUF, ERRLEN, ex.what());                      \
+        return BGABP_ERUNTIME;                                   \
+    }
+
+extern "C" {
+
+const char* bgabp_version(void) { return kVersion; }
+
+int bgabp_create(int n, const int* row_offsets, const int* col_indices, const double* values, int layout,
+                 bgabp_engine** out, char* err, size_t errlen) {
+    *out = nullptr;
+    auto h = std::make_unique<bgabp_engine>();
+    ABI_GUARD(err, errlen, {
+        h->E.build(n, row_offsets, col_indices, values, layout);
+        *out = h.release();
+        return BGABP_OK;
+    })
+}
+
+void bgabp_destroy(bgabp_engine* e) { delete e; }
+
+int bgabp_get_info(const bgabp_engine* h, bgabp_info* info) {
+    const Engine& E = h->E;
+    info->n = E.n;
+    info->nnz = E.nnz;
+    info->num_edges = E.num_edges;
+    info->layout = E.layout;
+    info->num_slots = E.S;
+    info->symmetric_values = E.symmetric ? 1 : 0;
+    info->bytes_per_sweep = 40.0 * (double)E.num_edges + 24.0 * E.n;
+    info->bytes_per_residual = 8.0 * (double)E.nnz + 16.0 * E.n;
+    info->device_bytes = E.device_bytes;
+    return BGABP_OK;
+}
+
+void* bgabp_stream(bgabp_engine* h) { return (void*)h->E.st; }
+
+int bgabp_reset_state(bgabp_engine* h) {
+    ABI_GUARD(nullptr, 0, {
+        Engine& E = h->E;
+        for (int k = 0; k < 2; ++k)
+            ck(cudaMemsetAsync(E.d_msg[k], 0, sizeof(double2) * (size_t)std::max<long long>(E.nslots, 1), E.st), "memset");
+        ck(cudaStreamSynchronize(E.st), "sync");
+        return BGABP_OK;
+    })
+}
+
+int bgabp_set_state(bgabp_engine* h, const double* lam, const double* m) {
+    ABI_GUARD(nullptr, 0, {
+        Engine& E = h->E;
+        if (E.nnz == 0) return BGABP_OK;
+        double *dl = nullptr, *dm = nullptr;
+        ck(cudaMallocAsync((void**)&dl, sizeof(double) * E.nnz, E.st), "malloc");
+        ck(cudaMallocAsync((void**)&dm, sizeof(double) * E.nnz, E.st), "malloc");
+        ck(cudaMemcpyAsync(dl, lam, sizeof(double) * E.nnz, cudaMemcpyHostToDevice, E.st), "H2D");
+        ck(cudaMemcpyAsync(dm, m, sizeof(double) * E.nnz, cudaMemcpyHostToDevice, E.st), "H2D");
+        ck(cudaMemsetAsync(E.d_msg[E.cur], 0, sizeof(double2) * (size_t)E.nslots, E.st), "memset");
+        k_state_scatter<<<nblk(E.nnz), 256, 0, E.st>>>(E.d_msg[E.cur], E.d_csr2slot, E.nnz, dl, dm);
+        ck(cudaFreeAsync(dl, E.st), "free");
+        ck(cudaFreeAsync(dm, E.st), "free");
+        ck(cudaStreamSynchronize(E.st), "sync");
+        return BGABP_OK;
+    })
+}
+
+int bgabp_get_state(bgabp_engine* h, double* lam, double* m) {
+    ABI_GUARD(nullptr, 0, {
+        Engine& E = h->E;
+        if (E.nnz == 0) return BGABP_OK;
+        double *dl = nullptr, *dm = nullptr;
+        ck(cudaMallocAsync((void**)&dl, sizeof(double) * E.nnz, E.st), "malloc");
+        ck(cudaMallocAsync((void**)&dm, sizeof(double) * E.nnz, E.st), "malloc");
+        k_state_gather<<<nblk(E.nnz), 256, 0, E.st>>>(E.d_msg[E.cur], E.d_csr2slot, E.nnz, dl, dm);
+        ck(cudaMemcpyAsync(lam, dl, sizeof(double) * E.nnz, cudaMemcpyDeviceToHost, E.st), "D2H");
+        ck(cudaMemcpyAsync(m, dm, sizeof(double) * E.nnz, cudaMemcpyDeviceToHost, E.st), "D2H");
+        ck(cudaFreeAsync(dl, E.st), "free");
+        ck(cudaFreeAsync(dm, E.st), "free");
+        ck(cudaStreamSynchronize(E.st), "sync");
+        return BGABP_OK;
+    })
+}
+
+int bgabp_sweep(bgabp_engine* h, const double* b, const bgabp_schedule* s, double* x, char* err, size_t errlen) {
+    ABI_GUARD(err, errlen, {
+        std::string msg;
+        int rc = h->E.sweep(b, *s, x, msg);
+        if (rc != BGABP_OK) put_err(err, errlen, msg);
+        return rc;
+    })
+}
+
+int bgabp_node_precisions(bgabp_engine* h, double* beta) {
+    ABI_GUARD(nullptr, 0, {
+        Engine& E = h->E;
+        if (E.n == 0) return BGABP_OK;
+        E.launch_aggregate(nullptr, E.d_msg[E.cur], nullptr, E.d_aux, nullptr);
+        ck(cudaMemcpyAsync(beta, E.d_aux, sizeof(double) * E.n, cudaMemcpyDeviceToHost, E.st), "D2H");
+        ck(cudaStreamSynchronize(E.st), "sync");
+        return BGABP_OK;
+    })
+}
+
+double bgabp_sweep_flops(const bgabp_engine* h) { return h->E.sweep_flops(); }
+
+int bgabp_solve(bgabp_engine* h, const double* b, const bgabp_schedule* s, const bgabp_options* opt,
+                bgabp_report* rep, double* x_out, double* history, char* detail, size_t dl) {
+    ABI_GUARD(detail, dl, {
+        Engine& E = h->E;
+        E.schedule_order_check(*s);
+        if (E.n > 0) ck(cudaMemcpyAsync(E.d_b, b, sizeof(double) * E.n, cudaMemcpyHostToDevice, E.st), "H2D b");
+        E.solve_begin(E.d_b, *s, *opt);
+        E.solve_run_to_end();
+        std::string d;
+        E.solve_report(*rep, d);
+        if (x_out && E.n > 0)
+            ck(cudaMemcpyAsync(x_out, E.d_x, sizeof(double) * E.n, cudaMemcpyDeviceToHost, E.st), "D2H x");
+        if (history)
+            ck(cudaMemcpyAsync(history, E.d_hist, sizeof(double) * (rep->iterations + 1), cudaMemcpyDeviceToHost, E.st),
+               "D2H hist");
+        ck(cudaStreamSynchronize(E.st), "sync");
+        put_err(detail, dl, d);
+        return BGABP_OK;
+    })
+}
+
+int bgabp_solve_device_begin(bgabp_engine* h, const double* b_dev, const bgabp_schedule* s, const bgabp_options* opt) {
+    ABI_GUARD(nullptr, 0, {
+        h->E.schedule_order_check(*s);
+        h->E.solve_begin(b_dev, *s, *opt);
+        return BGABP_OK;
+    })
+}
+
+int bgabp_solve_device_steps(bgabp_engine* h, int nsteps) {
+    ABI_GUARD(nullptr, 0, {
+        h->E.solve_steps(nsteps);
+        return BGABP_OK;
+    })
+}
+
+int bgabp_solve_device_end(bgabp_engine* h, bgabp_report* rep, double* x_dev, double* history_dev, char* detail,
+                           size_t dl) {
+    ABI_GUARD(detail, dl, {
+        Engine& E = h->E;
+        std::string d;
+        E.solve_report(*rep, d);
+        if (x_dev && E.n > 0)
+            ck(cudaMemcpyAsync(x_dev, E.d_x, sizeof(double) * E.n, cudaMemcpyDeviceToDevice, E.st), "D2D x");
+        if (history_dev)
+            ck(cudaMemcpyAsync(history_dev, E.d_hist, sizeof(double) * (rep->iterations + 1), cudaMemcpyDeviceToDevice,
+                               E.st),
+               "D2D hist");
+        ck(cudaStreamSynchronize(E.st), "sync");
+        put_err(detail, dl, d);
+        return BGABP_OK;
+    })
+}
+
+int bgabp_flood_sweeps_device(bgabp_engine* h, const double* b_dev, int nsweeps) {
+    ABI_GUARD(nullptr, 0, {
+        Engine& E = h->E;
+        for (int k = 0; k < nsweeps; ++k) {
+            E.launch_flood(b_dev, E.d_msg[E.cur], E.d_msg[E.cur ^ 1], nullptr, MODE_PLAIN, false);
+            E.cur ^= 1;
+        }
+        ck(cudaGetLastError(), "flood sweeps");
+        return BGABP_OK;
+    })
+}
+
+int bgabp_residual_inf_norm(bgabp_engine* h, const double* x, const double* b, double* out) {
+    ABI_GUARD(nullptr, 0, {
+        Engine& E = h->E;
+        *out = 0.0;
+        if (E.n == 0) return BGABP_OK;
+        E.reset_ctrl();
+        ck(cudaMemcpyAsync(E.d_b, b, sizeof(double) * E.n, cudaMemcpyHostToDevice, E.st), "H2D");
+        ck(cudaMemcpyAsync(E.d_aux, x, sizeof(double) * E.n, cudaMemcpyHostToDevice, E.st), "H2D");
+        E.launch_residual(E.d_b, E.d_aux, nullptr, &E.d_ctrl->red[2], MODE_PLAIN);
+        E.read_ctrl();
+        *out = bits2d(E.h_ctrl->red[2]);
+        return BGABP_OK;
+    })
+}
+
+int bgabp_precompute_lambda(bgabp_engine* h, const bgabp_schedule* s, double tol, int max_iter, double* lam_out,
+                            double* sigma_out, int* converged, int* iterations) {
+    ABI_GUARD(nullptr, 0, {
+        Engine& E = h->E;
+        int cv = 0, it = 0;
+        E.precompute_lambda(*s, tol, max_iter, cv, it);
+        if (converged) *converged = cv;
+        if (iterations) *iterations = it;
+        if (lam_out && E.nnz > 0) {
+            double* dl = nullptr;
+            ck(cudaMallocAsync((void**)&dl, sizeof(double) * E.nnz, E.st), "malloc");
+            k_lambda_gather<<<nblk(E.nnz), 256, 0, E.st>>>(E.d_lam, E.d_csr2slot, E.nnz, dl);
+            ck(cudaMemcpyAsync(lam_out, dl, sizeof(double) * E.nnz, cudaMemcpyDeviceToHost, E.st), "D2H");
+            ck(cudaFreeAsync(dl, E.st), "free");
+        }
+        if (sigma_out && E.n > 0)
+            ck(cudaMemcpyAsync(sigma_out, E.d_sigma, sizeof(double) * E.n, cudaMemcpyDeviceToHost, E.st), "D2H");
+        ck(cudaStreamSynchronize(E.st), "sync");
+        return BGABP_OK;
+    })
+}
+
+int bgabp_set_frozen(bgabp_engine* h, const double* lam, const double* sigma) {
+    ABI_GUARD(nullptr, 0, {
+        Engine& E = h->E;
+        E.ensure_frozen_buffers();
+        ck(cudaMemsetAsync(E.d_lam, 0, sizeof(double) * (size_t)std::max<long long>(E.nslots, 1), E.st), "memset");
+        if (E.nnz > 0) {
+            double* dl = nullptr;
+            ck(cudaMallocAsync((void**)&dl, sizeof(double) * E.nnz, E.st), "malloc");
+            ck(cudaMemcpyAsync(dl, lam, sizeof(double) * E.nnz, cudaMemcpyHostToDevice, E.st), "H2D");
+            k_lambda_scatter<<<nblk(E.nnz), 256, 0, E.st>>>(E.d_lam, E.d_csr2slot, E.nnz, dl);
+            ck(cudaFreeAsync(dl, E.st), "free");
+        }
+        E.frozen_finish();
+        if (E.n > 0)  // the caller's sigma wins over the recomputed one (FrozenLambda carries both)
+            ck(cudaMemcpyAsync(E.d_sigma, sigma, sizeof(double) * E.n, cudaMemcpyHostToDevice, E.st), "H2D");
+        ck(cudaStreamSynchronize(E.st), "sync");
+        return BGABP_OK;
+    })
+}
+
+int bgabp_correction_sweeps(bgabp_engine* h, const double* r, const bgabp_schedule* s, int sweeps, double* e_out) {
+    ABI_GUARD(nullptr, 0, {
+        Engine& E = h->E;
+        E.schedule_order_check(*s);
+        if (!E.has_frozen) throw InvalidArg("gabp: no frozen precisions (call precompute_lambda or set_frozen)");
+        if (E.n == 0) return BGABP_OK;
+        ck(cudaMemcpyAsync(E.d_r, r, sizeof(double) * E.n, cudaMemcpyHostToDevice, E.st), "H2D");
+        E.correction_sweeps_dev(E.d_r, *s, sweeps, E.d_e);
+        ck(cudaMemcpyAsync(e_out, E.d_e, sizeof(double) * E.n, cudaMemcpyDeviceToHost, E.st), "D2H");
+        ck(cudaStreamSynchronize(E.st), "sync");
+        return BGABP_OK;
+    })
+}
+
+int bgabp_error_correction_apply(bgabp_engine* h, const double* b, const double* x0, int sweeps,
+                                 const bgabp_schedule* s, int use_frozen, double* x_out, char* err, size_t errlen) {
+    ABI_GUARD(err, errlen, {
+        Engine& E = h->E;
+        E.schedule_order_check(*s);
+        if (use_frozen && !E.has_frozen) throw InvalidArg("gabp: no frozen precisions");
+        if (E.n == 0) return BGABP_OK;
+        ck(cudaMemcpyAsync(E.d_b, b, sizeof(double) * E.n, cudaMemcpyHostToDevice, E.st), "H2D");
+        ck(cudaMemcpyAsync(E.d_aux, x0, sizeof(double) * E.n, cudaMemcpyHostToDevice, E.st), "H2D");
+        E.launch_residual(E.d_b, E.d_aux, E.d_r, nullptr, MODE_PLAIN);  // gabp.cpp:327-335
+        if (use_frozen) {
+            E.correction_sweeps_dev(E.d_r, *s, sweeps, E.d_e);
+        } else {
+            std::string msg;
+            if (E.cold_sweeps_dev(E.d_r, *s, sweeps, E.d_e, msg, true) != BGABP_OK)
+                throw std::runtime_error("gabp error correction: " + msg);
+        }
+        k_axpy1<<<nblk(E.n), 256, 0, E.st>>>(E.d_aux, E.d_e, E.n);
+        ck(cudaMemcpyAsync(x_out, E.d_aux, sizeof(double) * E.n, cudaMemcpyDeviceToHost, E.st), "D2H");
+        ck(cudaStreamSynchronize(E.st), "sync");
+        return BGABP_OK;
+    })
+}
+
+// gabp.cpp:363-401; the outer loop stays on the host (one residual read per iteration)
+int bgabp_solve_error_correction(bgabp_engine* h, const double* b, const bgabp_schedule* s, int sweeps,
+                                 const bgabp_options* o, bgabp_report* rep, double* x_out, double* history,
+                                 char* detail, size_t dl) {
+    ABI_GUARD(detail, dl, {
+        Engine& E = h->E;
+        E.schedule_order_check(*s);
+        if (!E.has_frozen) throw InvalidArg("gabp: no frozen precisions");
+        std::vector<double> hist;
+        double r0 = 0.0;
+        for (int i = 0; i < E.n; ++i) r0 = std::max(r0, std::abs(b[i]));
+        hist.push_back(r0);
+        rep->status = BGABP_MAX_ITER;
+        rep->iterations = 0;
+        rep->flop_estimate = 0.0;
+        std::string d;
+        if (E.n > 0) {
+            ck(cudaMemcpyAsync(E.d_b, b, sizeof(double) * E.n, cudaMemcpyHostToDevice, E.st), "H2D");
+            ck(cudaMemsetAsync(E.d_aux, 0, sizeof(double) * E.n, E.st), "memset");
+        }
+        const double ee = (double)E.num_edges;
+        const double per_iter = 2.0 * (double)E.nnz + sweeps * (E.n + 1.0 * ee + 3.0 * ee);
+        if (r0 <= o->tol) {
+            rep->status = BGABP_CONVERGED;
+        } else {
+            for (int it = 1; it <= o->max_iter; ++it) {
+                E.reset_ctrl();
+                E.launch_residual(E.d_b, E.d_aux, E.d_r, nullptr, MODE_PLAIN);
+                E.correction_sweeps_dev(E.d_r, *s, sweeps, E.d_e);
+                k_axpy1<<<nblk(E.n), 256, 0, E.st>>>(E.d_aux, E.d_e, E.n);
+                E.launch_residual(E.d_b, E.d_aux, nullptr, &E.d_ctrl->red[2], MODE_PLAIN);
+                E.read_ctrl();
+                const double r = bits2d(E.h_ctrl->red[2]);
+                hist.push_back(r);
+                rep->iterations = it;
+                rep->flop_estimate += per_iter + 2.0 * (double)E.nnz;
+                if (!std::isfinite(r) || r > o->divergence_factor * r0) {
+                    rep->status = BGABP_DIVERGED;
+                    d = "residual blowup";
+                    break;
+                }
+                if (r <= o->tol) {
+                    rep->status = BGABP_CONVERGED;
+                    break;
+                }
+            }
+        }
+        if (x_out && E.n > 0)
+            ck(cudaMemcpyAsync(x_out, E.d_aux, sizeof(double) * E.n, cudaMemcpyDeviceToHost, E.st), "D2H");
+        ck(cudaStreamSynchronize(E.st), "sync");
+        if (history) std::memcpy(history, hist.data(), sizeof(double) * hist.size());
+        put_err(detail, dl, d);
+        return BGABP_OK;
+    })
+}
+
+}  // extern "C"

@@ -1,0 +1,130 @@
+// Internal host-side declarations of the B200 GaBP engine (not part of the C-ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/gabp_b200.h"
+#include "kernels.cuh"
+
+namespace bgabp {
+
+struct InvalidArg : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void put_err(char* err, size_t len, const std::string& s);
+void ck(cudaError_t e, const char* what);
+
+inline double bits2d(unsigned long long b) {
+    double d;
+    std::memcpy(&d, &b, sizeof d);
+    return d;
+}
+
+// dependency levels of one schedule's visit order (see k_level_dia)
+struct Levels {
+    std::vector<int> ptr;    // level l = nodes[ptr[l] .. ptr[l+1])
+    std::vector<int> order;  // the schedule's visit order (for pivot messages)
+    int* d_nodes = nullptr;
+    int* d_npos = nullptr;   // position of each node in `order`
+};
+
+struct Engine {
+    // matrix (host copy, canonical CSR) and message graph facts
+    int n = 0;
+    long long nnz = 0, num_edges = 0;
+    std::vector<int> ro, ci;
+    std::vector<double> val;
+    std::vector<long long> tpos;
+    bool symmetric = false;
+    std::vector<int> uptr, unbr;  // union neighbour lists
+    int layout = BGABP_LAYOUT_DIA, S = 0;
+    long long nslots = 0;
+    DiaP dia{};
+    CsrP csr{};
+    std::vector<long long> csr2slot;
+
+    // device state
+    cudaStream_t st = nullptr;
+    bool own_stream = true;
+    Ctrl* d_ctrl = nullptr;
+    Ctrl* h_ctrl = nullptr;
+    long long* d_csr2slot = nullptr;
+    double2* d_msg[2] = {nullptr, nullptr};
+    int cur = 0;
+    double *d_b = nullptr, *d_x = nullptr, *d_r = nullptr, *d_e = nullptr, *d_aux = nullptr;
+    double* d_hist = nullptr;
+    long long hist_cap = 0;
+    double *d_lam = nullptr, *d_lsrc = nullptr, *d_sigma = nullptr;
+    bool has_frozen = false;
+    std::vector<void*> allocs;
+    long long device_bytes = 0;
+    std::map<std::string, std::unique_ptr<Levels>> level_cache;
+    std::map<std::string, cudaGraphExec_t> graphs;
+
+    // device-resident solve loop
+    bool solve_flood = true;
+    const Levels* solve_levels = nullptr;
+    const double* solve_b = nullptr;
+    int solve_stop = 0, solve_max_iter = 0;
+    long long steps_enqueued = 0;
+
+    ~Engine();
+    void* dalloc(size_t bytes);
+    template <class T>
+    T* upload(const std::vector<T>& v);
+
+    void build(int n, const int* ro, const int* ci, const double* v, int layout,
+               cudaStream_t shared_stream = nullptr);
+    std::vector<int> schedule_order(const bgabp_schedule& s) const;
+    void schedule_order_check(const bgabp_schedule& s) const {
+        if (s.kind != BGABP_SCHED_FLOOD) (void)schedule_order(s);
+    }
+    const Levels& levels_for(const bgabp_schedule& s);
+
+    void launch_flood(const double* b, double2* m0, double2* m1, double* x, int mode, bool delta);
+    void launch_aggregate(const double* b, const double2* msg, double* x, double* beta, unsigned long long* npiv);
+    void launch_residual(const double* b, const double* x, double* r, unsigned long long* rmax, int mode);
+    void launch_levels(const Levels& L, const double* b, double2* msg, double* x, bool delta,
+                       unsigned long long* dslot, int mode);
+    void launch_gs_levels(const Levels& L, const double* b, double* x);
+    void launch_jacobi(const double* b, const double* x, double* xn);
+
+    void reset_ctrl();
+    void read_ctrl();
+    std::string ordered_detail(const std::vector<int>& order, unsigned long long key) const;
+    std::string decode_failure(const Ctrl& c, const std::vector<int>* order) const;
+
+    int sweep(const double* b, const bgabp_schedule& s, double* x, std::string& err);
+
+    void solve_begin(const double* b_dev, const bgabp_schedule& s, const bgabp_options& o);
+    void enqueue_step();
+    void solve_steps(int nsteps);
+    bool solve_done();
+    void solve_run_to_end();
+    void solve_report(bgabp_report& rep, std::string& detail);
+    double sweep_flops() const;
+
+    void ensure_frozen_buffers();
+    void frozen_finish();
+    void precompute_lambda(const bgabp_schedule& s, double tol, int max_iter, int& converged, int& iters);
+    void correction_sweeps_dev(const double* r_dev, const bgabp_schedule& s, int sweeps, double* e_dev);
+    int cold_sweeps_dev(const double* r_dev, const bgabp_schedule& s, int sweeps, double* e_dev, std::string& err,
+                        bool check, int seq = 0);
+    // probe of multigrid.cpp:54-70 on the device
+    bool sweeps_expand(const bgabp_schedule& s);
+};
+
+unsigned nblk_host(long long n, int t = 256);
+
+}  // namespace bgabp

@@ -1,0 +1,457 @@
+// Geometric multigrid V-cycle with the GaBP smoother on the device (multigrid.hpp:17-103,
+// multigrid.cpp:54-318).  Every level is a bgabp::Engine sharing one stream; a V-cycle is a
+// host-driven sequence of kernel launches with no synchronisation inside the cycle.  Smoother
+// breakdowns are recorded on the device (k_plain_check) and turned into the reference's
+// "smoother breakdown on level k: ..." after the cycle.  The coarsest level is solved with a
+// precomputed inverse (host partial-pivot LU at setup, device GEMV per cycle) in place of the
+// reference's Eigen PartialPivLU; only that solve's rounding differs from the reference.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "engine.h"
+#include "problems.h"
+
+using namespace bgabp;
+
+namespace {
+
+enum { GabpSeq = 0, GabpRB = 1, GabpFC = 2, GabpFlood = 3, Jacobi = 5, GsLex = 6, GsRB = 7, GsFC = 8 };
+bool is_gabp(int s) { return s >= 0 && s <= 3; }
+bool supported(int s) { return is_gabp(s) || (s >= 5 && s <= 8); }
+
+struct MgLevel {
+    std::unique_ptr<Engine> E;
+    int nx = 0;
+    bgabp_schedule sched{};
+    bool frozen_ok = false;
+    double *d_b = nullptr, *d_x = nullptr;  // this level's right-hand side and iterate (coarse levels)
+};
+
+// dense partial-pivot LU + explicit inverse of the coarsest operator (host, setup only)
+std::vector<double> dense_inverse(const Engine& E) {
+    const int n = E.n;
+    std::vector<double> a((size_t)n * n, 0.0), inv((size_t)n * n, 0.0);
+    for (int i = 0; i < n; ++i)
+        for (int p = E.ro[i]; p < E.ro[i + 1]; ++p) a[(size_t)i * n + E.ci[p]] = E.val[p];
+    std::vector<int> piv(n);
+    for (int k = 0; k < n; ++k) {
+        int best = k;
+        for (int i = k + 1; i < n; ++i)
+            if (std::abs(a[(size_t)i * n + k]) > std::abs(a[(size_t)best * n + k])) best = i;
+        piv[k] = best;
+        if (best != k)
+            for (int c = 0; c < n; ++c) std::swap(a[(size_t)k * n + c], a[(size_t)best * n + c]);
+        const double d = a[(size_t)k * n + k];
+        if (d == 0.0) continue;
+        for (int i = k + 1; i < n; ++i) {
+            double& l = a[(size_t)i * n + k];
+            l /= d;
+            if (l != 0.0)
+                for (int c = k + 1; c < n; ++c) a[(size_t)i * n + c] -= l * a[(size_t)k * n + c];
+        }
+    }
+    std::vector<double> y(n);
+    for (int col = 0; col < n; ++col) {
+        std::fill(y.begin(), y.end(), 0.0);
+        y[col] = 1.0;
+        for (int k = 0; k < n; ++k)
+            if (piv[k] != k) std::swap(y[k], y[piv[k]]);
+        for (int i = 0; i < n; ++i)
+            for (int c = 0; c < i; ++c) y[i] -= a[(size_t)i * n + c] * y[c];
+        for (int i = n - 1; i >= 0; --i) {
+            for (int c = i + 1; c < n; ++c) y[i] -= a[(size_t)i * n + c] * y[c];
+            y[i] /= a[(size_t)i * n + i];
+        }
+        for (int i = 0; i < n; ++i) inv[(size_t)i * n + col] = y[i];
+    }
+    return inv;
+}
+
+}  // namespace
+
+struct bgmg {
+    int smoother = 0;
+    cudaStream_t st = nullptr;
+    std::vector<MgLevel> levels;
+    double* d_inv = nullptr;
+    double* d_fine_b = nullptr;  // scratch for host-buffer calls
+    double* d_fine_x = nullptr;
+    std::vector<double> fine_rhs;  // named hierarchies: Hierarchy::fine_rhs
+    Ctrl* h_ctrl = nullptr;
+    int seq = 0;
+
+    ~bgmg() {
+        if (st) cudaStreamSynchronize(st);
+        levels.clear();
+        if (d_inv) cudaFree(d_inv);
+        if (d_fine_b) cudaFree(d_fine_b);
+        if (d_fine_x) cudaFree(d_fine_x);
+        if (h_ctrl) cudaFreeHost(h_ctrl);
+        if (st) cudaStreamDestroy(st);
+    }
+
+    Engine& E(int k) { return *levels[k].E; }
+    int nl() const { return (int)levels.size(); }
+
+    // Hierarchy::smooth (multigrid.cpp:163-208)
+    void smooth(int k, const double* b, double* x, int sweeps, bool frozen) {
+        if (sweeps <= 0) return;
+        Engine& L = E(k);
+        if (L.n == 0) return;
+        const unsigned g = nblk_host(L.n);
+        ++seq;
+        if (is_gabp(smoother)) {
+            L.launch_residual(b, x, L.d_r, nullptr, MODE_PLAIN);
+            if (frozen && levels[k].frozen_ok) {
+                L.correction_sweeps_dev(L.d_r, levels[k].sched, sweeps, L.d_e);
+            } else {
+                std::string unused;
+                L.cold_sweeps_dev(L.d_r, levels[k].sched, sweeps, L.d_e, unused, false, seq);
+            }
+            k_axpy1<<<g, 256, 0, st>>>(x, L.d_e, L.n);
+            return;
+        }
+        // point relaxations in place (classic.cpp:99-146)
+        k_plain_reset<<<1, 1, 0, st>>>(L.d_ctrl);
+        if (smoother == Jacobi) {
+            for (int s = 0; s < sweeps; ++s) {
+                L.launch_jacobi(b, x, L.d_e);
+                ck(cudaMemcpyAsync(x, L.d_e, sizeof(double) * L.n, cudaMemcpyDeviceToDevice, st), "copy");
+            }
+        } else {
+            const Levels& lv = L.levels_for(levels[k].sched);
+            for (int s = 0; s < sweeps; ++s) L.launch_gs_levels(lv, b, x);
+        }
+        k_plain_check<<<1, 1, 0, st>>>(L.d_ctrl, seq, 5);
+    }
+
+    // Hierarchy::cycle (multigrid.cpp:210-232)
+    void cycle(int k, const bgmg_cycle& spec, const double* b, double* x) {
+        Engine& L = E(k);
+        if (k == nl() - 1) {  // direct solve overwrites x (multigrid.cpp:212-216)
+            if (L.n > 0) k_gemv_rows<<<nblk_host((long long)L.n * 32), 256, 0, st>>>(d_inv, b, x, L.n);
+            return;
+        }
+        smooth(k, b, x, spec.pre, spec.frozen != 0);
+        MgLevel& C = levels[k + 1];
+        L.launch_residual(b, x, L.d_r, nullptr, MODE_PLAIN);
+        k_restrict<<<nblk_host(C.E->n), 256, 0, st>>>(L.d_r, levels[k].nx, C.d_b);
+        ck(cudaMemsetAsync(C.d_x, 0, sizeof(double) * std::max(C.E->n, 1), st), "memset");
+        cycle(k + 1, spec, C.d_b, C.d_x);
+        k_prolong_add<<<nblk_host(L.n), 256, 0, st>>>(C.d_x, C.nx, x, 0);
+        smooth(k, b, x, spec.post, spec.frozen != 0);
+    }
+
+    void clear_failures() {
+        for (auto& lv : levels) {
+            Ctrl c;
+            std::memset(&c, 0, sizeof(c));
+            for (int q = 0; q < 4; ++q) c.epiv[q] = c.npiv[q] = kNone;
+            c.opiv = kNone;
+            ck(cudaMemcpyAsync(lv.E->d_ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, st), "ctrl");
+        }
+        seq = 0;
+    }
+
+    // first smoother failure of the last cycle, in execution order; "" if none
+    std::string failure() {
+        int best_seq = 0x7fffffff, best = -1;
+        std::string msg;
+        for (int k = 0; k < nl(); ++k) {
+            ck(cudaMemcpyAsync(h_ctrl, levels[k].E->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaStreamSynchronize(st), "sync");
+            if (h_ctrl->halt && h_ctrl->fail_seq < best_seq) {
+                best_seq = h_ctrl->fail_seq;
+                best = k;
+                const Levels* lv = levels[k].sched.kind == BGABP_SCHED_FLOOD ? nullptr : &E(k).levels_for(levels[k].sched);
+                msg = E(k).decode_failure(*h_ctrl, lv ? &lv->order : nullptr);
+            }
+        }
+        if (best < 0) return "";
+        if (is_gabp(smoother)) return "smoother breakdown on level " + std::to_string(best) + ": " + msg;
+        return msg;  // relax() throws its own message (classic.cpp:27,43)
+    }
+
+    void v_cycle_dev(const bgmg_cycle& spec, const double* b, double* x) {
+        clear_failures();
+        cycle(0, spec, b, x);
+        ck(cudaGetLastError(), "v-cycle");
+    }
+
+    double residual_inf(const double* b, const double* x) {
+        Engine& L = E(0);
+        if (L.n == 0) return 0.0;
+        ck(cudaMemsetAsync(&L.d_ctrl->red[2], 0, sizeof(unsigned long long), st), "memset");
+        L.launch_residual(b, x, nullptr, &L.d_ctrl->red[2], MODE_PLAIN);
+        unsigned long long r;
+        ck(cudaMemcpyAsync(&r, &L.d_ctrl->red[2], sizeof(r), cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaStreamSynchronize(st), "sync");
+        return bits2d(r);
+    }
+
+    double inf_norm_dev(const double* v, int n) {
+        if (n == 0) return 0.0;
+        Engine& L = E(0);
+        ck(cudaMemsetAsync(&L.d_ctrl->red[3], 0, sizeof(unsigned long long), st), "memset");
+        k_inf_norm<<<std::min<unsigned>(nblk_host(n), 1184), 256, 0, st>>>(v, n, &L.d_ctrl->red[3]);
+        unsigned long long r;
+        ck(cudaMemcpyAsync(&r, &L.d_ctrl->red[3], sizeof(r), cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaStreamSynchronize(st), "sync");
+        return bits2d(r);
+    }
+
+    // mg_solve (multigrid.cpp:276-318) on device vectors; history on the host
+    void solve_dev(const bgmg_cycle& spec, const double* b, double* x, const bgmg_options& o, bgabp_report& rep,
+                   std::vector<double>& hist, std::string& detail) {
+        const int n = E(0).n;
+        ck(cudaMemsetAsync(x, 0, sizeof(double) * std::max(n, 1), st), "memset");
+        const double r0 = inf_norm_dev(b, n);
+        hist.assign(1, r0);
+        rep.status = BGABP_MAX_ITER;
+        rep.iterations = 0;
+        rep.flop_estimate = 0.0;
+        detail.clear();
+        if (r0 <= o.tol) {
+            rep.status = BGABP_CONVERGED;
+            return;
+        }
+        for (int it = 1; it <= o.max_cycles; ++it) {
+            v_cycle_dev(spec, b, x);
+            const double r = residual_inf(b, x);
+            std::string f = failure();
+            rep.iterations = it;
+            if (!f.empty()) {
+                rep.status = BGABP_DIVERGED;
+                detail = f;
+                return;
+            }
+            hist.push_back(r);
+            if (!std::isfinite(r) || r > o.divergence_factor * r0) {
+                rep.status = BGABP_DIVERGED;
+                detail = "residual blowup";
+                return;
+            }
+            if (r <= o.tol) {
+                rep.status = BGABP_CONVERGED;
+                return;
+            }
+        }
+    }
+
+    void ensure_fine_scratch() {
+        const size_t vb = sizeof(double) * std::max(E(0).n, 1);
+        if (!d_fine_b) ck(cudaMalloc(&d_fine_b, vb), "malloc");
+        if (!d_fine_x) ck(cudaMalloc(&d_fine_x, vb), "malloc");
+    }
+};
+
+static bgabp_schedule schedule_for(int sm, int nx) {  // multigrid.cpp:25-32
+    bgabp_schedule s{};
+    s.nx = s.ny = nx;
+    switch (sm) {
+        case GabpRB: case GsRB: s.kind = BGABP_SCHED_RED_BLACK_GRID; break;
+        case GabpFC: case GsFC: s.kind = BGABP_SCHED_FOUR_COLOR_GRID; break;
+        case GabpFlood: case Jacobi: s.kind = BGABP_SCHED_FLOOD; break;
+        default: s.kind = BGABP_SCHED_SEQUENTIAL;
+    }
+    return s;
+}
+
+// Hierarchy ctor (multigrid.cpp:74-109) over caller-supplied levels
+static void build_hierarchy(bgmg* h, int nlevels, const int* n, const int* const* ro, const int* const* ci,
+                            const double* const* v, const int* nx, int smoother) {
+    if (nlevels < 1) throw InvalidArg("Hierarchy: need 1 <= J2 and a coarsest exponent >= 1");
+    if (!supported(smoother)) throw InvalidArg("Hierarchy: unsupported smoother " + std::to_string(smoother));
+    h->smoother = smoother;
+    ck(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking), "stream");
+    ck(cudaMallocHost((void**)&h->h_ctrl, sizeof(Ctrl)), "host ctrl");
+    for (int k = 0; k < nlevels; ++k) {
+        if (k + 1 < nlevels && nx[k + 1] != (nx[k] - 1) / 2)
+            throw InvalidArg("Hierarchy: level sizes must halve ((nx-1)/2)");
+        if ((long long)nx[k] * nx[k] != n[k]) throw InvalidArg("Hierarchy: level is not a square grid");
+        MgLevel L;
+        L.E = std::make_unique<Engine>();
+        L.E->build(n[k], ro[k], ci[k], v[k], BGABP_LAYOUT_AUTO, h->st);
+        L.nx = nx[k];
+        L.sched = schedule_for(smoother, nx[k]);
+        if (k > 0) {
+            L.d_b = static_cast<double*>(L.E->dalloc(sizeof(double) * std::max(n[k], 1)));
+            L.d_x = static_cast<double*>(L.E->dalloc(sizeof(double) * std::max(n[k], 1)));
+        }
+        h->levels.push_back(std::move(L));
+    }
+    if (is_gabp(smoother)) {
+        for (int k = 0; k < (int)h->levels.size(); ++k) {
+            MgLevel& L = h->levels[k];
+            if (k > 0 && L.E->sweeps_expand(L.sched)) {  // multigrid.cpp:89-93
+                h->levels.resize(k + 1);
+                break;
+            }
+            int cv = 0, its = 0;
+            L.E->precompute_lambda(L.sched, 1e-10, 500, cv, its);  // multigrid.cpp:94-95
+            L.frozen_ok = cv != 0;
+        }
+    }
+    Engine& C = *h->levels.back().E;
+    std::vector<double> inv = dense_inverse(C);
+    ck(cudaMalloc(&h->d_inv, sizeof(double) * std::max<size_t>(inv.size(), 1)), "malloc");
+    if (!inv.empty())
+        ck(cudaMemcpyAsync(h->d_inv, inv.data(), sizeof(double) * inv.size(), cudaMemcpyHostToDevice, h->st), "H2D");
+    ck(cudaStreamSynchronize(h->st), "sync");
+}
+
+#define MG_GUARD(ERRBUF, ERRLEN, ...)       \
+    try {                                   \
+        __VA_ARGS__                         \
+    } catch (const InvalidArg& ex) {        \
+        put_err(ERRBUF, ERRLEN, ex.what()); \
+        return BGABP_EINVAL;                \
+    } catch (const CudaError& ex) {         \
+        put_err(ERRBUF, ERRLEN, ex.what()); \
+        return BGABP_ECUDA;                 \
+    } catch (const std::exception& ex) {    \
+        put_err(ERRBUF, ERRLEN, ex.what()); \
+        return BGABP_ERUNTIME;              \
+    }
+
+extern "C" {
+
+int bgmg_create(int nlevels, const int* n, const int* const* row_offsets, const int* const* col_indices,
+                const double* const* values, const int* nx, int smoother, bgmg** out, char* err, size_t errlen) {
+    *out = nullptr;
+    auto h = std::make_unique<bgmg>();
+    MG_GUARD(err, errlen, {
+        build_hierarchy(h.get(), nlevels, n, row_offsets, col_indices, values, nx, smoother);
+        *out = h.release();
+        return BGABP_OK;
+    })
+}
+
+int bgmg_create_named(const char* problem, int J1, int J2, int nparam, const char* const* keys, const double* vals,
+                      int smoother, bgmg** out, char* err, size_t errlen) {
+    *out = nullptr;
+    auto h = std::make_unique<bgmg>();
+    MG_GUARD(err, errlen, {
+        if (J2 < 1 || J1 - J2 + 1 < 1) throw InvalidArg("Hierarchy: need 1 <= J2 and a coarsest exponent >= 1");
+        std::vector<std::unique_ptr<bgabp_problem>> probs;
+        std::vector<int> ns, nxs;
+        std::vector<const int*> ros, cis;
+        std::vector<const double*> vs;
+        for (int J = J1; J >= J1 - J2 + 1; --J) {  // multigrid.cpp:79-83
+            std::string e;
+            probs.emplace_back(assemble_named(problem, J, nparam, keys, vals, e));
+            if (!probs.back()) throw InvalidArg(e);
+            const bgabp_problem& p = *probs.back();
+            ns.push_back(p.n);
+            nxs.push_back(p.nx);
+            ros.push_back(p.ro.data());
+            cis.push_back(p.ci.data());
+            vs.push_back(p.val.data());
+        }
+        build_hierarchy(h.get(), (int)ns.size(), ns.data(), ros.data(), cis.data(), vs.data(), nxs.data(), smoother);
+        h->fine_rhs = probs.front()->b;
+        *out = h.release();
+        return BGABP_OK;
+    })
+}
+
+void bgmg_destroy(bgmg* h) { delete h; }
+int bgmg_num_levels(const bgmg* h) { return (int)h->levels.size(); }
+int bgmg_level_frozen_ok(const bgmg* h, int k) { return h->levels[k].frozen_ok ? 1 : 0; }
+int bgmg_level_n(const bgmg* h, int k) { return h->levels[k].E->n; }
+void* bgmg_stream(bgmg* h) { return (void*)h->st; }
+
+int bgmg_fine_rhs(const bgmg* h, double* b_out) {
+    if (h->fine_rhs.empty()) return BGABP_EINVAL;
+    std::memcpy(b_out, h->fine_rhs.data(), sizeof(double) * h->fine_rhs.size());
+    return BGABP_OK;
+}
+
+int bgmg_vcycle(bgmg* h, const bgmg_cycle* spec, const double* b, double* x, char* err, size_t errlen) {
+    MG_GUARD(err, errlen, {
+        const int n = h->E(0).n;
+        h->ensure_fine_scratch();
+        ck(cudaMemcpyAsync(h->d_fine_b, b, sizeof(double) * n, cudaMemcpyHostToDevice, h->st), "H2D");
+        ck(cudaMemcpyAsync(h->d_fine_x, x, sizeof(double) * n, cudaMemcpyHostToDevice, h->st), "H2D");
+        h->v_cycle_dev(*spec, h->d_fine_b, h->d_fine_x);
+        ck(cudaMemcpyAsync(x, h->d_fine_x, sizeof(double) * n, cudaMemcpyDeviceToHost, h->st), "D2H");
+        ck(cudaStreamSynchronize(h->st), "sync");
+        std::string f = h->failure();
+        if (!f.empty()) {
+            put_err(err, errlen, f);
+            return BGABP_ERUNTIME;
+        }
+        return BGABP_OK;
+    })
+}
+
+int bgmg_solve(bgmg* h, const bgmg_cycle* spec, const double* b, const bgmg_options* opt, bgabp_report* rep,
+               double* x_out, double* history, char* detail, size_t dl) {
+    MG_GUARD(detail, dl, {
+        const int n = h->E(0).n;
+        h->ensure_fine_scratch();
+        ck(cudaMemcpyAsync(h->d_fine_b, b, sizeof(double) * n, cudaMemcpyHostToDevice, h->st), "H2D");
+        std::vector<double> hist;
+        std::string d;
+        h->solve_dev(*spec, h->d_fine_b, h->d_fine_x, *opt, *rep, hist, d);
+        if (x_out) ck(cudaMemcpyAsync(x_out, h->d_fine_x, sizeof(double) * n, cudaMemcpyDeviceToHost, h->st), "D2H");
+        ck(cudaStreamSynchronize(h->st), "sync");
+        if (history) std::memcpy(history, hist.data(), sizeof(double) * hist.size());
+        put_err(detail, dl, d);
+        return BGABP_OK;
+    })
+}
+
+int bgmg_solve_device(bgmg* h, const bgmg_cycle* spec, const double* b_dev, const bgmg_options* opt,
+                      bgabp_report* rep, double* x_dev, double* history, char* detail, size_t dl) {
+    MG_GUARD(detail, dl, {
+        std::vector<double> hist;
+        std::string d;
+        h->solve_dev(*spec, b_dev, x_dev, *opt, *rep, hist, d);
+        ck(cudaStreamSynchronize(h->st), "sync");
+        if (history) std::memcpy(history, hist.data(), sizeof(double) * hist.size());
+        put_err(detail, dl, d);
+        return BGABP_OK;
+    })
+}
+
+int bgmg_restrict(const double* fine, int mf, double* out) {
+    try {
+        const int mc = (mf - 1) / 2;
+        if (mc <= 0) return BGABP_EINVAL;
+        double *df, *dc;
+        ck(cudaMalloc(&df, sizeof(double) * mf * mf), "malloc");
+        ck(cudaMalloc(&dc, sizeof(double) * mc * mc), "malloc");
+        ck(cudaMemcpy(df, fine, sizeof(double) * mf * mf, cudaMemcpyHostToDevice), "H2D");
+        k_restrict<<<nblk_host((long long)mc * mc), 256>>>(df, mf, dc);
+        ck(cudaMemcpy(out, dc, sizeof(double) * mc * mc, cudaMemcpyDeviceToHost), "D2H");
+        cudaFree(df);
+        cudaFree(dc);
+        return BGABP_OK;
+    } catch (const std::exception&) {
+        return BGABP_ECUDA;
+    }
+}
+
+int bgmg_prolong(const double* coarse, int mc, double* out) {
+    try {
+        const int mf = 2 * mc + 1;
+        double *df, *dc;
+        ck(cudaMalloc(&df, sizeof(double) * mf * mf), "malloc");
+        ck(cudaMalloc(&dc, sizeof(double) * std::max(mc * mc, 1)), "malloc");
+        if (mc > 0) ck(cudaMemcpy(dc, coarse, sizeof(double) * mc * mc, cudaMemcpyHostToDevice), "H2D");
+        k_prolong_add<<<nblk_host((long long)mf * mf), 256>>>(dc, mc, df, 1);
+        ck(cudaMemcpy(out, df, sizeof(double) * mf * mf, cudaMemcpyDeviceToHost), "D2H");
+        cudaFree(df);
+        cudaFree(dc);
+        return BGABP_OK;
+    } catch (const std::exception&) {
+        return BGABP_ECUDA;
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,295 @@
+"""GPU parity of the GaBP engine against the CPU oracle and the golden vectors.
+
+Mirrors the reference's own tests (proj/tests/test_gabp.cpp, test_sparse.cpp,
+acceptance.cpp criterion 10) with the CUDA path as the system under test and the restated /
+reference CPU code as the checker.
+"""
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_1904_04093_b200 as g
+from oracle.oracle import Schedule as OSched
+from tests.cases import CASES, build_case, one_way_4x4, tree_5x5
+from tests.parity import assert_close
+
+pytestmark = pytest.mark.gpu
+
+
+def digest(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def gsched(s: OSched) -> g.Schedule:
+    return g.Schedule(s.kind, s.nx, s.ny, s.order)
+
+
+LAYOUTS = [g.Layout.Auto, g.Layout.Csr]
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_per_sweep_state_matches_golden_bitwise(orc, golden, name, layout):
+    """GabpEngine::sweep after every sweep: lambda, m (CSR order), beta, x and the residual."""
+    meta, arrays = golden
+    rec = meta["cases"][name]
+    A, b, sched = build_case(orc, name)
+    eng = g.GabpEngine(A, layout)
+    x = np.zeros(A.n)
+    for s, want in enumerate(rec["digests"]):
+        ok, err = eng.sweep_resident(b, gsched(sched), x)
+        assert [ok, err] == rec["ok"][s], f"sweep {s + 1}"
+        if not ok:
+            break
+        st = eng.get_state()
+        beta = eng.node_precisions()
+        r = eng.residual_inf_norm(x, b)
+        got = [digest(st.lambda_tilde), digest(st.m), digest(x), digest(beta), float(r).hex()]
+        if got != want:  # report with the elementwise bar before failing on bits
+            keep = f"{name}/{s + 1}"
+            if keep + "/x" in arrays:
+                for k, v in (("lam", st.lambda_tilde), ("m", st.m), ("x", x), ("beta", beta)):
+                    assert_close(v, arrays[f"{keep}/{k}"], f"{name} sweep {s + 1} {k}")
+        assert got == want, f"{name} sweep {s + 1}: not bit-identical to the reference"
+
+
+def test_config1_full_state_every_sweep_against_oracle(orc):
+    """Config 1 (BASELINE.json): poisson5(64,64), b~U[-1,1] seed 0, 200 flood sweeps, lambda, m,
+    beta and x compared with the oracle after every sweep (rel 1e-10; expected bit-identical)."""
+    A, b, sched = build_case(orc, "config1")
+    eng = g.GabpEngine(A)
+    assert eng.layout == g.Layout.Dia and eng.info["num_slots"] == 4
+    ref = orc.engine(A)
+    lam, m = ref.make_state()
+    xr = np.zeros(A.n)
+    x = np.zeros(A.n)
+    nonbit = 0
+    for s in range(200):
+        ok, _ = eng.sweep_resident(b, g.Schedule.parallel_flood(), x)
+        assert ok
+        ref.sweep(b, sched, lam, m, xr)
+        st = eng.get_state()
+        nonbit += assert_close(st.lambda_tilde, lam, f"lambda@{s + 1}")
+        nonbit += assert_close(st.m, m, f"m@{s + 1}")
+        nonbit += assert_close(x, xr, f"x@{s + 1}")
+        nonbit += assert_close(eng.node_precisions(), ref.node_precisions(lam, m), f"beta@{s + 1}")
+    assert nonbit == 0
+    rel = ref.o.residual_inf_norm(A, xr, b) / np.abs(b).max()
+    assert abs(rel - 2.33e-2) < 1e-3  # rel. residual ~2.3e-2 after 200 sweeps
+
+
+def test_sweep_with_caller_state_roundtrip(orc):
+    """The reference signature sweep(b, sched, state, x) with a caller-owned MessageState."""
+    A, b, sched = build_case(orc, "dd25_nonsym_flood")
+    eng = g.GabpEngine(A)
+    ref = orc.engine(A)
+    st = eng.make_state()
+    lam, m = ref.make_state()
+    x, xr = np.zeros(A.n), np.zeros(A.n)
+    for _ in range(7):
+        assert eng.sweep(b, g.Schedule.parallel_flood(), st, x)[0]
+        ref.sweep(b, sched, lam, m, xr)
+    assert st.lambda_tilde.tobytes() == lam.tobytes() and st.m.tobytes() == m.tobytes()
+    assert x.tobytes() == xr.tobytes()
+
+
+SOLVES = ["poisson9_flood", "poisson9_rb", "dd25_nonsym_flood", "dd25_nonsym_seq", "dd20_sym_flood", "ex7x7_flood",
+          "ex7x7_seq", "pivot2_seq", "pivot2_flood", "poisson64_flood"]
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("name", SOLVES)
+def test_solve_report_matches_golden(orc, golden, name, layout):
+    """solve(): status, iterations, detail, flop estimate and the whole residual history."""
+    meta, _ = golden
+    rec = meta["solves"][name]
+    A, b, sched = build_case(orc, name)
+    eng = g.GabpEngine(A, layout)
+    rep = eng.solve(b, gsched(sched), g.GabpOptions(tol=rec["tol"], max_iter=rec["max_iter"], stop=rec["stop"]))
+    assert (int(rep.status), rep.iterations, rep.detail) == (rec["status"], rec["iterations"], rec["detail"])
+    assert [float(v).hex() for v in rep.residual_history] == rec["history"]
+    assert rep.flop_estimate == rec["flops"]
+    if rec["status"] != 1 or rec["detail"] == "residual blowup":
+        assert digest(rep.solution) == rec["x"]
+
+
+def test_solve_stop_rules_and_edges(orc):
+    A = orc.poisson5(6, 6)
+    b = orc.rng(3).vector(A.n)
+    eng = g.GabpEngine(A)
+    ref = orc.engine(A)
+    # r0 <= tol: converged after 0 iterations, x = 0 (gabp.cpp:179-185)
+    rep = eng.solve(b, g.Schedule.parallel_flood(), g.GabpOptions(tol=10.0))
+    assert (rep.status, rep.iterations) == (g.SolveStatus.Converged, 0) and not rep.solution.any()
+    # max_iter = 0 -> MaxIter immediately
+    rep = eng.solve(b, g.Schedule.parallel_flood(), g.GabpOptions(tol=1e-30, max_iter=0))
+    assert (rep.status, rep.iterations) == (g.SolveStatus.MaxIter, 0)
+    # MessageDelta stop and tiny caps, every schedule
+    for sched in (OSched.parallel_flood(), OSched.sequential(), OSched.red_black_grid(6, 6),
+                  OSched.four_color_grid(6, 6)):
+        for stop, tol, cap in ((1, 1e-9, 500), (0, 1e-9, 7), (0, 1e-9, 1), (1, 0.5, 50)):
+            want = ref.solve(b, sched, tol=tol, max_iter=cap, stop=stop)
+            got = eng.solve(b, gsched(sched), g.GabpOptions(tol=tol, max_iter=cap, stop=stop))
+            assert (int(got.status), got.iterations) == (want.status, want.iterations), (sched.kind, stop, cap)
+            assert got.residual_history.tobytes() == want.residual_history.tobytes()
+            assert got.solution.tobytes() == want.solution.tobytes()
+
+
+def test_diagonal_system_solves_in_one_sweep():
+    """test_gabp.cpp:63-71"""
+    D = g.SparseMatrix(2, np.array([0, 1, 2], np.int32), np.array([0, 1], np.int32), np.array([2.0, 4.0]))
+    rep = g.GabpEngine(D).solve(np.array([2.0, 8.0]), g.Schedule.sequential(2), g.GabpOptions(tol=1e-14))
+    assert rep.status == g.SolveStatus.Converged and rep.iterations == 1
+    assert np.allclose(rep.solution, [1.0, 2.0])
+
+
+def test_pivot_breakdown_is_divergence(orc):
+    """test_gabp.cpp:73-85 through solve() and sweep()."""
+    from tests.cases import pivot_2x2
+    A = pivot_2x2(orc)
+    eng = g.GabpEngine(A)
+    rep = eng.solve(np.ones(2), g.Schedule.sequential(2), g.GabpOptions())
+    assert rep.status == g.SolveStatus.Diverged and "pivot" in rep.detail
+    x = np.zeros(2)
+    eng.reset_state()
+    ok, err = eng.sweep_resident(np.ones(2), g.Schedule.parallel_flood(), x)
+    assert not ok and err == "zero pivot at node 0"
+
+
+def test_schedule_errors_match_reference(orc):
+    A = orc.poisson5(3, 3)
+    eng = g.GabpEngine(A)
+    x = np.zeros(9)
+    with pytest.raises(ValueError, match="does not cover every node"):
+        eng.sweep_resident(np.ones(9), g.Schedule.red_black_grid(4, 3), x)
+    with pytest.raises(ValueError, match="not a permutation"):
+        eng.sweep_resident(np.ones(9), g.Schedule.custom([0, 0, 1, 2, 3, 4, 5, 6, 7]), x)
+
+
+def test_tree_exactness_and_hand_elimination(orc):
+    """test_gabp.cpp:87-111: saturated tree messages equal hand elimination; x equals A^-1 b."""
+    A = tree_5x5(orc)
+    eng = g.GabpEngine(A)
+    st = eng.make_state()
+    x = np.zeros(5)
+    for _ in range(10):
+        assert eng.sweep(np.ones(5), g.Schedule.sequential(5), st, x)[0]
+    D = A.dense()
+    lam13 = -D[2, 0] * D[0, 2] / D[0, 0]
+    lam23 = -D[2, 1] * D[1, 2] / D[1, 1]
+    expected = -D[4, 2] * D[2, 4] / (D[2, 2] + lam13 + lam23)
+    pos = int(np.where((np.repeat(np.arange(5), np.diff(A.row_offsets)) == 4) & (A.col_indices == 2))[0][0])
+    assert abs(st.lambda_tilde[pos] * D[2, 4] - expected) <= 1e-12 * abs(expected)
+    assert np.max(np.abs(x - np.linalg.solve(D, np.ones(5)))) < 1e-12
+    rng = orc.rng(101)
+    for trial in range(5):
+        n = 20 + 36 * trial
+        T, edges = rng.tree(n)
+        diam = orc.tree_diameter(n, edges)
+        bb = rng.vector(n)
+        eng = g.GabpEngine(T)
+        st = eng.make_state()
+        x = np.zeros(n)
+        for _ in range(2 * diam):
+            assert eng.sweep(bb, g.Schedule.sequential(n), st, x)[0]
+        assert np.max(np.abs(x - orc.dense_solve(T, bb))) < 1e-10
+
+
+def test_flood_iterate_equals_computation_tree(orc):
+    """acceptance.cpp:296-316 (criterion 10) with the GPU flood sweep."""
+    rng = orc.rng(1010)
+    for trial in range(10):
+        n = rng.uniform_int(4, 8)
+        A = rng.diag_dominant(n, trial % 2 == 0, 0.5)
+        b = rng.vector(A.n)
+        eng = g.GabpEngine(A)
+        x = np.zeros(A.n)
+        for depth in range(1, 6):
+            assert eng.sweep_resident(b, g.Schedule.parallel_flood(), x)[0]
+            for root in range(A.n):
+                t = orc.computation_tree_solve(A, b, root, depth, 2000000)
+                assert abs(t - x[root]) <= 1e-12 * max(1.0, abs(x[root]))
+
+
+def test_message_graph_one_way_edges(orc):
+    """test_gabp.cpp:43-61: 7 edges, node 3 sends but never receives."""
+    A = one_way_4x4(orc)
+    eng = g.GabpEngine(A)
+    assert eng.num_edges == 7
+    x = np.zeros(4)
+    b = np.arange(1.0, 5.0)
+    for _ in range(30):
+        eng.sweep_resident(b, g.Schedule.parallel_flood(), x)
+    assert np.max(np.abs(x - np.linalg.solve(A.dense(), b))) < 1e-10
+
+
+def test_frozen_path_matches_golden(orc, golden):
+    """precompute_lambda / correction_sweeps / solve_error_correction (gabp.cpp:221-401)."""
+    meta, arrays = golden
+    for name, rec in meta["frozen"].items():
+        A, b, sched = build_case(orc, name)
+        for layout in LAYOUTS:
+            eng = g.GabpEngine(A, layout)
+            fz = eng.precompute_lambda(gsched(sched), 1e-10, 500)
+            assert (fz.converged, fz.iterations) == (rec["converged"], rec["iterations"])
+            assert digest(fz.lambda_tilde) == rec["lam"], name
+            assert digest(fz.sigma) == rec["sigma"], name
+            e = eng.correction_sweeps(b, gsched(sched), fz, 3)
+            assert digest(e) == rec["corr3"], name
+            rep = eng.solve_error_correction(b, gsched(sched), 2, fz, g.GabpOptions(tol=1e-10, max_iter=3000))
+            assert (int(rep.status), rep.iterations) == (rec["ec_status"], rec["ec_iterations"])
+            assert [float(v).hex() for v in rep.residual_history] == rec["ec_history"]
+
+
+def test_error_correction_known_answers(orc):
+    """test_gabp.cpp:310-336: exact solution untouched; cold correction replays the iteration."""
+    A = orc.poisson5(5, 5)
+    b = orc.rng(13).vector(A.n)
+    xs = orc.dense_solve(A, b)
+    eng = g.GabpEngine(A)
+    fz = eng.precompute_lambda(g.Schedule.sequential())
+    assert np.max(np.abs(eng.error_correction_apply(b, xs, 3, g.Schedule.sequential(), fz) - xs)) < 1e-12
+    A4 = orc.poisson5(4, 4)
+    b4 = orc.rng(21).vector(A4.n)
+    e4 = g.GabpEngine(A4)
+    for k in (1, 3, 7):
+        cold = e4.error_correction_apply(b4, np.zeros(A4.n), k, g.Schedule.sequential())
+        st = e4.make_state()
+        x = np.zeros(A4.n)
+        for _ in range(k):
+            e4.sweep(b4, g.Schedule.sequential(), st, x)
+        assert np.max(np.abs(cold - x)) < 1e-14
+
+
+def test_residual_inf_norm_known_answers(orc):
+    """test_sparse.cpp:96-104"""
+    I3 = g.SparseMatrix(3, np.array([0, 1, 2, 3], np.int32), np.arange(3, dtype=np.int32), np.ones(3))
+    assert g.GabpEngine(I3).residual_inf_norm([1, 2, 3], [1, 2, 3]) == 0.0
+    E = orc.example7x7()
+    assert g.GabpEngine(E).residual_inf_norm(np.zeros(7), np.ones(7)) == 1.0
+
+
+def test_empty_and_single_node_systems():
+    E0 = g.SparseMatrix(0, np.array([0], np.int32), np.zeros(0, np.int32), np.zeros(0))
+    rep = g.GabpEngine(E0).solve(np.zeros(0), g.Schedule.parallel_flood(), g.GabpOptions())
+    assert rep.status == g.SolveStatus.Converged and rep.iterations == 0
+    one = g.SparseMatrix(1, np.array([0, 1], np.int32), np.array([0], np.int32), np.array([4.0]))
+    rep = g.GabpEngine(one).solve(np.array([2.0]), g.Schedule.parallel_flood(), g.GabpOptions(tol=1e-15))
+    assert rep.status == g.SolveStatus.Converged and rep.solution[0] == 0.5
+
+
+def test_device_stepping_api_equals_host_solve(orc):
+    import torch
+    A = orc.poisson5(40, 40)
+    b = orc.rng(8).vector(A.n)
+    eng = g.GabpEngine(A)
+    tol = 1e-8 * np.abs(b).max()
+    want = eng.solve(b, g.Schedule.parallel_flood(), g.GabpOptions(tol=tol, max_iter=100000))
+    bd = torch.tensor(b, device="cuda")
+    xd = torch.zeros(A.n, dtype=torch.float64, device="cuda")
+    eng.solve_device_begin(bd.data_ptr(), g.Schedule.parallel_flood(), g.GabpOptions(tol=tol, max_iter=100000))
+    eng.solve_device_steps(want.iterations + 40)
+    status, its, _, _ = eng.solve_device_end(xd.data_ptr())
+    assert (status, its) == (want.status, want.iterations)
+    assert xd.cpu().numpy().tobytes() == want.solution.tobytes()
