@@ -202,7 +202,7 @@ def run_gpu(args, world, rank, local):
     b_host = torch.from_numpy(P.b).pin_memory()
     b_dev = b_host.to(dev)
     tol = 1e-8 * float(np.abs(P.b).max())
-    max_iter = max(20000, args.warmup + args.steps + 2)
+    max_iter = max(20000, args.warmup + 2 * args.steps + 4)
     opt = g.GabpOptions(tol=tol, max_iter=max_iter)
     sched = g.Schedule.parallel_flood()
 
@@ -221,21 +221,18 @@ def run_gpu(args, world, rank, local):
         torch.cuda.synchronize()
     barrier(world)
     ms = ev0.elapsed_time(ev1)
-    status, its, _, _ = eng.solve_device_end()
-    assert int(status) == 2 and its >= args.warmup + args.steps - 1, (status, its)  # no early stop in the window
     ms_max = max_over_ranks(ms, world)
     value = world * E * args.steps / (ms_max / 1e3)
 
-    # ---- dominant kernel alone: K bare flood sweeps, CUDA events on the launching stream -------
-    eng.flood_sweeps_device(b_dev.data_ptr(), 3)
-    torch.cuda.synchronize()
-    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    k0.record(stream)
-    eng.flood_sweeps_device(b_dev.data_ptr(), args.steps)
-    k1.record(stream)
-    k1.synchronize()
-    t_sweep = k0.elapsed_time(k1) / args.steps / 1e3
-    bytes_sweep = float(info["bytes_per_sweep"])
+    # ---- dominant kernel: the fused sweep+residual launch of the same loop, CUDA events around
+    # every launch on the engine's stream (the loop continues the solve above, no graphs) --------
+    hot_ms = eng.solve_device_steps_timed(args.steps)
+    t_sweep = hot_ms / args.steps / 1e3
+    status, its, _, _ = eng.solve_device_end()
+    assert int(status) == 2 and its >= args.warmup + 2 * args.steps - 2, (status, its)  # never stopped early
+    # algorithmic bytes of one fused launch: the sweep's 40E + 24n plus the residual's own reads,
+    # x(t-2) (8n; A and b are the sweep's, shared when A is symmetric) -- SURVEY.md 8(d)
+    bytes_sweep = float(info["bytes_per_sweep"]) + 8.0 * n + (0.0 if info["symmetric_values"] else 8.0 * E)
     peak, peak_src = peaks()
     achieved = bytes_sweep / t_sweep / 1e9
     traffic = None
@@ -267,10 +264,11 @@ def run_gpu(args, world, rank, local):
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE.json config 2: b ~ U[-1,1], seed 1)",
             "config": workload_config(P, args, info),
-            "roofline": {"bound": "hbm", "kernel": "k_flood_dia<4> (K1 fused flood sweep)", "achieved": achieved,
+            "roofline": {"bound": "hbm", "kernel": "k_flood_solve_dia<4> (K1 flood sweep + K4 residual, fused)",
+                         "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "peak_source": peak_src, "bytes_per_launch": bytes_sweep,
-                         "bytes_formula": "40*E + 24*n (SURVEY.md 8(d))", "us_per_launch": t_sweep * 1e6,
+                         "bytes_formula": "40*E + 24*n (B_sweep, SURVEY.md 8(d)) + 8*n (x read of the fused residual)", "us_per_launch": t_sweep * 1e6,
                          "frac_of_8TBs": achieved / 8000.0, "share_of_step": t_sweep * 1e3 / (ms_max / args.steps)},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / e2e_sweeps,
                     "d2h_bytes_per_step": d2h / e2e_sweeps,

@@ -130,8 +130,12 @@ int bgabp_solve_device_begin(bgabp_engine* e, const double* b_dev, const bgabp_s
 int bgabp_solve_device_steps(bgabp_engine* e, int nsteps);
 int bgabp_solve_device_end(bgabp_engine* e, bgabp_report* rep, double* x_dev, double* history_dev,
                            char* detail, size_t detaillen);
-/* `nsweeps` bare flood sweeps on device b (no residual, no stop logic): the hot kernel alone,
- * for timing it with events on bgabp_stream(). */
+/* Same as bgabp_solve_device_steps, launched without graphs and with a CUDA event pair around
+ * the hot kernel of every iteration (the fused flood sweep + residual for DIA flood solves);
+ * synchronises and returns the summed device time of those launches in *hot_ms. */
+int bgabp_solve_device_steps_timed(bgabp_engine* e, int nsteps, double* hot_ms);
+/* `nsweeps` bare flood sweeps on device b (no residual, no stop logic; x of the previous sweep
+ * is written to the handle's x buffer): the sweep kernel alone. */
 int bgabp_flood_sweeps_device(bgabp_engine* e, const double* b_dev, int nsweeps);
 
 /* residual_inf_norm(A, x, b) (sparse.cpp:104-115) on the handle's matrix */
@@ -203,6 +207,8 @@ bgabp_problem* bgabp_problem_poisson5(int nx, int ny);          /* tests/oracles
 bgabp_problem* bgabp_problem_config(int config, int size, unsigned seed); /* configs 2..5 */
 /* config-5 coarse level: same K field rule, level `k` below the finest (k=0 finest) */
 bgabp_problem* bgabp_problem_config5_level(int J_fine, int k, unsigned seed);
+/* the same family with another log-K standard deviation (config 5 uses sigma = 2) */
+bgabp_problem* bgabp_problem_varcoef2d_level(int J_fine, int k, unsigned seed, double sigma);
 void bgabp_problem_free(bgabp_problem* p);
 int bgabp_problem_n(const bgabp_problem* p);
 long long bgabp_problem_nnz(const bgabp_problem* p);

@@ -228,6 +228,8 @@ void Engine::build(int n_, const int* ro_, const int* ci_, const double* v_, int
     d_r = static_cast<double*>(dalloc(vb));
     d_e = static_cast<double*>(dalloc(vb));
     d_aux = static_cast<double*>(dalloc(vb));
+    d_x2 = static_cast<double*>(dalloc(vb));
+    d_spread = static_cast<unsigned long long*>(dalloc(sizeof(unsigned long long) * 8 * kSpread));
     cur = 0;
     ck(cudaStreamSynchronize(st), "setup sync");
 }
@@ -507,6 +509,7 @@ int Engine::sweep(const double* b, const bgabp_schedule& s, double* x, std::stri
 // ---------------------------------------------------------------------------------------------
 void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bgabp_options& o) {
     solve_flood = s.kind == BGABP_SCHED_FLOOD;
+    solve_fused = solve_flood && layout == BGABP_LAYOUT_DIA;
     solve_levels = solve_flood ? nullptr : &levels_for(s);
     solve_b = b_dev;
     solve_stop = o.stop;
@@ -525,6 +528,8 @@ void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bga
     for (int k = 0; k < 2; ++k)
         ck(cudaMemsetAsync(d_msg[k], 0, sizeof(double2) * (size_t)std::max<long long>(nslots, 1), st), "memset");
     ck(cudaMemsetAsync(d_x, 0, sizeof(double) * std::max(n, 1), st), "memset x");
+    ck(cudaMemsetAsync(d_x2, 0, sizeof(double) * std::max(n, 1), st), "memset x");
+    ck(cudaMemsetAsync(d_spread, 0, sizeof(unsigned long long) * 8 * kSpread, st), "memset");
     cur = 0;
     if (n > 0) k_inf_norm<<<std::min<unsigned>(nblk(n), 1184), 256, 0, st>>>(b_dev, n, &d_ctrl->red[0]);
     k_solve_arm<<<1, 1, 0, st>>>(d_ctrl, d_hist);
@@ -533,8 +538,35 @@ void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bga
 }
 
 void Engine::enqueue_step() {
+    if (solve_fused) {
+        const bool dl = solve_stop == BGABP_STOP_MESSAGE_DELTA;
+        const unsigned g = nblk(n);
+        // register cap per slot count: 4 resident blocks for 2-4 slots, fewer for 6-8 (no spills)
+#define FUSED(SS_, MB_)                                                                                            \
+    if (symmetric) {                                                                                               \
+        if (dl) k_flood_solve_dia<SS_, true, true, MB_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_x, d_x2, d_ctrl, d_spread); \
+        else k_flood_solve_dia<SS_, false, true, MB_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_x, d_x2, d_ctrl, d_spread); \
+    } else {                                                                                                       \
+        if (dl) k_flood_solve_dia<SS_, true, false, MB_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_x, d_x2, d_ctrl, d_spread); \
+        else k_flood_solve_dia<SS_, false, false, MB_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_x, d_x2, d_ctrl, d_spread); \
+    }
+        if (timed_events) ck(cudaEventRecord((*timed_events)[2 * timed_index], st), "event");
+        switch (S) {
+            case 2: FUSED(2, 4) break;
+            case 4: FUSED(4, 4) break;
+            case 6: FUSED(6, 3) break;
+            case 8: FUSED(8, 2) break;
+            default: throw InvalidArg("gabp: unsupported DIA slot count");
+        }
+#undef FUSED
+        if (timed_events) ck(cudaEventRecord((*timed_events)[2 * timed_index + 1], st), "event");
+        k_solve_decide_lag2<<<1, kSpread, 0, st>>>(d_ctrl, d_hist, d_spread);
+        return;
+    }
     if (solve_flood) {
+        if (timed_events) ck(cudaEventRecord((*timed_events)[2 * timed_index], st), "event");
         launch_flood(solve_b, d_msg[0], d_msg[1], d_x, MODE_SOLVE, solve_stop == BGABP_STOP_MESSAGE_DELTA);
+        if (timed_events) ck(cudaEventRecord((*timed_events)[2 * timed_index + 1], st), "event");
         launch_residual(solve_b, d_x, nullptr, nullptr, MODE_SOLVE);
         k_solve_finalize<<<1, 1, 0, st>>>(d_ctrl, d_hist);
     } else {
@@ -549,13 +581,13 @@ void Engine::solve_steps(int nsteps) {
     if (nsteps <= 0) return;
     // graph-replay chunks of iterations: the kernels read their step index from the device,
     // so one captured chunk is valid for any position in the loop
-    const size_t per_step = solve_flood ? 3 : solve_levels->ptr.size() + 1;
+    const size_t per_step = solve_fused ? 2 : solve_flood ? 3 : solve_levels->ptr.size() + 1;
     const bool use_graph = per_step * 16 <= 4096 && n > 0;
     int left = nsteps;
     while (left > 0) {
         const int chunk = use_graph ? std::min(left, 16) : left;
         if (use_graph && chunk == 16) {
-            const std::string key = std::string(solve_flood ? "f" : "o") + std::to_string(solve_stop) + ":" +
+            const std::string key = std::string(solve_fused ? "F" : solve_flood ? "f" : "o") + std::to_string(solve_stop) + ":" +
                                     std::to_string((long long)(uintptr_t)solve_b) + ":" +
                                     std::to_string((long long)(uintptr_t)solve_levels);
             auto it = graphs.find(key);
@@ -588,7 +620,7 @@ void Engine::solve_run_to_end() {
     // enqueue growing chunks until the device has decided (at most max_iter + 1 iterations)
     int chunk = 16;
     while (!solve_done()) {
-        const long long cap = (long long)solve_max_iter + 1 - steps_enqueued;
+        const long long cap = (long long)solve_max_iter + (solve_fused ? 2 : 1) - steps_enqueued;
         if (cap <= 0) throw CudaError("solve loop did not terminate");
         solve_steps((int)std::min<long long>(chunk, cap));
         chunk = std::min(chunk * 2, 512);
@@ -617,6 +649,11 @@ void Engine::solve_report(bgabp_report& rep, std::string& detail) {
     const double per_iter = sweep_flops() + 2.0 * (double)nnz;  // gabp.cpp:200-202
     rep.flop_estimate = 0.0;
     for (int k = 0; k < c.iterations - (pivot ? 1 : 0); ++k) rep.flop_estimate += per_iter;
+}
+
+const double* Engine::solve_x() const {
+    if (!solve_fused) return d_x;
+    return (h_ctrl->solx & 1) ? d_x2 : d_x;
 }
 
 double Engine::sweep_flops() const {  // gabp.cpp:165-172
@@ -979,7 +1016,7 @@ int bgabp_solve(bgabp_engine* h, const double* b, const bgabp_schedule* s, const
         std::string d;
         E.solve_report(*rep, d);
         if (x_out && E.n > 0)
-            ck(cudaMemcpyAsync(x_out, E.d_x, sizeof(double) * E.n, cudaMemcpyDeviceToHost, E.st), "D2H x");
+            ck(cudaMemcpyAsync(x_out, E.solve_x(), sizeof(double) * E.n, cudaMemcpyDeviceToHost, E.st), "D2H x");
         if (history)
             ck(cudaMemcpyAsync(history, E.d_hist, sizeof(double) * (rep->iterations + 1), cudaMemcpyDeviceToHost, E.st),
                "D2H hist");
@@ -1011,7 +1048,7 @@ int bgabp_solve_device_end(bgabp_engine* h, bgabp_report* rep, double* x_dev, do
         std::string d;
         E.solve_report(*rep, d);
         if (x_dev && E.n > 0)
-            ck(cudaMemcpyAsync(x_dev, E.d_x, sizeof(double) * E.n, cudaMemcpyDeviceToDevice, E.st), "D2D x");
+            ck(cudaMemcpyAsync(x_dev, E.solve_x(), sizeof(double) * E.n, cudaMemcpyDeviceToDevice, E.st), "D2D x");
         if (history_dev)
             ck(cudaMemcpyAsync(history_dev, E.d_hist, sizeof(double) * (rep->iterations + 1), cudaMemcpyDeviceToDevice,
                                E.st),
@@ -1022,11 +1059,37 @@ int bgabp_solve_device_end(bgabp_engine* h, bgabp_report* rep, double* x_dev, do
     })
 }
 
+int bgabp_solve_device_steps_timed(bgabp_engine* h, int nsteps, double* hot_ms) {
+    ABI_GUARD(nullptr, 0, {
+        Engine& E = h->E;
+        std::vector<cudaEvent_t> ev(2 * (size_t)std::max(nsteps, 0));
+        for (auto& e : ev) ck(cudaEventCreate(&e), "event");
+        E.timed_events = &ev;
+        for (int k = 0; k < nsteps; ++k) {
+            E.timed_index = k;
+            E.enqueue_step();
+        }
+        E.timed_events = nullptr;
+        ck(cudaGetLastError(), "timed steps");
+        ck(cudaStreamSynchronize(E.st), "sync");
+        double total = 0.0;
+        for (int k = 0; k < nsteps; ++k) {
+            float ms = 0.f;
+            ck(cudaEventElapsedTime(&ms, ev[2 * k], ev[2 * k + 1]), "elapsed");
+            total += ms;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+        E.steps_enqueued += nsteps;
+        *hot_ms = total;
+        return BGABP_OK;
+    })
+}
+
 int bgabp_flood_sweeps_device(bgabp_engine* h, const double* b_dev, int nsweeps) {
     ABI_GUARD(nullptr, 0, {
         Engine& E = h->E;
         for (int k = 0; k < nsweeps; ++k) {
-            E.launch_flood(b_dev, E.d_msg[E.cur], E.d_msg[E.cur ^ 1], nullptr, MODE_PLAIN, false);
+            E.launch_flood(b_dev, E.d_msg[E.cur], E.d_msg[E.cur ^ 1], E.d_x, MODE_PLAIN, false);
             E.cur ^= 1;
         }
         ck(cudaGetLastError(), "flood sweeps");

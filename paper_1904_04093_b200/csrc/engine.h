@@ -64,6 +64,8 @@ struct Engine {
     int cur = 0;
     double *d_b = nullptr, *d_x = nullptr, *d_r = nullptr, *d_e = nullptr, *d_aux = nullptr;
     double* d_hist = nullptr;
+    double* d_x2 = nullptr;          // second x buffer of the fused flood solve (x(k) in x{k&1})
+    unsigned long long* d_spread = nullptr;  // per-warp max slots of the fused solve step
     long long hist_cap = 0;
     double *d_lam = nullptr, *d_lsrc = nullptr, *d_sigma = nullptr;
     bool has_frozen = false;
@@ -74,10 +76,13 @@ struct Engine {
 
     // device-resident solve loop
     bool solve_flood = true;
+    bool solve_fused = false;
     const Levels* solve_levels = nullptr;
     const double* solve_b = nullptr;
     int solve_stop = 0, solve_max_iter = 0;
     long long steps_enqueued = 0;
+    std::vector<cudaEvent_t>* timed_events = nullptr;  // bgabp_solve_device_steps_timed
+    int timed_index = 0;
 
     ~Engine();
     void* dalloc(size_t bytes);
@@ -113,6 +118,7 @@ struct Engine {
     bool solve_done();
     void solve_run_to_end();
     void solve_report(bgabp_report& rep, std::string& detail);
+    const double* solve_x() const;
     double sweep_flops() const;
 
     void ensure_frozen_buffers();

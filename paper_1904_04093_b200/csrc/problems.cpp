@@ -473,8 +473,12 @@ bgabp_problem* bgabp_problem_config(int config, int size, unsigned seed) {
 }
 
 bgabp_problem* bgabp_problem_config5_level(int J_fine, int k, unsigned seed) {
+    return bgabp_problem_varcoef2d_level(J_fine, k, seed, 2.0);
+}
+
+bgabp_problem* bgabp_problem_varcoef2d_level(int J_fine, int k, unsigned seed, double sigma) {
     try {
-        return varcoef2d_problem(J_fine, k, seed, 2.0);
+        return varcoef2d_problem(J_fine, k, seed, sigma);
     } catch (const std::exception&) {
         return nullptr;
     }

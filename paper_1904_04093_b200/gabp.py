@@ -83,6 +83,7 @@ def lib():
             "bgabp_solve_device_steps": (C.c_int, [_vp, C.c_int]),
             "bgabp_solve_device_end": (C.c_int, [_vp, C.POINTER(_Rep), _vp, _vp, C.c_char_p, C.c_size_t]),
             "bgabp_flood_sweeps_device": (C.c_int, [_vp, _vp, C.c_int]),
+            "bgabp_solve_device_steps_timed": (C.c_int, [_vp, C.c_int, _dp]),
             "bgabp_residual_inf_norm": (C.c_int, [_vp, _dp, _dp, _dp]),
             "bgabp_precompute_lambda": (C.c_int, [_vp, S, C.c_double, C.c_int, _dp, _dp, _ip, _ip]),
             "bgabp_set_frozen": (C.c_int, [_vp, _dp, _dp]),
@@ -113,6 +114,7 @@ def lib():
             "bgabp_problem_poisson5": (_vp, [C.c_int, C.c_int]),
             "bgabp_problem_config": (_vp, [C.c_int, C.c_int, C.c_uint]),
             "bgabp_problem_config5_level": (_vp, [C.c_int, C.c_int, C.c_uint]),
+            "bgabp_problem_varcoef2d_level": (_vp, [C.c_int, C.c_int, C.c_uint, C.c_double]),
             "bgabp_problem_free": (None, [_vp]),
             "bgabp_problem_n": (C.c_int, [_vp]),
             "bgabp_problem_nnz": (C.c_longlong, [_vp]),
@@ -443,6 +445,12 @@ class GabpEngine:
     def solve_device_steps(self, nsteps):
         _raise(lib().bgabp_solve_device_steps(self._h, int(nsteps)), "solve_device_steps")
 
+    def solve_device_steps_timed(self, nsteps):
+        """Enqueue nsteps iterations with events around each hot kernel; returns its total ms."""
+        ms = C.c_double(0)
+        _raise(lib().bgabp_solve_device_steps_timed(self._h, int(nsteps), C.byref(ms)), "solve_device_steps_timed")
+        return ms.value
+
     def solve_device_end(self, x_ptr=None, hist_ptr=None):
         rep = _Rep()
         det = C.create_string_buffer(512)
@@ -655,8 +663,9 @@ def config_problem(config, size=0, seed=None) -> AssembledProblem:
     return _take_problem(p)
 
 
-def config5_level(J_fine, k, seed=4) -> AssembledProblem:
-    p = lib().bgabp_problem_config5_level(J_fine, k, seed)
+def config5_level(J_fine, k, seed=4, sigma=2.0) -> AssembledProblem:
+    """Level k (0 = finest) of the config-5 hierarchy; sigma = std of log K (config 5: 2)."""
+    p = lib().bgabp_problem_varcoef2d_level(J_fine, k, seed, sigma)
     if not p:
         raise ValueError("config 5 level out of range")
     return _take_problem(p)
