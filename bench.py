@@ -287,42 +287,86 @@ def run_gpu(args, world, rank, local):
 # ------------------------------------------------------------------------------------------------
 # config 5: multigrid V(2,2) time to 1e-8 (secondary line, --workload mg)
 # ------------------------------------------------------------------------------------------------
+def _mg_levels(g, J, sigma):
+    levels = [g.config5_level(J, k, sigma=sigma) for k in range(J - 4)]  # down to 31 x 31 (J = 5)
+    return levels, levels[0].b
+
+
 def run_mg(args, world, rank, local):
+    """Config 5: V(2,2) with red-black GaBP / flood GaBP / red-black GS to rel. residual 1e-8."""
     import torch
 
     import paper_1904_04093_b200 as g
     torch.cuda.set_device(local)
     J = args.mg_J
-    levels, nxs = [], []
-    for k in range(J - 4):  # down to 31 x 31 (J = 5)
-        p = g.config5_level(J, k)
-        levels.append(p.A)
-        nxs.append(p.nx)
-        if k == 0:
-            b = p.b
     out = {"metric": "multigrid V(2,2) time to rel. residual 1e-8", "unit": "s", "higher_is_better": False,
-           "config": {"workload": f"config5: var-coeff 2D diffusion {nxs[0]}^2, K=exp(N(0,2^2)), {len(levels)} levels"},
-           "dtype": "f64", "data": "synthetic (BASELINE.json config 5, seed 4)", "results": {}}
-    bd = torch.tensor(b, device="cuda")
-    xd = torch.zeros_like(bd)
-    tol = 1e-8 * float(np.abs(b).max())
-    for name, sm in (("gabp_red_black", g.MgSmoother.GabpRedBlack), ("gs_red_black", g.MgSmoother.GsRedBlack),
-                     ("gabp_flood", g.MgSmoother.GabpFlood)):
-        t0 = time.perf_counter()
-        h = g.Hierarchy.from_levels(levels, nxs, sm)
-        setup = time.perf_counter() - t0
-        spec = g.CycleSpec(2, 2, sm)
-        cap = args.mg_cycles if sm != g.MgSmoother.GabpFlood else min(args.mg_cycles, 30)
-        g.mg_solve_device(h, spec, bd.data_ptr(), xd.data_ptr(), g.MgSolveOptions(tol=tol, max_cycles=2))
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        rep = g.mg_solve_device(h, spec, bd.data_ptr(), xd.data_ptr(), g.MgSolveOptions(tol=tol, max_cycles=cap))
-        torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
-        out["results"][name] = {"status": rep.status.name, "cycles": rep.iterations, "seconds": dt,
-                                "setup_seconds": setup, "levels": h.num_levels(),
-                                "final_rel_residual": float(rep.residual_history[-1] / np.abs(b).max())}
-        del h
+           "dtype": "f64", "data": "synthetic (BASELINE.json config 5 recipe, seed 4)",
+           "config": {"workload": f"config5: 2D -div(K grad u), {(1 << J) - 1}^2 vertices, {J - 4} levels to 31^2, "
+                                  "K = exp(N(0, sigma^2)) per unknown, harmonic faces, rediscretised levels "
+                                  "(log K coarsened by full weighting), rows scaled 1/h^2"},
+           "gpu": {}, "cpu_reference": {}}
+    for sigma in args.mg_sigmas:
+        levels, b = _mg_levels(g, J, sigma)
+        bd = torch.tensor(b, device="cuda")
+        xd = torch.zeros_like(bd)
+        tol = 1e-8 * float(np.abs(b).max())
+        for name, sm in (("gabp_red_black", g.MgSmoother.GabpRedBlack), ("gs_red_black", g.MgSmoother.GsRedBlack),
+                         ("gabp_flood", g.MgSmoother.GabpFlood)):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            h = g.Hierarchy.from_levels([p.A for p in levels], [p.nx for p in levels], sm)
+            torch.cuda.synchronize()
+            setup = time.perf_counter() - t0
+            spec = g.CycleSpec(2, 2, sm)
+            cap = args.mg_cycles if sm != g.MgSmoother.GabpFlood else min(args.mg_cycles, 40)
+            g.mg_solve_device(h, spec, bd.data_ptr(), xd.data_ptr(), g.MgSolveOptions(tol=tol, max_cycles=1))
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rep = g.mg_solve_device(h, spec, bd.data_ptr(), xd.data_ptr(), g.MgSolveOptions(tol=tol, max_cycles=cap))
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            out["gpu"][f"sigma{sigma}/{name}"] = {
+                "status": rep.status.name, "cycles": rep.iterations, "seconds": dt,
+                "ms_per_cycle": 1e3 * dt / max(rep.iterations, 1), "setup_seconds": setup, "levels": h.num_levels(),
+                "final_rel_residual": float(rep.residual_history[-1] / np.abs(b).max()), "detail": rep.detail}
+            del h
+    # the reference's V-cycle on the host (Eigen-free restatement of multigrid.cpp over the
+    # reference's own compiled GabpEngine), on a bounded sample: the same recipe at J = mg_cpu_J
+    if rank == 0 and not args.no_cpu_baseline:
+        from oracle.oracle import Csr, Oracle
+        o = Oracle.reference() or Oracle.restatement()
+        for sigma in args.mg_sigmas:
+            levels, b = _mg_levels(g, args.mg_cpu_J, sigma)
+            tol = 1e-8 * float(np.abs(b).max())
+            for name, sm in (("gabp_red_black", 1), ("gs_red_black", 7)):
+                t0 = time.perf_counter()
+                oh = o.hierarchy([Csr(p.A.n, p.A.row_offsets, p.A.col_indices, p.A.values) for p in levels],
+                                 [p.nx for p in levels], sm)
+                setup = time.perf_counter() - t0
+                t0 = time.perf_counter()
+                rep = oh.solve(2, 2, b, tol=tol, max_cycles=args.mg_cycles)
+                dt = time.perf_counter() - t0
+                out["cpu_reference"][f"J{args.mg_cpu_J}/sigma{sigma}/{name}"] = {
+                    "status": ["Converged", "Diverged", "MaxIter"][rep.status], "cycles": rep.iterations,
+                    "seconds": dt, "ms_per_cycle": 1e3 * dt / max(rep.iterations, 1), "setup_seconds": setup,
+                    "cores": 1, "kind": "reference" if o is Oracle.reference() else "port"}
+            if args.mg_cpu_J == J:
+                continue
+            # the GPU at the CPU's size too, for a like-for-like time-to-solution
+            lv2, b2 = _mg_levels(g, args.mg_cpu_J, sigma)
+            bd2 = torch.tensor(b2, device="cuda")
+            xd2 = torch.zeros_like(bd2)
+            for name, sm in (("gabp_red_black", g.MgSmoother.GabpRedBlack), ("gs_red_black", g.MgSmoother.GsRedBlack)):
+                h = g.Hierarchy.from_levels([p.A for p in lv2], [p.nx for p in lv2], sm)
+                tol2 = 1e-8 * float(np.abs(b2).max())
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                rep = g.mg_solve_device(h, g.CycleSpec(2, 2, sm), bd2.data_ptr(), xd2.data_ptr(),
+                                        g.MgSolveOptions(tol=tol2, max_cycles=args.mg_cycles))
+                torch.cuda.synchronize()
+                out["gpu"][f"J{args.mg_cpu_J}/sigma{sigma}/{name}"] = {
+                    "status": rep.status.name, "cycles": rep.iterations, "seconds": time.perf_counter() - t0}
+                del h
     if rank == 0:
         print(json.dumps(out), flush=True)
 
@@ -340,6 +384,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mg-J", type=int, default=12)
     ap.add_argument("--mg-cycles", type=int, default=100)
+    ap.add_argument("--mg-cpu-J", type=int, default=9)
+    ap.add_argument("--mg-sigmas", type=float, nargs="+", default=[2.0, 1.0])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

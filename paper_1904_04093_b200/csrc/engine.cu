@@ -304,14 +304,21 @@ std::vector<int> Engine::schedule_order(const bgabp_schedule& s) const {
 }
 
 const Levels& Engine::levels_for(const bgabp_schedule& s) {
+    // the cache key needs no O(n log n) order build except for custom orders (the multigrid
+    // smoother looks its levels up on every smoothing call)
     std::string key = std::to_string(s.kind) + ":" + std::to_string(s.nx) + "x" + std::to_string(s.ny);
-    std::vector<int> order = schedule_order(s);
-    if (s.kind == BGABP_SCHED_CUSTOM) {
-        key += ":";
-        for (int v : order) key += std::to_string(v) + ",";
+    if (s.kind == BGABP_SCHED_CUSTOM) {  // FNV-1a of the order; a hit is confirmed element-wise
+        unsigned long long hsh = 1469598103934665603ull;
+        for (int q = 0; q < n && s.order; ++q) hsh = (hsh ^ (unsigned)s.order[q]) * 1099511628211ull;
+        key += ":" + std::to_string(hsh);
     }
     auto it = level_cache.find(key);
-    if (it != level_cache.end()) return *it->second;
+    if (it != level_cache.end()) {
+        if (s.kind != BGABP_SCHED_CUSTOM || (s.order && std::equal(s.order, s.order + n, it->second->order.begin())))
+            return *it->second;
+        level_cache.erase(it);
+    }
+    std::vector<int> order = schedule_order(s);
     std::vector<int> pos(n), lev(n, 0);
     for (int q = 0; q < n; ++q) pos[order[q]] = q;
     int nlev = 0;

@@ -92,8 +92,9 @@ struct Engine {
     void build(int n, const int* ro, const int* ci, const double* v, int layout,
                cudaStream_t shared_stream = nullptr);
     std::vector<int> schedule_order(const bgabp_schedule& s) const;
-    void schedule_order_check(const bgabp_schedule& s) const {
-        if (s.kind != BGABP_SCHED_FLOOD) (void)schedule_order(s);
+    // validates the schedule (reference exceptions) and caches its levels
+    void schedule_order_check(const bgabp_schedule& s) {
+        if (s.kind != BGABP_SCHED_FLOOD) (void)levels_for(s);
     }
     const Levels& levels_for(const bgabp_schedule& s);
 
