@@ -141,7 +141,7 @@ def cpu_reference_rate(P, iters):
     dt = time.perf_counter() - t0
     assert rep.iterations == iters
     return {"value": E * iters / dt, "unit": UNIT, "cores": 1, "kind": kind,
-            "sample": f"{iters} solve iterations (flood sweep + residual, gabp.cpp:187-218) of the full config-2 "
+            "sample": f"{iters} solve iterations (flood sweep + residual, gabp.cpp:187-218) of the full {P.A.n}-unknown "
                       f"system, 1 thread (the reference is single-threaded), best of 1 after 1 warm-up iteration",
             "seconds": dt, "cpu": _cpu_name(), "nproc": os.cpu_count()}
 
@@ -160,8 +160,8 @@ def run_reference_arm(args, world, rank):
     if rank != 0:
         return
     import paper_1904_04093_b200 as g  # input generation only (host code, no device work)
-    P = g.config_problem(2)
-    iters = max(1, min(args.steps, args.ref_iters))
+    P = g.config_problem(args.config)
+    iters = max(1, min(args.steps, args.ref_iters if args.config != 4 else min(args.ref_iters, 4)))
     cb = cpu_reference_rate(P, iters)
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
             "steps": iters, "warmup": 1, "ms_per_step": cb["seconds"] * 1e3 / iters, "higher_is_better": True,
@@ -172,11 +172,19 @@ def run_reference_arm(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+WORKLOADS = {
+    2: "config2: poisson5 2048x2048, flood GaBP solve loop (sweep + residual + stop test per step)",
+    3: "config3: upwind convection-diffusion 1024x1024 (cell Peclet 2, theta 0.3), nonsymmetric flood GaBP solve loop",
+    4: "config4: 3D anisotropic lognormal diffusion 256^3 7-point, flood GaBP, fixed 300 sweeps",
+}
+
+
 def workload_config(P, args, eng_info=None):
     n = P.A.n
     E = int(P.A.nnz - n)
-    cfg = {"workload": "config2: poisson5 2048x2048, flood GaBP solve loop (sweep + residual + stop test per step)",
-           "n": n, "nnz": int(P.A.nnz), "edges": E, "tol": "1e-8*||b||_inf", "max_iter": 20000,
+    cfg = {"workload": WORKLOADS[args.config],
+           "n": n, "nnz": int(P.A.nnz), "edges": E, "tol": "1e-8*||b||_inf",
+           "max_iter": 300 if args.config == 4 else 20000,
            "l2": "inputs larger than L2: %.0f MB moved per sweep vs 126 MB L2" % ((40 * E + 24 * n) / 1e6),
            "parallelism": f"{args.gpus} independent replicas (one system per GPU)"}
     if eng_info:
@@ -193,7 +201,7 @@ def run_gpu(args, world, rank, local):
     import paper_1904_04093_b200 as g
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    P = g.config_problem(2)
+    P = g.config_problem(args.config)
     n = P.A.n
     eng = g.GabpEngine(P.A)
     E = eng.num_edges
@@ -260,6 +268,19 @@ def run_gpu(args, world, rank, local):
     h2d = 8 * n  # b per solve call
     d2h = 8 * n + 8 * (e2e_sweeps + 1)  # x + residual history per call
 
+    # ---- the configuration's own run: solve to 1e-8 (cap 20000) or the fixed 300 sweeps ---------
+    cap = 300 if args.config == 4 else 20000
+    tts = None
+    if args.config in (3, 4) or args.full_solve:
+        full_opt = g.GabpOptions(tol=0.0 if args.config == 4 else tol, max_iter=cap)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep = eng.solve(b_np, sched, full_opt)
+        t_full = time.perf_counter() - t0
+        tts = {"status": rep.status.name, "iterations": rep.iterations, "seconds": t_full,
+               "final_rel_residual": float(rep.residual_history[-1] / np.abs(P.b).max()),
+               "how": "one bgabp_solve call with host buffers (H2D b, D2H x + history included)"}
+
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE.json config 2: b ~ U[-1,1], seed 1)",
@@ -273,10 +294,16 @@ def run_gpu(args, world, rank, local):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / e2e_sweeps,
                     "d2h_bytes_per_step": d2h / e2e_sweeps,
                     "how": f"{args.e2e_calls} x bgabp_solve(host b, max_iter={e2e_sweeps}) incl. H2D b, D2H x + history"},
-            "gpu_launches": 3 * args.steps, "clocks": clk.summary()}
+            "gpu_launches": 2 * args.steps, "clocks": clk.summary()}
+    if tts is not None:
+        line["solve"] = tts
+    if args.config != 2:
+        line["data"] = f"synthetic (BASELINE.json config {args.config})"
+        line["roofline"]["kernel"] = line["roofline"]["kernel"].replace("<4>", f"<{info['num_slots']}>")
+        line["roofline"]["traffic"] = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cb = cpu_reference_rate(P, args.ref_iters)
+            cb = cpu_reference_rate(P, args.ref_iters if args.config != 4 else min(args.ref_iters, 4))
             line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as ex:  # the oracle is test infrastructure; its absence must not hide the GPU number
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "unavailable", "sample": str(ex)}
@@ -377,7 +404,8 @@ def main():
     ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="config2", choices=["config2", "mg"])
+    ap.add_argument("--workload", default="config2", choices=["config2", "config3", "config4", "mg"])
+    ap.add_argument("--full-solve", action="store_true", help="config 2: also run the capped 20000-sweep solve")
     ap.add_argument("--e2e-sweeps", type=int, default=500)
     ap.add_argument("--e2e-calls", type=int, default=3)
     ap.add_argument("--ref-iters", type=int, default=20)
@@ -388,6 +416,7 @@ def main():
     ap.add_argument("--mg-sigmas", type=float, nargs="+", default=[2.0, 1.0])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    args.config = int(args.workload[-1]) if args.workload.startswith("config") else 2
     if args.impl == "reference":
         world = int(os.environ.get("WORLD_SIZE", "1"))
         rank = int(os.environ.get("RANK", "0"))
