@@ -500,7 +500,14 @@ int Engine::sweep(const double* b, const bgabp_schedule& s, double* x, std::stri
     reset_ctrl();
     ck(cudaMemcpyAsync(d_b, b, sizeof(double) * n, cudaMemcpyHostToDevice, st), "H2D b");
     ck(cudaMemcpyAsync(d_x, x, sizeof(double) * n, cudaMemcpyHostToDevice, st), "H2D x");
-    launch_levels(L, d_b, d_msg[cur], d_x, false, nullptr, MODE_PLAIN);
+    if (rb_applicable(s)) {  // same visit, colour-compact storage (state converted around it)
+        rb_build(s.nx);
+        rb_state(true, d_msg[cur]);
+        launch_rb_sweep(d_b, d_x, false, false, nullptr, MODE_PLAIN);
+        rb_state(false, d_msg[cur]);
+    } else {
+        launch_levels(L, d_b, d_msg[cur], d_x, false, nullptr, MODE_PLAIN);
+    }
     ck(cudaGetLastError(), "level launch");
     ck(cudaMemcpyAsync(x, d_x, sizeof(double) * n, cudaMemcpyDeviceToHost, st), "D2H x");
     read_ctrl();
@@ -518,6 +525,8 @@ void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bga
     solve_flood = s.kind == BGABP_SCHED_FLOOD;
     solve_fused = solve_flood && layout == BGABP_LAYOUT_DIA;
     solve_levels = solve_flood ? nullptr : &levels_for(s);
+    solve_rb = !solve_flood && rb_applicable(s);
+    if (solve_rb) rb_build(s.nx);
     solve_b = b_dev;
     solve_stop = o.stop;
     solve_max_iter = o.max_iter;
@@ -537,6 +546,7 @@ void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bga
     ck(cudaMemsetAsync(d_x, 0, sizeof(double) * std::max(n, 1), st), "memset x");
     ck(cudaMemsetAsync(d_x2, 0, sizeof(double) * std::max(n, 1), st), "memset x");
     ck(cudaMemsetAsync(d_spread, 0, sizeof(unsigned long long) * 8 * kSpread, st), "memset");
+    if (solve_rb) ck(cudaMemsetAsync(d_rbmsg, 0, sizeof(double2) * 4 * (size_t)std::max(n, 2), st), "memset");
     cur = 0;
     if (n > 0) k_inf_norm<<<std::min<unsigned>(nblk(n), 1184), 256, 0, st>>>(b_dev, n, &d_ctrl->red[0]);
     k_solve_arm<<<1, 1, 0, st>>>(d_ctrl, d_hist);
@@ -577,8 +587,11 @@ void Engine::enqueue_step() {
         launch_residual(solve_b, d_x, nullptr, nullptr, MODE_SOLVE);
         k_solve_finalize<<<1, 1, 0, st>>>(d_ctrl, d_hist);
     } else {
-        launch_levels(*solve_levels, solve_b, d_msg[0], d_x, solve_stop == BGABP_STOP_MESSAGE_DELTA,
-                      &d_ctrl->delta[0], MODE_SOLVE);
+        if (solve_rb)
+            launch_rb_sweep(solve_b, d_x, false, solve_stop == BGABP_STOP_MESSAGE_DELTA, &d_ctrl->delta[0], MODE_SOLVE);
+        else
+            launch_levels(*solve_levels, solve_b, d_msg[0], d_x, solve_stop == BGABP_STOP_MESSAGE_DELTA,
+                          &d_ctrl->delta[0], MODE_SOLVE);
         launch_residual(solve_b, d_x, nullptr, nullptr, MODE_SOLVE_ORDERED);
         k_solve_finalize_ordered<<<1, 1, 0, st>>>(d_ctrl, d_hist);
     }
@@ -635,6 +648,10 @@ void Engine::solve_run_to_end() {
 }
 
 void Engine::solve_report(bgabp_report& rep, std::string& detail) {
+    if (solve_rb) {  // the handle's state stays in the natural layout between calls
+        rb_state(false, d_msg[0]);
+        cur = 0;
+    }
     read_ctrl();
     const Ctrl& c = *h_ctrl;
     rep.status = c.status;
@@ -801,20 +818,27 @@ int Engine::cold_sweeps_dev(const double* r_dev, const bgabp_schedule& s, int sw
     const Levels* L = flood ? nullptr : &levels_for(s);
     if (check) reset_ctrl();
     k_plain_reset<<<1, 1, 0, st>>>(d_ctrl);
-    for (int k = 0; k < 2; ++k)
-        ck(cudaMemsetAsync(d_msg[k], 0, sizeof(double2) * (size_t)std::max<long long>(nslots, 1), st), "memset");
-    ck(cudaMemsetAsync(e_dev, 0, sizeof(double) * std::max(n, 1), st), "memset");
-    cur = 0;
-    if (n == 0 || sweeps <= 0) return BGABP_OK;
-    if (flood) {
-        for (int k = 0; k < sweeps; ++k) {
-            launch_flood(r_dev, d_msg[cur], d_msg[cur ^ 1], nullptr, k == 0 ? MODE_PLAIN : MODE_PLAIN_X, false);
-            cur ^= 1;
-            k_plain_check<<<1, 1, 0, st>>>(d_ctrl, seq, 4);
-        }
-        launch_aggregate(r_dev, d_msg[cur], e_dev, nullptr, &d_ctrl->npiv[0]);
+    if (rb_applicable(s) && n > 0 && sweeps > 0) {
+        // colour-compact red-black: the cold first red phase reads no message, every later read
+        // slot has been written by then, and every sweep writes all of e -- nothing to clear
+        rb_build(s.nx);
+        for (int k = 0; k < sweeps; ++k) launch_rb_sweep(r_dev, e_dev, k == 0, false, nullptr, MODE_PLAIN);
     } else {
-        for (int k = 0; k < sweeps; ++k) launch_levels(*L, r_dev, d_msg[cur], e_dev, false, nullptr, MODE_PLAIN);
+        for (int k = 0; k < 2; ++k)
+            ck(cudaMemsetAsync(d_msg[k], 0, sizeof(double2) * (size_t)std::max<long long>(nslots, 1), st), "memset");
+        ck(cudaMemsetAsync(e_dev, 0, sizeof(double) * std::max(n, 1), st), "memset");
+        cur = 0;
+        if (n == 0 || sweeps <= 0) return BGABP_OK;
+        if (flood) {
+            for (int k = 0; k < sweeps; ++k) {
+                launch_flood(r_dev, d_msg[cur], d_msg[cur ^ 1], nullptr, k == 0 ? MODE_PLAIN : MODE_PLAIN_X, false);
+                cur ^= 1;
+                k_plain_check<<<1, 1, 0, st>>>(d_ctrl, seq, 4);
+            }
+            launch_aggregate(r_dev, d_msg[cur], e_dev, nullptr, &d_ctrl->npiv[0]);
+        } else {
+            for (int k = 0; k < sweeps; ++k) launch_levels(*L, r_dev, d_msg[cur], e_dev, false, nullptr, MODE_PLAIN);
+        }
     }
     k_plain_check<<<1, 1, 0, st>>>(d_ctrl, seq, 4);
     ck(cudaGetLastError(), "cold sweeps");

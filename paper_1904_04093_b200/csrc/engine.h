@@ -12,6 +12,7 @@
 
 #include "../../include/gabp_b200.h"
 #include "kernels.cuh"
+#include "rb_kernels.cuh"
 
 namespace bgabp {
 
@@ -78,6 +79,7 @@ struct Engine {
     bool solve_flood = true;
     bool solve_fused = false;
     const Levels* solve_levels = nullptr;
+    bool solve_rb = false;
     const double* solve_b = nullptr;
     int solve_stop = 0, solve_max_iter = 0;
     long long steps_enqueued = 0;
@@ -105,6 +107,16 @@ struct Engine {
                        unsigned long long* dslot, int mode);
     void launch_gs_levels(const Levels& L, const double* b, double* x);
     void launch_jacobi(const double* b, const double* x, double* xn);
+
+    // colour-compact red-black path (rb_kernels.cuh) for 5-point grids with odd nx
+    bool rb_ready = false;
+    int rb_nx = 0;
+    RbP rb{};
+    double2* d_rbmsg = nullptr;
+    bool rb_applicable(const bgabp_schedule& s) const;
+    void rb_build(int nx);
+    void launch_rb_sweep(const double* b, double* x, bool cold, bool delta, unsigned long long* dslot, int mode);
+    void rb_state(bool to_compact, double2* natural);
 
     void reset_ctrl();
     void read_ctrl();

@@ -1,0 +1,124 @@
+// Colour-compact red-black GaBP sweep for 5-point grids with an odd number of columns
+// (every multigrid level: 2^J - 1 points per axis), SURVEY.md §2.2 K2 specialised.
+//
+// With nx odd the red-black colour (ix+iy) mod 2 equals the parity of the natural index g, so
+// red node q is g = 2q and black node q is g = 2q+1, and every neighbour of a node sits at a
+// constant offset in the other colour's compact numbering:
+//     red q   -> black {q-(nx+1)/2, q-1, q, q+(nx-1)/2}     (natural offsets -nx, -1, +1, +nx)
+//     black q -> red   {q-(nx-1)/2, q, q+1, q+(nx+1)/2}
+// Messages and coefficients are stored per colour, slot-major ([4][n_colour]), so the red phase
+// and the black phase each read and write fully coalesced lines instead of every other element
+// of the natural-order arrays (the generic level kernel wastes half of every 32-byte sector).
+// Arithmetic is the reference's in-place visit (gabp.cpp:49-100) in natural CSR column order
+// (S, W, diagonal, E, N); the colour-grouped order of red_black_grid (schedule.cpp:78-83) visits
+// reds by ascending g, then blacks, so a node's pivot position is q (red) or n_red + q (black).
+#pragma once
+
+#include "kernels.cuh"
+
+namespace bgabp {
+
+struct RbP {
+    int nx, nR, nB;
+    const uint32_t* mask[2];  // [colour] DIA mask bits of the natural slots (-nx, -1, +1, +nx)
+    const double* c[2];       // [colour][4][n_c] A_{k,j} of the node's outgoing message per slot
+    const double* rowv[2];    // [colour][4][n_c] A_{j,k} (residual / GS), == c if symmetric
+    const double* diag[2];    // [colour][n_c]
+};
+
+__device__ __forceinline__ int rb_other(int colour, int q, int s, int nx) {
+    // compact index in the other colour of neighbour slot s of node q of `colour`
+    const int h = (nx - 1) / 2;
+    if (colour == 0) return s == 0 ? q - h - 1 : s == 1 ? q - 1 : s == 2 ? q : q + h;
+    return s == 0 ? q - h : s == 1 ? q : s == 2 ? q + 1 : q + h + 1;
+}
+
+// One colour phase of a red-black sweep.  COLD: first sweep of a cold start on the red phase
+// (every in-message is still zero, so none is read and no buffer has to be cleared).
+template <int COLOUR, bool COLD, bool DELTA>
+static __global__ void __launch_bounds__(256) k_rb_half(RbP P, const double* __restrict__ b, double2* mine,
+                                                       double2* other, double* __restrict__ x, Ctrl* ctrl,
+                                                       unsigned long long* dslot, int mode) {
+    if (mode == MODE_SOLVE && ld_ctrl(&ctrl->done)) return;
+    if (block_sees_failure(ctrl)) return;
+    const int nc = COLOUR == 0 ? P.nR : P.nB, no = COLOUR == 0 ? P.nB : P.nR;
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    double dmax = 0.0;
+    if (q < nc) {
+        const int g = 2 * q + COLOUR;
+        const uint32_t mk = P.mask[COLOUR][q];
+        const double dj = P.diag[COLOUR][q];
+        double sig = 0.0, acc = b[g];
+        double2 in[4];
+        double cc[4];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            in[s] = make_double2(0.0, 0.0);
+            cc[s] = 0.0;
+            if (!COLD && (mk & (1u << s))) in[s] = mine[s * nc + q];
+            if (mk & (1u << (16 + s))) cc[s] = __ldg(P.c[COLOUR] + s * nc + q);
+        }
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            if (s == 2) sig = dadd(sig, dj);
+            if (mk & (1u << s)) {
+                acc = dadd(acc, in[s].y);
+                if (mk & (1u << (16 + s))) sig = dadd(sig, dmul(in[s].x, cc[s]));
+            }
+        }
+        const unsigned long long pk = (unsigned long long)(COLOUR == 0 ? q : P.nR + q) << 32;
+        if (fabs(sig) < kPivotFloor) atomicMin(&ctrl->opiv, pk);
+        x[g] = ddiv(acc, sig);
+        const int off[4] = {-P.nx, -1, 1, P.nx};
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            if (!(mk & (1u << (16 + s)))) continue;
+            const double den = dsub(sig, dmul(in[s].x, cc[s]));
+            if (fabs(den) < kPivotFloor) atomicMin(&ctrl->opiv, pk | (unsigned)(g + off[s] + 1));
+            const double nl = ddiv(-cc[s], den);
+            const double nm = dmul(nl, dsub(acc, in[s].y));
+            double2* dst = other + (3 - s) * no + rb_other(COLOUR, q, s, P.nx);
+            if (DELTA) {
+                const double2 o = *dst;
+                dmax = fmax(dmax, fmax(nan_skip_abs(dsub(nl, o.x)), nan_skip_abs(dsub(nm, o.y))));
+            }
+            *dst = make_double2(nl, nm);
+        }
+    }
+    if (DELTA) warp_max_commit(dslot, dmax);
+}
+
+// colour-split copies of the DIA arrays (natural slots -nx, -1, +1, +nx)
+static __global__ void k_rb_split(int n, int nR, const uint32_t* __restrict__ mask, const double* __restrict__ c,
+                                  const double* __restrict__ rowv, const double* __restrict__ diag, uint32_t* mR,
+                                  uint32_t* mB, double* cR, double* cB, double* rR, double* rB, double* dR, double* dB) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    const int q = g >> 1, nB = n - nR;
+    const bool red = !(g & 1);
+    (red ? mR : mB)[q] = mask[g];
+    (red ? dR : dB)[q] = diag[g];
+    for (int s = 0; s < 4; ++s) {
+        (red ? cR : cB)[s * (red ? nR : nB) + q] = c[(size_t)s * n + g];
+        if (rR) (red ? rR : rB)[s * (red ? nR : nB) + q] = rowv[(size_t)s * n + g];
+    }
+}
+
+// message state natural DIA [4][n] <-> colour-compact ([4][nR] reds, then [4][nB] blacks)
+template <bool TO_COMPACT>
+static __global__ void k_rb_convert(int n, int nR, double2* nat, double2* cmp) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    const int q = g >> 1, nB = n - nR;
+    const bool red = !(g & 1);
+    double2* base = red ? cmp : cmp + 4 * (size_t)nR;
+    const int nc = red ? nR : nB;
+    for (int s = 0; s < 4; ++s) {
+        if (TO_COMPACT)
+            base[s * nc + q] = nat[(size_t)s * n + g];
+        else
+            nat[(size_t)s * n + g] = base[s * nc + q];
+    }
+}
+
+}  // namespace bgabp
