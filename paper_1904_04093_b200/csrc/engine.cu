@@ -559,20 +559,22 @@ void Engine::enqueue_step() {
         const bool dl = solve_stop == BGABP_STOP_MESSAGE_DELTA;
         const unsigned g = nblk(n);
         // register cap per slot count: 4 resident blocks for 2-4 slots, fewer for 6-8 (no spills)
-#define FUSED(SS_, MB_)                                                                                            \
+#define FUSED(SS_, MB_, DF_)                                                                                       \
     if (symmetric) {                                                                                               \
-        if (dl) k_flood_solve_dia<SS_, true, true, MB_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_x, d_x2, d_ctrl, d_spread); \
-        else k_flood_solve_dia<SS_, false, true, MB_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_x, d_x2, d_ctrl, d_spread); \
+        if (dl) k_flood_solve_dia<SS_, true, true, MB_, DF_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_x, d_x2, d_ctrl, d_spread); \
+        else k_flood_solve_dia<SS_, false, true, MB_, DF_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_x, d_x2, d_ctrl, d_spread); \
     } else {                                                                                                       \
-        if (dl) k_flood_solve_dia<SS_, true, false, MB_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_x, d_x2, d_ctrl, d_spread); \
-        else k_flood_solve_dia<SS_, false, false, MB_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_x, d_x2, d_ctrl, d_spread); \
+        if (dl) k_flood_solve_dia<SS_, true, false, MB_, DF_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_x, d_x2, d_ctrl, d_spread); \
+        else k_flood_solve_dia<SS_, false, false, MB_, DF_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_x, d_x2, d_ctrl, d_spread); \
     }
         if (timed_events) ck(cudaEventRecord((*timed_events)[2 * timed_index], st), "event");
+        // (resident blocks, deferred x loads) per slot count, from tools/exp_flood.cu on the B200:
+        // S=4 2048^2: (3, early) 133 us vs (4, deferred) 135; S=6 256^3: (4, deferred) 696 us vs (3, early) 725
         switch (S) {
-            case 2: FUSED(2, 4) break;
-            case 4: FUSED(4, 4) break;
-            case 6: FUSED(6, 3) break;
-            case 8: FUSED(8, 2) break;
+            case 2: FUSED(2, 4, true) break;
+            case 4: FUSED(4, 3, false) break;
+            case 6: FUSED(6, 4, true) break;
+            case 8: FUSED(8, 2, true) break;
             default: throw InvalidArg("gabp: unsupported DIA slot count");
         }
 #undef FUSED

@@ -293,3 +293,35 @@ def test_device_stepping_api_equals_host_solve(orc):
     status, its, _, _ = eng.solve_device_end(xd.data_ptr())
     assert (status, its) == (want.status, want.iterations)
     assert xd.cpu().numpy().tobytes() == want.solution.tobytes()
+
+
+@pytest.mark.parametrize("kind", ["chain", "mixed9", "general", "zeros4"])
+def test_fused_solve_every_slot_count(orc, ref, kind):
+    """The fused DIA solve step for S = 2 (1-D chain), 8 (9-point 'mixed' problem, nonsymmetric
+    'general' convection) and tiny explicit-zero matrices: whole solve report bit-identical."""
+    O = ref if ref is not None else orc
+    if kind == "chain":
+        n = 300
+        rows = [i for i in range(n) for _ in range(3)]
+        cols = [min(max(i + d, 0), n - 1) for i in range(n) for d in (-1, 0, 1)]
+        vals = [(2.5 if d == 0 else -1.0) for i in range(n) for d in (-1, 0, 1)]
+        A = orc.make_csr(n, rows, cols, vals)
+        b = orc.rng(2).vector(n)
+    elif kind == "zeros4":
+        from tests.cases import explicit_zeros
+        A = explicit_zeros(orc)
+        b = orc.rng(4).vector(4)
+    else:
+        p = g.assemble("mixed" if kind == "mixed9" else "general", 5)
+        from oracle.oracle import Csr
+        A = Csr(p.A.n, p.A.row_offsets, p.A.col_indices, p.A.values)
+        b = p.b
+    eng = g.GabpEngine(A)
+    tol = 1e-9 * np.abs(b).max()
+    for stop in (0, 1):
+        got = eng.solve(b, g.Schedule.parallel_flood(), g.GabpOptions(tol=tol, max_iter=4000, stop=stop))
+        want = O.engine(A).solve(b, OSched.parallel_flood(), tol=tol, max_iter=4000, stop=stop)
+        assert (int(got.status), got.iterations, got.detail) == (want.status, want.iterations, want.detail), kind
+        assert got.residual_history.tobytes() == want.residual_history.tobytes()
+        if want.status != 1:
+            assert got.solution.tobytes() == want.solution.tobytes()

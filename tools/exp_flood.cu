@@ -1,7 +1,8 @@
-// Tuning experiment (not part of the product): times the flood-sweep kernel variants of
-// paper_1904_04093_b200/csrc/kernels.cuh on poisson5(N,N) in the DIA layout.
+// Tuning experiment (not part of the product): times variants of the fused flood solve step of
+// paper_1904_04093_b200/csrc/kernels.cuh on a symmetric grid Laplacian in the DIA layout.
 //   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -fmad=false -o tools/exp_flood tools/exp_flood.cu
-//   tools/exp_flood [N]
+//   tools/exp_flood 2 2048      (2-D, 2048^2, S = 4)      tools/exp_flood 3 256   (3-D, 256^3, S = 6)
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -28,32 +29,48 @@ T* up(const std::vector<T>& v) {
     return d;
 }
 
-int main(int argc, char** argv) {
-    const int N = argc > 1 ? std::atoi(argv[1]) : 2048;
-    const int n = N * N, S = 4;
+template <int S>
+void run(int N) {
+    const int dims = S / 2;
+    long long nn = 1;
+    for (int d = 0; d < dims; ++d) nn *= N;
+    const int n = (int)nn;
     DiaP P;
     std::memset(&P, 0, sizeof(P));
     P.n = n;
     P.S = S;
-    P.nneg = 2;
-    const int off[4] = {-N, -1, 1, N};
-    for (int s = 0; s < 4; ++s) {
-        P.off[s] = off[s];
-        P.rev[s] = 3 - s;
+    P.nneg = S / 2;
+    std::vector<int> st;
+    int stride = 1;
+    for (int d = 0; d < dims; ++d) {
+        st.push_back(stride);
+        stride *= N;
+    }
+    for (int s = 0; s < S; ++s) {
+        P.off[s] = s < S / 2 ? -st[S / 2 - 1 - s] : st[s - S / 2];
+        P.rev[s] = S - 1 - s;
     }
     std::vector<uint32_t> mask(n);
-    std::vector<double> c((size_t)S * n, 0.0), diag(n, 4.0), b(n);
-    for (int iy = 0; iy < N; ++iy)
-        for (int ix = 0; ix < N; ++ix) {
-            const int j = iy * N + ix;
-            const bool ok[4] = {iy > 0, ix > 0, ix < N - 1, iy < N - 1};
-            for (int s = 0; s < 4; ++s)
-                if (ok[s]) {
-                    mask[j] |= (1u << s) | (1u << (16 + s));
-                    c[(size_t)s * n + j] = -1.0;
-                }
-            b[j] = std::sin(0.001 * j);
+    std::vector<double> c((size_t)S * n, 0.0), diag(n, 2.0 * dims + 0.01), b(n);
+    long long E = 0;
+    std::vector<int> co(dims);
+    for (int j = 0; j < n; ++j) {
+        int rem = j;
+        for (int d = 0; d < dims; ++d) {
+            co[d] = rem % N;
+            rem /= N;
         }
+        for (int s = 0; s < S; ++s) {
+            const int d = s < S / 2 ? (S / 2 - 1 - s) : (s - S / 2);
+            const bool ok = s < S / 2 ? co[d] > 0 : co[d] < N - 1;
+            if (ok) {
+                mask[j] |= (1u << s) | (1u << (16 + s));
+                c[(size_t)s * n + j] = -1.0;
+                ++E;
+            }
+        }
+        b[j] = std::sin(0.001 * j);
+    }
     P.mask = up(mask);
     P.c = up(c);
     P.rowv = P.c;
@@ -69,10 +86,10 @@ int main(int argc, char** argv) {
     CK(cudaMalloc(&x1, sizeof(double) * n));
     CK(cudaMalloc(&hist, sizeof(double) * 100000));
     Ctrl* ctrl;
-    unsigned int* arrive;
+    unsigned long long* spread;
     CK(cudaMalloc(&ctrl, sizeof(Ctrl)));
-    CK(cudaMalloc(&arrive, sizeof(unsigned int)));
-    CK(cudaMemset(arrive, 0, 4));
+    CK(cudaMalloc(&spread, 8 * 64 * 8));
+    CK(cudaMemset(spread, 0, 8 * 64 * 8));
     auto reset = [&]() {
         Ctrl h;
         std::memset(&h, 0, sizeof(h));
@@ -86,11 +103,11 @@ int main(int argc, char** argv) {
         CK(cudaMemcpy(ctrl, &h, sizeof(h), cudaMemcpyHostToDevice));
     };
     const unsigned g = (n + 255) / 256;
-    const double bytes = 40.0 * (4.0 * n - 4.0 * N) + 24.0 * n;
+    const double bytes = 40.0 * E + 32.0 * n;
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    const int steps = 60;
+    const int steps = 40;
     auto timeit = [&](const char* name, auto&& launch) {
         reset();
         for (int k = 0; k < 5; ++k) launch();
@@ -103,35 +120,33 @@ int main(int argc, char** argv) {
         float ms;
         cudaEventElapsedTime(&ms, e0, e1);
         const double us = ms * 1e3 / steps;
-        std::printf("%-58s %8.2f us/step  %7.1f GB/s (B_sweep)  %.3f of 6557\n", name, us, bytes / us / 1e3,
+        std::printf("S=%d %-44s %8.2f us/step  %7.1f GB/s  %.3f of 6557\n", S, name, us, bytes / us / 1e3,
                     bytes / us / 1e3 / 6557.4);
     };
-    int par = 0;
-    timeit("flood plain (x write), 256 thr", [&] {
-        k_flood_dia<4, false><<<g, 256>>>(P, db, par ? m1 : m0, par ? m0 : m1, x0, ctrl, MODE_PLAIN);
-        par ^= 1;
+#define W(NAME, MINB, DEFER, UNC)                                                                             \
+    timeit(NAME, [&] {                                                                                        \
+        k_flood_solve_dia<S, false, true, MINB, DEFER, true, false, UNC><<<g, 256>>>(P, db, m0, m1, x0, x1, \
+                                                                                    ctrl, spread);           \
+        k_solve_decide_lag2<<<1, 64>>>(ctrl, hist, spread);                                                   \
     });
-    timeit("residual alone", [&] { k_residual_dia<4><<<g, 256>>>(P, db, x0, nullptr, &ctrl->red[0], ctrl, MODE_PLAIN); });
-    unsigned long long* spread;
-    CK(cudaMalloc(&spread, 8 * 64 * 8));
-    CK(cudaMemset(spread, 0, 8 * 64 * 8));
-#define V(MINB, DEFER)                                                                                     \
-    timeit("fused MINB=" #MINB " DEFER=" #DEFER, [&] {                                                    \
-        k_flood_solve_dia<4, false, true, MINB, DEFER><<<g, 256>>>(P, db, m0, m1, x0, x1, ctrl, spread); \
-        k_solve_decide_lag2<<<1, 64>>>(ctrl, hist, spread);                                              \
-    });
-    V(4, true)
-    timeit("fused MINB=4 ASYNC", [&] {
-        k_flood_solve_dia<4, false, true, 4, true, true, true><<<g, 256>>>(P, db, m0, m1, x0, x1, ctrl, spread);
+    W("MINB=4 DEFER predicated", 4, true, false)
+    W("MINB=4 DEFER unconditional", 4, true, true)
+    W("MINB=3 DEFER unconditional", 3, true, true)
+    W("MINB=4 early-x unconditional", 4, false, true)
+    W("MINB=3 early-x unconditional", 3, false, true)
+    W("MINB=2 early-x unconditional", 2, false, true)
+    timeit("MINB=3 early-x unconditional DELTA", [&] {
+        k_flood_solve_dia<S, true, true, 3, false, true, false, true><<<g, 256>>>(P, db, m0, m1, x0, x1, ctrl, spread);
         k_solve_decide_lag2<<<1, 64>>>(ctrl, hist, spread);
     });
-    timeit("fused MINB=3 ASYNC", [&] {
-        k_flood_solve_dia<4, false, true, 3, true, true, true><<<g, 256>>>(P, db, m0, m1, x0, x1, ctrl, spread);
-        k_solve_decide_lag2<<<1, 64>>>(ctrl, hist, spread);
-    });
-    timeit("fused MINB=4 DELTA", [&] {
-        k_flood_solve_dia<4, true, true, 4, true><<<g, 256>>>(P, db, m0, m1, x0, x1, ctrl, spread);
-        k_solve_decide_lag2<<<1, 64>>>(ctrl, hist, spread);
-    });
+    cudaFree(m0);
+    cudaFree(m1);
+}
+
+int main(int argc, char** argv) {
+    const int dims = argc > 1 ? std::atoi(argv[1]) : 2;
+    const int N = argc > 2 ? std::atoi(argv[2]) : 2048;
+    if (dims == 2) run<4>(N);
+    if (dims == 3) run<6>(N);
     return 0;
 }
