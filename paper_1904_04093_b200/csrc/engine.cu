@@ -53,6 +53,9 @@ Engine::~Engine() {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     for (void* p : allocs) cudaFree(p);
     if (h_ctrl) cudaFreeHost(h_ctrl);
+    if (h_poll) cudaFreeHost(h_poll);
+    for (auto& e : poll_ev)
+        if (e) cudaEventDestroy(e);
     if (st && own_stream) cudaStreamDestroy(st);
 }
 
@@ -639,13 +642,34 @@ bool Engine::solve_done() {
 }
 
 void Engine::solve_run_to_end() {
-    // enqueue growing chunks until the device has decided (at most max_iter + 1 iterations)
-    int chunk = 16;
-    while (!solve_done()) {
-        const long long cap = (long long)solve_max_iter + (solve_fused ? 2 : 1) - steps_enqueued;
-        if (cap <= 0) throw CudaError("solve loop did not terminate");
-        solve_steps((int)std::min<long long>(chunk, cap));
-        chunk = std::min(chunk * 2, 512);
+    // Enqueue growing chunks until the device has decided (at most max_iter + 2 iterations).
+    // Two chunks stay queued: the host reads chunk k's stop flag (a 4-byte copy behind it) while
+    // chunk k+1 runs, so the GPU never idles on the poll.
+    if (!h_poll) {
+        ck(cudaMallocHost((void**)&h_poll, 2 * sizeof(int)), "cudaMallocHost");
+        for (auto& e : poll_ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    }
+    read_ctrl();
+    if (h_ctrl->done) return;
+    const long long total = (long long)solve_max_iter + (solve_fused ? 2 : 1);
+    int chunk = 16, inflight = 0, oldest = 0;
+    while (true) {
+        while (inflight < 2 && steps_enqueued < total) {
+            solve_steps((int)std::min<long long>(chunk, total - steps_enqueued));
+            const int sl = (oldest + inflight) & 1;
+            ck(cudaMemcpyAsync(&h_poll[sl], &d_ctrl->done, sizeof(int), cudaMemcpyDeviceToHost, st), "poll");
+            ck(cudaEventRecord(poll_ev[sl], st), "event");
+            ++inflight;
+            chunk = std::min(chunk * 2, 512);
+        }
+        if (inflight == 0) throw CudaError("solve loop did not terminate");
+        ck(cudaEventSynchronize(poll_ev[oldest]), "poll sync");
+        --inflight;
+        if (h_poll[oldest]) {
+            ck(cudaStreamSynchronize(st), "sync");
+            return;
+        }
+        oldest ^= 1;
     }
 }
 

@@ -83,6 +83,8 @@ struct Engine {
     const double* solve_b = nullptr;
     int solve_stop = 0, solve_max_iter = 0;
     long long steps_enqueued = 0;
+    int* h_poll = nullptr;  // pinned stop flags of the two chunks in flight (solve_run_to_end)
+    cudaEvent_t poll_ev[2] = {nullptr, nullptr};
     std::vector<cudaEvent_t>* timed_events = nullptr;  // bgabp_solve_device_steps_timed
     int timed_index = 0;
 

@@ -372,9 +372,10 @@ class GabpEngine:
     def sweep_flops(self):
         return lib().bgabp_sweep_flops(self._h)
 
-    def solve(self, b, sched: Schedule, opt: GabpOptions = GabpOptions()) -> SolveReport:
+    def solve(self, b, sched: Schedule, opt: GabpOptions = GabpOptions(), x_out=None) -> SolveReport:
+        """GabpEngine::solve (gabp.cpp:174-219).  x_out: optional caller buffer (e.g. pinned) for x."""
         n = self.A.n
-        x = np.zeros(n)
+        x = np.zeros(n) if x_out is None else x_out
         hist = np.zeros(max(opt.max_iter, 0) + 2)
         rep = _Rep()
         det = C.create_string_buffer(512)

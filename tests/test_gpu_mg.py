@@ -144,6 +144,26 @@ def test_mg_solve_matches_cpu_restatement(orc, ref, golden, prob, J1, J2, sm, pr
         assert (h.num_levels(), int(got.status), got.iterations) == (rec["levels"], rec["status"], rec["iterations"])
 
 
+@pytest.mark.parametrize("prob,sm,pre,post", [("poisson", S.GabpRedBlack, 1, 1), ("general", S.GabpRedBlack, 2, 2),
+                                              ("poisson", S.GabpSequential, 1, 1), ("poisson", S.GabpFlood, 2, 2),
+                                              ("mixed", S.GabpFourColor, 0, 4)])
+def test_frozen_cycle_matches_cpu_restatement(orc, ref, prob, sm, pre, post):
+    """CycleSpec.frozen (multigrid.cpp:177-178 -> correction_sweeps, gabp.cpp:289-325)."""
+    O = _oracle_for(ref, orc)
+    from oracle.oracle import Csr
+    levels = [g.assemble(prob, J) for J in (5, 4, 3)]
+    b = levels[0].b
+    oh = O.hierarchy([Csr(p.A.n, p.A.row_offsets, p.A.col_indices, p.A.values) for p in levels],
+                     [p.nx for p in levels], int(sm))
+    tol = 1e-8 * np.abs(b).max()
+    want = oh.solve(pre, post, b, tol=tol, max_cycles=60, frozen=True)
+    h = g.Hierarchy(prob, 5, 3, {}, sm)
+    assert [h.level_frozen_ok(k) for k in range(h.num_levels())] == [oh.frozen_ok(k) for k in range(oh.num_levels)]
+    got = g.mg_solve(h, g.CycleSpec(pre, post, sm, True), b, g.MgSolveOptions(tol=tol, max_cycles=60))
+    assert (int(got.status), got.iterations) == (want.status, want.iterations)
+    assert_close(got.residual_history, want.residual_history, "history", rel=1e-7)
+
+
 def test_single_v_cycle_matches_restatement_closely(orc, ref):
     """One V(2,2) red-black GaBP cycle from x=0: every smoothing sweep is bit-exact, only the
     coarsest solve differs in rounding."""
