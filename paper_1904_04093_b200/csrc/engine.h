@@ -119,6 +119,12 @@ struct Engine {
     void rb_build(int nx);
     void launch_rb_sweep(const double* b, double* x, bool cold, bool delta, unsigned long long* dslot, int mode);
     void rb_state(bool to_compact, double2* natural);
+    // cold smoothing with recorded lambda / sigma per sweep (multigrid smoother fast path)
+    std::vector<double*> rb_lamrec, rb_sigrec;
+    int rb_pre_sweeps = 0;
+    bool rb_pre_failed = false;
+    bool rb_precompute(int sweeps);
+    void rb_smooth_add(const double* r, int sweeps, double* x);
 
     void reset_ctrl();
     void read_ctrl();

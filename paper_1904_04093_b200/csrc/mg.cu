@@ -106,6 +106,11 @@ struct bgmg {
         ++seq;
         if (is_gabp(smoother)) {
             L.launch_residual(b, x, L.d_r, nullptr, MODE_PLAIN);
+            if (!(frozen && levels[k].frozen_ok) && L.rb_applicable(levels[k].sched) && L.rb_ready &&
+                L.rb_pre_sweeps >= sweeps) {
+                L.rb_smooth_add(L.d_r, sweeps, x);  // recorded lambda/sigma, x += e fused
+                return;
+            }
             if (frozen && levels[k].frozen_ok) {
                 L.correction_sweeps_dev(L.d_r, levels[k].sched, sweeps, L.d_e);
             } else {
@@ -176,7 +181,21 @@ struct bgmg {
         return msg;  // relax() throws its own message (classic.cpp:27,43)
     }
 
+    // record the cold-start precisions the cycle's smoothing calls need (once per level)
+    void prepare(const bgmg_cycle& spec) {
+        if (!is_gabp(smoother) || spec.frozen) return;
+        const int sw = std::max(spec.pre, spec.post);
+        if (sw <= 0) return;
+        for (int k = 0; k + 1 < nl(); ++k) {
+            Engine& L = E(k);
+            if (!L.rb_applicable(levels[k].sched)) continue;
+            L.rb_build(levels[k].sched.nx);
+            L.rb_precompute(sw);
+        }
+    }
+
     void v_cycle_dev(const bgmg_cycle& spec, const double* b, double* x) {
+        prepare(spec);
         clear_failures();
         cycle(0, spec, b, x);
         ck(cudaGetLastError(), "v-cycle");

@@ -66,6 +66,64 @@ void Engine::launch_rb_sweep(const double* b, double* x, bool cold, bool delta, 
     }
 }
 
+// Record lambda^(s), sigma^(s) of a cold red-black start for s = 1..sweeps (rb_kernels.cuh).
+// Returns false when the recursion breaks down within those sweeps (the caller then keeps the
+// full sweep, which reports the breakdown exactly where the reference does).
+bool Engine::rb_precompute(int sweeps) {
+    if (rb_pre_failed) return false;
+    if (rb_pre_sweeps >= sweeps) return true;
+    const size_t nd = (size_t)std::max(n, 2);
+    double* lam = static_cast<double*>(dalloc(sizeof(double) * 4 * nd));  // in-slot lambda, per colour
+    for (int s = (int)rb_lamrec.size(); s < sweeps; ++s) {
+        rb_lamrec.push_back(static_cast<double*>(dalloc(sizeof(double) * 4 * nd)));
+        rb_sigrec.push_back(static_cast<double*>(dalloc(sizeof(double) * nd)));
+    }
+    reset_ctrl();
+    const unsigned gr = nblk_host(rb.nR), gb = nblk_host(std::max(rb.nB, 1));
+    double* lR = lam;
+    double* lB = lam + 4 * (size_t)rb.nR;
+    for (int s = 0; s < sweeps; ++s) {
+        double* recR = rb_lamrec[s];
+        double* recB = rb_lamrec[s] + 4 * (size_t)rb.nR;
+        if (s == 0)
+            k_rb_lambda_half<0, true><<<gr, 256, 0, st>>>(rb, lR, lB, recR, rb_sigrec[s], d_ctrl);
+        else
+            k_rb_lambda_half<0, false><<<gr, 256, 0, st>>>(rb, lR, lB, recR, rb_sigrec[s], d_ctrl);
+        if (rb.nB > 0) k_rb_lambda_half<1, false><<<gb, 256, 0, st>>>(rb, lB, lR, recB, rb_sigrec[s] + rb.nR, d_ctrl);
+    }
+    ck(cudaGetLastError(), "rb precompute");
+    read_ctrl();
+    if (h_ctrl->opiv != kNone) {
+        rb_pre_failed = true;
+        return false;
+    }
+    rb_pre_sweeps = sweeps;
+    return true;
+}
+
+// e from `sweeps` cold red-black mean-only sweeps on A e = r, then x += e (multigrid.cpp:180-188)
+void Engine::rb_smooth_add(const double* r, int sweeps, double* x) {
+    if (n == 0 || sweeps <= 0) return;
+    double* mR = reinterpret_cast<double*>(d_rbmsg);
+    double* mB = mR + 4 * (size_t)rb.nR;
+    const unsigned gr = nblk_host(rb.nR), gb = nblk_host(std::max(rb.nB, 1));
+    for (int s = 0; s < sweeps; ++s) {
+        const bool first = s == 0, last = s + 1 == sweeps;
+        const double* recR = rb_lamrec[s];
+        const double* recB = rb_lamrec[s] + 4 * (size_t)rb.nR;
+        const double* sR = rb_sigrec[s];
+        const double* sB = rb_sigrec[s] + rb.nR;
+        if (first && last) k_rb_mean_half<0, true, true><<<gr, 256, 0, st>>>(rb, r, mR, mB, recR, sR, x);
+        else if (first) k_rb_mean_half<0, true, false><<<gr, 256, 0, st>>>(rb, r, mR, mB, recR, sR, x);
+        else if (last) k_rb_mean_half<0, false, true><<<gr, 256, 0, st>>>(rb, r, mR, mB, recR, sR, x);
+        else k_rb_mean_half<0, false, false><<<gr, 256, 0, st>>>(rb, r, mR, mB, recR, sR, x);
+        if (rb.nB > 0) {
+            if (last) k_rb_mean_half<1, false, true><<<gb, 256, 0, st>>>(rb, r, mB, mR, recB, sB, x);
+            else k_rb_mean_half<1, false, false><<<gb, 256, 0, st>>>(rb, r, mB, mR, recB, sB, x);
+        }
+    }
+}
+
 void Engine::rb_state(bool to_compact, double2* natural) {
     if (n == 0) return;
     if (to_compact)

@@ -104,6 +104,80 @@ static __global__ void k_rb_split(int n, int nR, const uint32_t* __restrict__ ma
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Cold smoothing with precomputed precisions ("optimisations that preserve bitwise
+// results"): Hierarchy::smooth restarts the messages at zero on every call (multigrid.cpp:180),
+// and the lambda recursion never reads the means, so lambda^(s) and sigma^(s) of sweep s of a
+// cold start depend on A alone.  They are recorded once per level (k_rb_lambda_half) and every
+// smoothing sweep then moves only the means: per edge 8 B in, 8 B lambda, 8 B out instead of
+// 16 + 8 + 16, with the values the reference computes bit for bit.
+// ---------------------------------------------------------------------------------------------
+
+// one colour phase of a cold lambda-only red-black sweep; records sigma of every visited node
+// (the x-stage divisor) and the lambda of every outgoing message, source-major
+template <int COLOUR, bool COLD>
+static __global__ void __launch_bounds__(256) k_rb_lambda_half(RbP P, double* lam_mine, double* lam_other,
+                                                              double* __restrict__ lam_rec,
+                                                              double* __restrict__ sig_rec, Ctrl* ctrl) {
+    const int nc = COLOUR == 0 ? P.nR : P.nB, no = COLOUR == 0 ? P.nB : P.nR;
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nc) return;
+    const int g = 2 * q + COLOUR;
+    const uint32_t mk = P.mask[COLOUR][q];
+    double sig = 0.0, in[4], cc[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        in[s] = (!COLD && (mk & (1u << s))) ? lam_mine[s * nc + q] : 0.0;
+        cc[s] = (mk & (1u << (16 + s))) ? __ldg(P.c[COLOUR] + s * nc + q) : 0.0;
+    }
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        if (s == 2) sig = dadd(sig, P.diag[COLOUR][q]);
+        if ((mk & (1u << s)) && (mk & (1u << (16 + s)))) sig = dadd(sig, dmul(in[s], cc[s]));
+    }
+    sig_rec[q] = sig;
+    const unsigned long long pk = (unsigned long long)(COLOUR == 0 ? q : P.nR + q) << 32;
+    if (fabs(sig) < kPivotFloor) atomicMin(&ctrl->opiv, pk);
+    const int off[4] = {-P.nx, -1, 1, P.nx};
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        double nl = 0.0;
+        if (mk & (1u << (16 + s))) {
+            const double den = dsub(sig, dmul(in[s], cc[s]));
+            if (fabs(den) < kPivotFloor) atomicMin(&ctrl->opiv, pk | (unsigned)(g + off[s] + 1));
+            nl = ddiv(-cc[s], den);
+            lam_other[(3 - s) * no + rb_other(COLOUR, q, s, P.nx)] = nl;
+        }
+        lam_rec[s * nc + q] = nl;
+    }
+}
+
+// one colour phase of a cold mean-only red-black sweep with the recorded lambda/sigma of this
+// sweep.  FIRST: the red phase of sweep 1 (no message read).  LAST: the last sweep of the call,
+// which folds Hierarchy::smooth's x += e (multigrid.cpp:188) into the visit; earlier sweeps
+// write no e at all (every visit overwrites it, only the last value is ever used).
+template <int COLOUR, bool FIRST, bool LAST>
+static __global__ void __launch_bounds__(256) k_rb_mean_half(RbP P, const double* __restrict__ r, double* m_mine,
+                                                            double* m_other, const double* __restrict__ lam_rec,
+                                                            const double* __restrict__ sig_rec, double* __restrict__ x) {
+    const int nc = COLOUR == 0 ? P.nR : P.nB, no = COLOUR == 0 ? P.nB : P.nR;
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nc) return;
+    const int g = 2 * q + COLOUR;
+    const uint32_t mk = P.mask[COLOUR][q];
+    double acc = r[g], in[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) in[s] = (!FIRST && (mk & (1u << s))) ? m_mine[s * nc + q] : 0.0;
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+        if (mk & (1u << s)) acc = dadd(acc, in[s]);
+    if (LAST) x[g] = dadd(x[g], ddiv(acc, sig_rec[q]));
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+        if (mk & (1u << (16 + s)))
+            m_other[(3 - s) * no + rb_other(COLOUR, q, s, P.nx)] = dmul(__ldg(lam_rec + s * nc + q), dsub(acc, in[s]));
+}
+
 // message state natural DIA [4][n] <-> colour-compact ([4][nR] reds, then [4][nB] blacks)
 template <bool TO_COMPACT>
 static __global__ void k_rb_convert(int n, int nR, double2* nat, double2* cmp) {
