@@ -204,6 +204,8 @@ typedef struct bgabp_problem bgabp_problem;
 bgabp_problem* bgabp_problem_named(const char* name, int J, int nparam, const char* const* keys,
                                    const double* vals, char* err, size_t errlen);
 bgabp_problem* bgabp_problem_poisson5(int nx, int ny);          /* tests/oracles.hpp:140-152 */
+/* load_matrix_market (sparse.cpp:123-180): coordinate real general|symmetric; NULL + err on error */
+bgabp_problem* bgabp_problem_matrix_market(const char* path, char* err, size_t errlen);
 bgabp_problem* bgabp_problem_config(int config, int size, unsigned seed); /* configs 2..5 */
 /* config-5 coarse level: same K field rule, level `k` below the finest (k=0 finest) */
 bgabp_problem* bgabp_problem_config5_level(int J_fine, int k, unsigned seed);

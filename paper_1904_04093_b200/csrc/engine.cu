@@ -92,14 +92,14 @@ void Engine::build(int n_, const int* ro_, const int* ci_, const double* v_, int
         const int* it = std::lower_bound(lo, hi, c);
         return (it != hi && *it == c) ? (long long)(it - ci.data()) : -1;
     };
-    symmetric = true;
+    int sym = 1;
+#pragma omp parallel for schedule(static) reduction(min : sym)
     for (int i = 0; i < n; ++i)
         for (int p = ro[i]; p < ro[i + 1]; ++p) {
             tpos[p] = find(ci[p], i);
-            if (tpos[p] < 0 || val[tpos[p]] != val[p] ||
-                std::memcmp(&val[tpos[p]], &val[p], sizeof(double)) != 0)
-                symmetric = false;
+            if (tpos[p] < 0 || std::memcmp(&val[tpos[p]], &val[p], sizeof(double)) != 0) sym = 0;
         }
+    symmetric = sym != 0;
 
     // union neighbour lists (row j and column j, sorted): the dependency graph of the schedules
     std::vector<int> ucount(n + 1, 0);
@@ -122,15 +122,20 @@ void Engine::build(int n_, const int* ro_, const int* ci_, const double* v_, int
             unbr[fill[i]++] = j;
             if (tpos[p] < 0) unbr[fill[j]++] = i;
         }
+#pragma omp parallel for schedule(static)
     for (int i = 0; i < n; ++i) std::sort(unbr.begin() + uptr[i], unbr.begin() + uptr[i + 1]);
 
     // offsets of the union structure decide the layout
     std::vector<int> offs;
     {
-        std::map<int, int> seen;
-        for (int i = 0; i < n && (int)seen.size() <= kMaxDia; ++i)
-            for (long long s = uptr[i]; s < uptr[i + 1]; ++s) seen[unbr[s] - i] = 1;
-        for (auto& kv : seen) offs.push_back(kv.first);
+        // distinct offsets, stopping at kMaxDia + 1 (a linear scan over <= 9 values per entry; a
+        // map insertion per entry took seconds on the 84M-entry config-5 level)
+        for (int i = 0; i < n && (int)offs.size() <= kMaxDia; ++i)
+            for (long long s = uptr[i]; s < uptr[i + 1]; ++s) {
+                const int d = unbr[s] - i;
+                if (std::find(offs.begin(), offs.end(), d) == offs.end()) offs.push_back(d);
+            }
+        std::sort(offs.begin(), offs.end());
     }
     const bool dia_ok = !offs.empty() && (int)offs.size() <= kMaxDia && offs.size() % 2 == 0;
     if (want_layout == BGABP_LAYOUT_DIA && !dia_ok)
@@ -156,28 +161,43 @@ void Engine::build(int n_, const int* ro_, const int* ci_, const double* v_, int
         dia.n = n;
         dia.S = S;
         dia.nneg = (int)(std::lower_bound(offs.begin(), offs.end(), 0) - offs.begin());
-        std::map<int, int> slot_of;
-        for (int s = 0; s < S; ++s) {
-            dia.off[s] = offs[s];
-            slot_of[offs[s]] = s;
-        }
-        for (int s = 0; s < S; ++s) dia.rev[s] = slot_of.at(-offs[s]);
+        for (int s = 0; s < S; ++s) dia.off[s] = offs[s];
+        auto slot_of = [&](int off) {  // <= 8 sorted offsets: a linear scan beats a map by far
+            int s = 0;
+            while (dia.off[s] != off) ++s;
+            return s;
+        };
+        for (int s = 0; s < S; ++s) dia.rev[s] = slot_of(-offs[s]);
         nslots = (long long)S * n;
         std::vector<uint32_t> mask(n, 0u);
         std::vector<double> c((size_t)nslots, 0.0), rowv;
         if (!symmetric) rowv.assign((size_t)nslots, 0.0);
-        for (int i = 0; i < n; ++i)
+        // per node i, everything it owns: in-edges j->i from row i (slot of j-i), out-edges i->k
+        // from column i (the transpose partner of a row entry, or a union neighbour outside row i)
+#pragma omp parallel for schedule(static)
+        for (int i = 0; i < n; ++i) {
+            uint32_t mk = 0u;
             for (int p = ro[i]; p < ro[i + 1]; ++p) {
                 const int j = ci[p];
                 if (j == i) continue;
-                // entry A_ij: in-edge j->i of node i (slot off=j-i), out-edge j->i of node j (slot off=i-j)
-                const int si = slot_of.at(j - i), sj = slot_of.at(i - j);
-                mask[i] |= 1u << si;
-                mask[j] |= 1u << (16 + sj);
-                c[(size_t)sj * n + j] = val[p];
+                const int si = slot_of(j - i);
+                mk |= 1u << si;
                 if (!symmetric) rowv[(size_t)si * n + i] = val[p];
                 csr2slot[p] = (long long)si * n + i;
+                if (tpos[p] >= 0) {
+                    mk |= 1u << (16 + si);
+                    c[(size_t)si * n + i] = val[tpos[p]];
+                }
             }
+            for (long long u = uptr[i]; u < uptr[i + 1]; ++u) {
+                const int k = unbr[u];
+                if (find(i, k) >= 0) continue;  // already handled through row i
+                const int sk = slot_of(k - i);
+                mk |= 1u << (16 + sk);
+                c[(size_t)sk * n + i] = val[find(k, i)];
+            }
+            mask[i] = mk;
+        }
         dia.mask = upload(mask);
         dia.c = upload(c);
         dia.rowv = symmetric ? dia.c : upload(rowv);
@@ -841,10 +861,11 @@ void Engine::correction_sweeps_dev(const double* r_dev, const bgabp_schedule& s,
 int Engine::cold_sweeps_dev(const double* r_dev, const bgabp_schedule& s, int sweeps, double* e_dev,
                             std::string& err, bool check, int seq) {
     const bool flood = s.kind == BGABP_SCHED_FLOOD;
-    const Levels* L = flood ? nullptr : &levels_for(s);
+    const bool rbp = rb_applicable(s) && n > 0 && sweeps > 0;
+    const Levels* L = (flood || (rbp && !check)) ? nullptr : &levels_for(s);
     if (check) reset_ctrl();
     k_plain_reset<<<1, 1, 0, st>>>(d_ctrl);
-    if (rb_applicable(s) && n > 0 && sweeps > 0) {
+    if (rbp) {
         // colour-compact red-black: the cold first red phase reads no message, every later read
         // slot has been written by then, and every sweep writes all of e -- nothing to clear
         rb_build(s.nx);
@@ -882,7 +903,9 @@ int Engine::cold_sweeps_dev(const double* r_dev, const bgabp_schedule& s, int sw
 bool Engine::sweeps_expand(const bgabp_schedule& s) {
     if (n == 0) return false;
     const bool flood = s.kind == BGABP_SCHED_FLOOD;
-    const Levels* L = flood ? nullptr : &levels_for(s);
+    const bool rbp = rb_applicable(s);
+    if (rbp) rb_build(s.nx);
+    const Levels* L = (flood || rbp) ? nullptr : &levels_for(s);
     unsigned long long* d_norms = static_cast<unsigned long long*>(dalloc(sizeof(unsigned long long) * 32));
     ck(cudaMemsetAsync(d_norms, 0, sizeof(unsigned long long) * 32, st), "memset");
     std::vector<double> ones(n, 1.0);
@@ -897,6 +920,8 @@ bool Engine::sweeps_expand(const bgabp_schedule& s) {
         if (flood) {
             launch_flood(d_ones, d_msg[cur], d_msg[cur ^ 1], nullptr, k == 0 ? MODE_PLAIN : MODE_PLAIN_X, false);
             cur ^= 1;
+        } else if (rbp) {  // colour-compact: max |m| over the same values, permuted
+            launch_rb_sweep(d_ones, d_e, k == 0, false, nullptr, MODE_PLAIN);
         } else {
             launch_levels(*L, d_ones, d_msg[cur], d_e, false, nullptr, MODE_PLAIN);
         }
@@ -905,7 +930,7 @@ bool Engine::sweeps_expand(const bgabp_schedule& s) {
             launch_aggregate(d_ones, d_msg[cur], d_e, nullptr, &d_ctrl->npiv[0]);
             k_plain_check<<<1, 1, 0, st>>>(d_ctrl, k, 4);
         }
-        k_max_abs_m<<<gr, 256, 0, st>>>(d_msg[cur], nslots, d_norms + k);
+        k_max_abs_m<<<gr, 256, 0, st>>>(rbp ? d_rbmsg : d_msg[cur], nslots, d_norms + k);
     }
     ck(cudaGetLastError(), "probe");
     unsigned long long hn[32];

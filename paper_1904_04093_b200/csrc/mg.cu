@@ -28,6 +28,7 @@ struct MgLevel {
     int nx = 0;
     bgabp_schedule sched{};
     bool frozen_ok = false;
+    bool frozen_pending = false;  // precompute_lambda deferred to first use
     double *d_b = nullptr, *d_x = nullptr;  // this level's right-hand side and iterate (coarse levels)
 };
 
@@ -181,8 +182,19 @@ struct bgmg {
         return msg;  // relax() throws its own message (classic.cpp:27,43)
     }
 
+    void ensure_frozen() {
+        for (auto& lv : levels) {
+            if (!lv.frozen_pending) continue;
+            int cv = 0, its = 0;
+            lv.E->precompute_lambda(lv.sched, 1e-10, 500, cv, its);  // multigrid.cpp:94-95
+            lv.frozen_ok = cv != 0;
+            lv.frozen_pending = false;
+        }
+    }
+
     // record the cold-start precisions the cycle's smoothing calls need (once per level)
     void prepare(const bgmg_cycle& spec) {
+        if (spec.frozen) ensure_frozen();
         if (!is_gabp(smoother) || spec.frozen) return;
         const int sw = std::max(spec.pre, spec.post);
         if (sw <= 0) return;
@@ -310,9 +322,10 @@ static void build_hierarchy(bgmg* h, int nlevels, const int* n, const int* const
                 h->levels.resize(k + 1);
                 break;
             }
-            int cv = 0, its = 0;
-            L.E->precompute_lambda(L.sched, 1e-10, 500, cv, its);  // multigrid.cpp:94-95
-            L.frozen_ok = cv != 0;
+            // multigrid.cpp:94-95 computes the frozen precisions here for every level it keeps
+            // before a truncation; they are only read by frozen cycles and level_frozen_ok, so
+            // they are computed on first use (bgmg::ensure_frozen) with the same values
+            L.frozen_pending = true;
         }
     }
     Engine& C = *h->levels.back().E;
@@ -380,7 +393,14 @@ int bgmg_create_named(const char* problem, int J1, int J2, int nparam, const cha
 
 void bgmg_destroy(bgmg* h) { delete h; }
 int bgmg_num_levels(const bgmg* h) { return (int)h->levels.size(); }
-int bgmg_level_frozen_ok(const bgmg* h, int k) { return h->levels[k].frozen_ok ? 1 : 0; }
+int bgmg_level_frozen_ok(const bgmg* h, int k) {
+    try {
+        const_cast<bgmg*>(h)->ensure_frozen();
+    } catch (const std::exception&) {
+        return -1;
+    }
+    return h->levels[k].frozen_ok ? 1 : 0;
+}
 int bgmg_level_n(const bgmg* h, int k) { return h->levels[k].E->n; }
 void* bgmg_stream(bgmg* h) { return (void*)h->st; }
 

@@ -12,6 +12,7 @@
 // drawn in unknown-index order, Gaussians first.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -443,6 +444,77 @@ bgabp_problem* bgabp_problem_named(const char* name, int J, int nparam, const ch
 }
 
 bgabp_problem* bgabp_problem_poisson5(int nx, int ny) { return poisson5_problem(nx, ny); }
+
+// Matrix Market coordinate real general|symmetric, square (sparse.cpp:123-180): 1-based entries,
+// symmetric files mirror off-diagonal entries, duplicates are summed in make_csr's order
+// (std::sort of the entry indices by (row, col), sparse.cpp:36-75).
+bgabp_problem* bgabp_problem_matrix_market(const char* path, char* err, size_t errlen) {
+    auto fail = [&](const std::string& m) -> bgabp_problem* {
+        if (err && errlen) std::snprintf(err, errlen, "%s", m.c_str());
+        return nullptr;
+    };
+    std::FILE* f = std::fopen(path, "r");
+    if (!f) return fail(std::string("cannot open ") + path);
+    std::unique_ptr<std::FILE, int (*)(std::FILE*)> guard(f, std::fclose);
+    char line[4096];
+    if (!std::fgets(line, sizeof line, f)) return fail(std::string("empty Matrix Market file: ") + path);
+    bool symmetric = false;
+    std::string first(line);
+    while (!first.empty() && (first.back() == '\n' || first.back() == '\r')) first.pop_back();
+    if (first.rfind("%%MatrixMarket", 0) == 0) {
+        char tag[64] = {0}, object[64] = {0}, format[64] = {0}, field[64] = {0}, symm[64] = {0};
+        std::sscanf(first.c_str(), "%63s %63s %63s %63s %63s", tag, object, format, field, symm);
+        if (std::string(object) != "matrix" || std::string(format) != "coordinate" || std::string(field) != "real")
+            return fail("unsupported Matrix Market header: " + first);
+        if (std::string(symm) == "symmetric")
+            symmetric = true;
+        else if (std::string(symm) != "general")
+            return fail("unsupported symmetry: " + std::string(symm));
+        if (!std::fgets(line, sizeof line, f)) return fail("truncated Matrix Market file");
+    }
+    while (line[0] == '%' || line[0] == '\n' || line[0] == '\r' || line[0] == 0)
+        if (!std::fgets(line, sizeof line, f)) return fail("truncated Matrix Market file");
+    long rows = 0, cols = 0, entries = 0;
+    if (std::sscanf(line, "%ld %ld %ld", &rows, &cols, &entries) != 3) return fail(std::string("bad size line: ") + line);
+    if (rows != cols) return fail("matrix is not square");
+    std::vector<int> ri, ci;
+    std::vector<double> vi;
+    for (long k = 0; k < entries; ++k) {
+        long i = 0, j = 0;
+        double v = 0.0;
+        if (std::fscanf(f, "%ld %ld %lf", &i, &j, &v) != 3) return fail("truncated entry list");
+        if (i < 1 || i > rows || j < 1 || j > cols) return fail("entry index out of bounds");
+        ri.push_back((int)(i - 1));
+        ci.push_back((int)(j - 1));
+        vi.push_back(v);
+        if (symmetric && i != j) {
+            ri.push_back((int)(j - 1));
+            ci.push_back((int)(i - 1));
+            vi.push_back(v);
+        }
+    }
+    std::vector<size_t> order(ri.size());
+    for (size_t k = 0; k < order.size(); ++k) order[k] = k;
+    std::sort(order.begin(), order.end(),
+              [&](size_t a, size_t b) { return ri[a] != ri[b] ? ri[a] < ri[b] : ci[a] < ci[b]; });
+    auto* P = new bgabp_problem;
+    P->n = (int)rows;
+    P->ro.assign(P->n + 1, 0);
+    int pr = -1, pc = -1;
+    for (size_t t : order) {
+        if (ri[t] == pr && ci[t] == pc) {
+            P->val.back() += vi[t];
+            continue;
+        }
+        pr = ri[t];
+        pc = ci[t];
+        P->ci.push_back(pc);
+        P->val.push_back(vi[t]);
+        ++P->ro[pr + 1];
+    }
+    for (int i = 0; i < P->n; ++i) P->ro[i + 1] += P->ro[i];
+    return P;
+}
 
 // BASELINE.json configs; size <= 0 selects the config's own size
 bgabp_problem* bgabp_problem_config(int config, int size, unsigned seed) {

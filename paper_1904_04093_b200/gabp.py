@@ -112,6 +112,7 @@ def lib():
             "bgabp_problem_named": (_vp, [C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_char_p), _dp, C.c_char_p,
                                           C.c_size_t]),
             "bgabp_problem_poisson5": (_vp, [C.c_int, C.c_int]),
+            "bgabp_problem_matrix_market": (_vp, [C.c_char_p, C.c_char_p, C.c_size_t]),
             "bgabp_problem_config": (_vp, [C.c_int, C.c_int, C.c_uint]),
             "bgabp_problem_config5_level": (_vp, [C.c_int, C.c_int, C.c_uint]),
             "bgabp_problem_varcoef2d_level": (_vp, [C.c_int, C.c_int, C.c_uint, C.c_double]),
@@ -649,6 +650,16 @@ def assemble(name, J, params=None) -> AssembledProblem:
     if not p:
         raise ValueError(err.value.decode())
     return _take_problem(p, 1.0 / (1 << J))
+
+
+def load_matrix_market(path) -> SparseMatrix:
+    """load_matrix_market (sparse.cpp:123-180): canonical CSR, duplicates summed."""
+    L = lib()
+    err = C.create_string_buffer(512)
+    p = L.bgabp_problem_matrix_market(str(path).encode(), err, 512)
+    if not p:
+        raise RuntimeError(err.value.decode())
+    return _take_problem(p).A
 
 
 def poisson5(nx, ny) -> SparseMatrix:
