@@ -198,6 +198,18 @@ void Engine::build(int n_, const int* ro_, const int* ci_, const double* v_, int
             }
             mask[i] = mk;
         }
+        // a 5-point grid in x-fastest order: offsets {-nx, -1, +1, +nx} and no edge that wraps
+        // from the end of one row to the start of the next (the pipelined sequential sweep
+        // relies on west/south being the only earlier neighbours)
+        if (S == 4 && dia.off[1] == -1 && dia.off[2] == 1 && dia.off[3] == -dia.off[0] && dia.off[3] > 1 &&
+            n % dia.off[3] == 0) {
+            const int gx = dia.off[3];
+            bool clean = true;
+            for (int i = 0; i < n && clean; i += gx)
+                if ((mask[i] & (2u | (2u << 16))) || (mask[i + gx - 1] & (4u | (4u << 16)))) clean = false;
+            grid5 = clean;
+            grid5_nx = gx;
+        }
         dia.mask = upload(mask);
         dia.c = upload(c);
         dia.rowv = symmetric ? dia.c : upload(rowv);
@@ -528,6 +540,8 @@ int Engine::sweep(const double* b, const bgabp_schedule& s, double* x, std::stri
         rb_state(true, d_msg[cur]);
         launch_rb_sweep(d_b, d_x, false, false, nullptr, MODE_PLAIN);
         rb_state(false, d_msg[cur]);
+    } else if (seq_applicable(s)) {  // lexicographic order on a 5-point grid: one pipelined launch
+        launch_seq_sweep(d_b, d_msg[cur], d_x, false, nullptr, MODE_PLAIN);
     } else {
         launch_levels(L, d_b, d_msg[cur], d_x, false, nullptr, MODE_PLAIN);
     }
@@ -549,6 +563,7 @@ void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bga
     solve_fused = solve_flood && layout == BGABP_LAYOUT_DIA;
     solve_levels = solve_flood ? nullptr : &levels_for(s);
     solve_rb = !solve_flood && rb_applicable(s);
+    solve_seq = !solve_flood && !solve_rb && seq_applicable(s);
     if (solve_rb) rb_build(s.nx);
     solve_b = b_dev;
     solve_stop = o.stop;
@@ -614,6 +629,9 @@ void Engine::enqueue_step() {
     } else {
         if (solve_rb)
             launch_rb_sweep(solve_b, d_x, false, solve_stop == BGABP_STOP_MESSAGE_DELTA, &d_ctrl->delta[0], MODE_SOLVE);
+        else if (solve_seq)
+            launch_seq_sweep(solve_b, d_msg[0], d_x, solve_stop == BGABP_STOP_MESSAGE_DELTA, &d_ctrl->delta[0],
+                             MODE_SOLVE);
         else
             launch_levels(*solve_levels, solve_b, d_msg[0], d_x, solve_stop == BGABP_STOP_MESSAGE_DELTA,
                           &d_ctrl->delta[0], MODE_SOLVE);
@@ -627,7 +645,7 @@ void Engine::solve_steps(int nsteps) {
     // graph-replay chunks of iterations: the kernels read their step index from the device,
     // so one captured chunk is valid for any position in the loop
     const size_t per_step = solve_fused ? 2 : solve_flood ? 3 : solve_levels->ptr.size() + 1;
-    const bool use_graph = per_step * 16 <= 4096 && n > 0;
+    const bool use_graph = per_step * 16 <= 4096 && n > 0 && !solve_seq;  // cooperative launches stay out of graphs
     int left = nsteps;
     while (left > 0) {
         const int chunk = use_graph ? std::min(left, 16) : left;
@@ -883,6 +901,8 @@ int Engine::cold_sweeps_dev(const double* r_dev, const bgabp_schedule& s, int sw
                 k_plain_check<<<1, 1, 0, st>>>(d_ctrl, seq, 4);
             }
             launch_aggregate(r_dev, d_msg[cur], e_dev, nullptr, &d_ctrl->npiv[0]);
+        } else if (seq_applicable(s)) {
+            for (int k = 0; k < sweeps; ++k) launch_seq_sweep(r_dev, d_msg[cur], e_dev, false, nullptr, MODE_PLAIN);
         } else {
             for (int k = 0; k < sweeps; ++k) launch_levels(*L, r_dev, d_msg[cur], e_dev, false, nullptr, MODE_PLAIN);
         }

@@ -13,6 +13,7 @@
 #include "../../include/gabp_b200.h"
 #include "kernels.cuh"
 #include "rb_kernels.cuh"
+#include "seq_kernels.cuh"
 
 namespace bgabp {
 
@@ -80,6 +81,7 @@ struct Engine {
     bool solve_fused = false;
     const Levels* solve_levels = nullptr;
     bool solve_rb = false;
+    bool solve_seq = false;
     const double* solve_b = nullptr;
     int solve_stop = 0, solve_max_iter = 0;
     long long steps_enqueued = 0;
@@ -125,6 +127,14 @@ struct Engine {
     bool rb_pre_failed = false;
     bool rb_precompute(int sweeps);
     void rb_smooth_add(const double* r, int sweeps, double* x);
+    // pipelined lexicographic sweep on 5-point grids (seq_kernels.cuh)
+    bool grid5 = false;  // DIA offsets {-nx,-1,+1,+nx} with no wrap-around edges at row ends
+    int grid5_nx = 0;
+    int* d_progress = nullptr;
+    bool seq_applicable(const bgabp_schedule& s) const {
+        return grid5 && s.kind == BGABP_SCHED_SEQUENTIAL && n > 0;
+    }
+    void launch_seq_sweep(const double* b, double2* msg, double* x, bool delta, unsigned long long* dslot, int mode);
 
     void reset_ctrl();
     void read_ctrl();
