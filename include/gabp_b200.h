@@ -138,6 +138,29 @@ int bgabp_solve_device_steps_timed(bgabp_engine* e, int nsteps, double* hot_ms);
  * is written to the handle's x buffer): the sweep kernel alone. */
 int bgabp_flood_sweeps_device(bgabp_engine* e, const double* b_dev, int nsweeps);
 
+/* ---- sharded flood solve (one contiguous row block per rank; no reference counterpart: the
+ * reference is single-process, gabp.cpp:174-219 is the loop these steps split) -----------------
+ * The handle holds the block's local matrix (owned rows + ghost rows, DIA layout).  set_range
+ * restricts the fused step to the owned local nodes [own_lo, own_hi) and adds gofs (the global
+ * index of local node 0) to the pivot keys.  Per iteration the driver calls step_compute, MAX
+ * all-reduces the 4 int64 words at reduce_buffer across ranks, calls step_decide (the reference's
+ * stop rule on the combined words, identical on every rank), then exchanges halos:
+ * pack(which = t&1) the in-slot messages of the neighbour's nodes, unpack them on the neighbour
+ * (only slots whose sender lies in [sender_lo, sender_hi)), and copy x buffer (t-1)&1 of owned
+ * nodes into the neighbour's ghost range.  Every call is stream-ordered on bgabp_stream(e); r0 is
+ * the global ||b||_inf.  End with bgabp_solve_device_end.  Pointers are device pointers. */
+int bgabp_shard_set_range(bgabp_engine* e, int own_lo, int own_hi, int gofs);
+int bgabp_shard_solve_begin(bgabp_engine* e, const double* b_dev, const bgabp_options* opt, double r0);
+int bgabp_shard_step_compute(bgabp_engine* e);
+void* bgabp_shard_reduce_buffer(bgabp_engine* e);
+int bgabp_shard_step_decide(bgabp_engine* e);
+void* bgabp_shard_msg(bgabp_engine* e, int which);
+void* bgabp_shard_x(bgabp_engine* e, int which);
+int bgabp_shard_pack(bgabp_engine* e, int which, int lo, int len, void* out_dev);
+int bgabp_shard_unpack(bgabp_engine* e, int which, const void* recv_dev, int lo, int len, int sender_lo,
+                       int sender_hi);
+int bgabp_shard_state(bgabp_engine* e, int* done, int* step);
+
 /* residual_inf_norm(A, x, b) (sparse.cpp:104-115) on the handle's matrix */
 int bgabp_residual_inf_norm(bgabp_engine* e, const double* x, const double* b, double* out);
 

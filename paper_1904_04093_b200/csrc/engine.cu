@@ -160,6 +160,9 @@ void Engine::build(int n_, const int* ro_, const int* ci_, const double* v_, int
         std::memset(&dia, 0, sizeof(dia));
         dia.n = n;
         dia.S = S;
+        dia.j0 = 0;
+        dia.j1 = n;
+        dia.gofs = 0;
         dia.nneg = (int)(std::lower_bound(offs.begin(), offs.end(), 0) - offs.begin());
         for (int s = 0; s < S; ++s) dia.off[s] = offs[s];
         auto slot_of = [&](int off) {  // <= 8 sorted offsets: a linear scan beats a map by far
@@ -558,7 +561,8 @@ int Engine::sweep(const double* b, const bgabp_schedule& s, double* x, std::stri
 // ---------------------------------------------------------------------------------------------
 // solve (gabp.cpp:174-219): device-resident loop, stop logic in k_solve_finalize*
 // ---------------------------------------------------------------------------------------------
-void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bgabp_options& o) {
+void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bgabp_options& o,
+                         const double* r0_override) {
     solve_flood = s.kind == BGABP_SCHED_FLOOD;
     solve_fused = solve_flood && layout == BGABP_LAYOUT_DIA;
     solve_levels = solve_flood ? nullptr : &levels_for(s);
@@ -586,7 +590,14 @@ void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bga
     ck(cudaMemsetAsync(d_spread, 0, sizeof(unsigned long long) * 8 * kSpread, st), "memset");
     if (solve_rb) ck(cudaMemsetAsync(d_rbmsg, 0, sizeof(double2) * 4 * (size_t)std::max(n, 2), st), "memset");
     cur = 0;
-    if (n > 0) k_inf_norm<<<std::min<unsigned>(nblk(n), 1184), 256, 0, st>>>(b_dev, n, &d_ctrl->red[0]);
+    if (r0_override) {  // sharded solve: ||b||_inf over all ranks, supplied by the driver
+        unsigned long long bits;
+        std::memcpy(&bits, r0_override, sizeof bits);
+        ck(cudaMemcpyAsync(&d_ctrl->red[0], &bits, sizeof bits, cudaMemcpyHostToDevice, st), "r0");
+        ck(cudaStreamSynchronize(st), "sync");
+    } else if (n > 0) {
+        k_inf_norm<<<std::min<unsigned>(nblk(n), 1184), 256, 0, st>>>(b_dev, n, &d_ctrl->red[0]);
+    }
     k_solve_arm<<<1, 1, 0, st>>>(d_ctrl, d_hist);
     ck(cudaGetLastError(), "solve arm");
     steps_enqueued = 0;
@@ -594,8 +605,17 @@ void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bga
 
 void Engine::enqueue_step() {
     if (solve_fused) {
+        enqueue_fused_kernel();
+        k_solve_decide_lag2<<<1, kSpread, 0, st>>>(d_ctrl, d_hist, d_spread);
+        return;
+    }
+    enqueue_step_other();
+}
+
+void Engine::enqueue_fused_kernel() {
+    {
         const bool dl = solve_stop == BGABP_STOP_MESSAGE_DELTA;
-        const unsigned g = nblk(n);
+        const unsigned g = nblk(std::max(dia.j1 - dia.j0, 1));
         // register cap per slot count: 4 resident blocks for 2-4 slots, fewer for 6-8 (no spills)
 #define FUSED(SS_, MB_, DF_)                                                                                       \
     if (symmetric) {                                                                                               \
@@ -617,9 +637,10 @@ void Engine::enqueue_step() {
         }
 #undef FUSED
         if (timed_events) ck(cudaEventRecord((*timed_events)[2 * timed_index + 1], st), "event");
-        k_solve_decide_lag2<<<1, kSpread, 0, st>>>(d_ctrl, d_hist, d_spread);
-        return;
     }
+}
+
+void Engine::enqueue_step_other() {
     if (solve_flood) {
         if (timed_events) ck(cudaEventRecord((*timed_events)[2 * timed_index], st), "event");
         launch_flood(solve_b, d_msg[0], d_msg[1], d_x, MODE_SOLVE, solve_stop == BGABP_STOP_MESSAGE_DELTA);
@@ -739,9 +760,18 @@ void Engine::solve_report(bgabp_report& rep, std::string& detail) {
     for (int k = 0; k < c.iterations - (pivot ? 1 : 0); ++k) rep.flop_estimate += per_iter;
 }
 
-const double* Engine::solve_x() const {
+const double* Engine::solve_x() {
     if (!solve_fused) return d_x;
-    return (h_ctrl->solx & 1) ? d_x2 : d_x;
+    const Ctrl& c = *h_ctrl;  // read by solve_report
+    const double* xs = (c.solx & 1) ? d_x2 : d_x;
+    if (c.status == BGABP_DIVERGED && c.detail_kind == 1 && n > 0) {
+        // the reference stops its x-stage at the pivot node: x(k) below it, x(k-1) from it on
+        const double* xo = (c.solx & 1) ? d_x : d_x2;
+        k_compose_pivot_x<<<nblk(n), 256, 0, st>>>(xs, xo, d_aux, n, (long long)c.detail_key - dia.gofs);
+        ck(cudaGetLastError(), "compose x");
+        return d_aux;
+    }
+    return xs;
 }
 
 double Engine::sweep_flops() const {  // gabp.cpp:165-172
@@ -1346,6 +1376,88 @@ int bgabp_solve_error_correction(bgabp_engine* h, const double* b, const bgabp_s
         ck(cudaStreamSynchronize(E.st), "sync");
         if (history) std::memcpy(history, hist.data(), sizeof(double) * hist.size());
         put_err(detail, dl, d);
+        return BGABP_OK;
+    })
+}
+
+// ---- sharded flood solve (one row block per rank; the driver moves halos and reduces) ---------
+int bgabp_shard_set_range(bgabp_engine* h, int own_lo, int own_hi, int gofs) {
+    ABI_GUARD(nullptr, 0, {
+        Engine& E = h->E;
+        if (E.layout != BGABP_LAYOUT_DIA) throw InvalidArg("shard: DIA layout required");
+        if (own_lo < 0 || own_hi > E.n || own_lo > own_hi) throw InvalidArg("shard: bad owned range");
+        E.dia.j0 = own_lo;
+        E.dia.j1 = own_hi;
+        E.dia.gofs = gofs;
+        if (!E.d_red4) E.d_red4 = static_cast<unsigned long long*>(E.dalloc(sizeof(unsigned long long) * 4));
+        if (!E.d_pack) {
+            E.pack_cap = 0;
+        }
+        return BGABP_OK;
+    })
+}
+
+int bgabp_shard_solve_begin(bgabp_engine* h, const double* b_dev, const bgabp_options* opt, double r0) {
+    ABI_GUARD(nullptr, 0, {
+        bgabp_schedule fl{};
+        fl.kind = BGABP_SCHED_FLOOD;
+        h->E.solve_begin(b_dev, fl, *opt, &r0);
+        return BGABP_OK;
+    })
+}
+
+int bgabp_shard_step_compute(bgabp_engine* h) {
+    ABI_GUARD(nullptr, 0, {
+        Engine& E = h->E;
+        if (!E.solve_fused || !E.d_red4) throw InvalidArg("shard: call set_range and shard_solve_begin first");
+        E.enqueue_fused_kernel();
+        k_shard_fold<<<1, kSpread, 0, E.st>>>(E.d_ctrl, E.d_spread, E.d_red4);
+        ck(cudaGetLastError(), "shard compute");
+        return BGABP_OK;
+    })
+}
+
+void* bgabp_shard_reduce_buffer(bgabp_engine* h) { return (void*)h->E.d_red4; }
+
+int bgabp_shard_step_decide(bgabp_engine* h) {
+    ABI_GUARD(nullptr, 0, {
+        Engine& E = h->E;
+        k_shard_decide<<<1, 1, 0, E.st>>>(E.d_ctrl, E.d_hist, E.d_red4);
+        ck(cudaGetLastError(), "shard decide");
+        return BGABP_OK;
+    })
+}
+
+void* bgabp_shard_msg(bgabp_engine* h, int which) { return (void*)h->E.d_msg[which & 1]; }
+void* bgabp_shard_x(bgabp_engine* h, int which) { return (void*)((which & 1) ? h->E.d_x2 : h->E.d_x); }
+
+int bgabp_shard_pack(bgabp_engine* h, int which, int lo, int len, void* out_dev) {
+    ABI_GUARD(nullptr, 0, {
+        Engine& E = h->E;
+        if (len > 0)
+            k_shard_pack<<<nblk(len), 256, 0, E.st>>>(E.dia, E.d_msg[which & 1], static_cast<double2*>(out_dev), lo, len);
+        ck(cudaGetLastError(), "shard pack");
+        return BGABP_OK;
+    })
+}
+
+int bgabp_shard_unpack(bgabp_engine* h, int which, const void* recv_dev, int lo, int len, int sender_lo,
+                       int sender_hi) {
+    ABI_GUARD(nullptr, 0, {
+        Engine& E = h->E;
+        if (len > 0)
+            k_shard_unpack<<<nblk(len), 256, 0, E.st>>>(E.dia, E.d_msg[which & 1], static_cast<const double2*>(recv_dev),
+                                                        lo, len, sender_lo, sender_hi);
+        ck(cudaGetLastError(), "shard unpack");
+        return BGABP_OK;
+    })
+}
+
+int bgabp_shard_state(bgabp_engine* h, int* done, int* step) {
+    ABI_GUARD(nullptr, 0, {
+        h->E.read_ctrl();
+        *done = h->E.h_ctrl->done;
+        *step = h->E.h_ctrl->step;
         return BGABP_OK;
     })
 }

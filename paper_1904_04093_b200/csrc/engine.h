@@ -143,13 +143,19 @@ struct Engine {
 
     int sweep(const double* b, const bgabp_schedule& s, double* x, std::string& err);
 
-    void solve_begin(const double* b_dev, const bgabp_schedule& s, const bgabp_options& o);
+    void solve_begin(const double* b_dev, const bgabp_schedule& s, const bgabp_options& o,
+                     const double* r0_override = nullptr);
     void enqueue_step();
+    void enqueue_fused_kernel();  // the fused DIA flood step alone (solve loop and sharded steps)
+    void enqueue_step_other();
+    unsigned long long* d_red4 = nullptr;  // sharded solve: this rank's four reduction words
+    void* d_pack = nullptr;
+    long long pack_cap = 0;
     void solve_steps(int nsteps);
     bool solve_done();
     void solve_run_to_end();
     void solve_report(bgabp_report& rep, std::string& detail);
-    const double* solve_x() const;
+    const double* solve_x();  // after solve_report (composes the node-pivot x on the fused path)
     double sweep_flops() const;
 
     void ensure_frozen_buffers();

@@ -125,6 +125,16 @@ def lib():
             "bgabp_problem_values": (_dp, [_vp]),
             "bgabp_problem_rhs": (_dp, [_vp]),
             "bgabp_problem_exact": (_dp, [_vp]),
+            "bgabp_shard_set_range": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int]),
+            "bgabp_shard_solve_begin": (C.c_int, [_vp, _vp, C.POINTER(_Opts), C.c_double]),
+            "bgabp_shard_step_compute": (C.c_int, [_vp]),
+            "bgabp_shard_reduce_buffer": (_vp, [_vp]),
+            "bgabp_shard_step_decide": (C.c_int, [_vp]),
+            "bgabp_shard_msg": (_vp, [_vp, C.c_int]),
+            "bgabp_shard_x": (_vp, [_vp, C.c_int]),
+            "bgabp_shard_pack": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _vp]),
+            "bgabp_shard_unpack": (C.c_int, [_vp, C.c_int, _vp, C.c_int, C.c_int, C.c_int, C.c_int]),
+            "bgabp_shard_state": (C.c_int, [_vp, _ip, _ip]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)

@@ -1,0 +1,259 @@
+"""Sharded synchronous GaBP solve: one contiguous row block per shard.
+
+Each shard holds its owned rows plus ghost rows (halo width H = the largest neighbour offset)
+and runs the fused flood step of the single-GPU solve (K1+K4) on its owned nodes only.  Per
+iteration t:
+
+    compute   sweep t + residual of x(t-2) on owned nodes, folded into 4 int64 words
+    reduce    MAX all-reduce of those words (residual, message delta, encoded edge / node pivot)
+    decide    the reference's stop logic (gabp.cpp:187-218) on the combined words, on every shard
+    exchange  halo in-slot messages of sweep t and halo x(t-1) with the neighbouring shards
+
+so every shard takes the same decision at the same iteration and the solve is bit-identical to
+the single-engine one.  The transport is torch.distributed (NCCL between GPUs; gloo in the CPU
+tests); shards of one process exchange by copies.  The compute side is the CUDA engine
+(`GpuShard`); tests/shard_emu.py is a numpy stand-in with the same interface so this driver is
+tested with world_size 2 over gloo on the CPU.
+"""
+from __future__ import annotations
+
+import contextlib
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from .gabp import GabpEngine, GabpOptions, Layout, SparseMatrix, _raise, lib
+
+
+@dataclass
+class ShardLayout:
+    """Global rows [lo, hi) owned by shard `index`; local arrays cover [glo, ghi) (ghosts around)."""
+    index: int
+    count: int
+    n: int
+    lo: int
+    hi: int
+    glo: int
+    ghi: int
+
+    @property
+    def n_local(self):
+        return self.ghi - self.glo
+
+    @property
+    def own_lo(self):
+        return self.lo - self.glo
+
+    @property
+    def own_hi(self):
+        return self.hi - self.glo
+
+    @staticmethod
+    def partition(n, halo, count, align=1):
+        """`count` contiguous blocks of whole `align`-node units (e.g. grid rows), each >= halo."""
+        units = n // align
+        if units * align != n:
+            raise ValueError("n is not a multiple of align")
+        bounds = [(units * k) // count * align for k in range(count + 1)]
+        out = []
+        for k in range(count):
+            lo, hi = bounds[k], bounds[k + 1]
+            if hi - lo < halo:
+                raise ValueError(f"shard {k} owns {hi - lo} nodes, fewer than the halo {halo}")
+            out.append(ShardLayout(k, count, n, lo, hi, max(0, lo - halo), min(n, hi + halo)))
+        return out
+
+
+def dia_halo(A: SparseMatrix):
+    """Largest |column - row| of A: the halo a row block needs."""
+    rows = np.repeat(np.arange(A.n), np.diff(A.row_offsets))
+    return int(np.max(np.abs(A.col_indices.astype(np.int64) - rows))) if A.nnz else 0
+
+
+def local_matrix(A: SparseMatrix, L: ShardLayout) -> SparseMatrix:
+    """Owned rows in full; ghost rows keep their diagonal and their couplings to owned nodes, which
+    are the coefficients of the owned nodes' outgoing messages (gabp.cpp:120-139)."""
+    ro = A.row_offsets
+    s, e = int(ro[L.glo]), int(ro[L.ghi])
+    rows = np.repeat(np.arange(L.glo, L.ghi), np.diff(ro[L.glo:L.ghi + 1]))
+    cols = A.col_indices[s:e]
+    vals = A.values[s:e]
+    keep = ((rows >= L.lo) & (rows < L.hi)) | ((cols >= L.lo) & (cols < L.hi)) | (rows == cols)
+    rows, cols, vals = rows[keep], cols[keep], vals[keep]
+    counts = np.bincount(rows - L.glo, minlength=L.n_local)
+    lro = np.zeros(L.n_local + 1, np.int32)
+    np.cumsum(counts, out=lro[1:])
+    return SparseMatrix(L.n_local, lro, (cols - L.glo).astype(np.int32), np.ascontiguousarray(vals, np.float64))
+
+
+def _device_view(ptr, count, dtype, device):
+    """A torch tensor over `count` elements of engine-owned device memory (no copy)."""
+    import torch
+    typestr = {torch.int64: "<i8", torch.float64: "<f8"}[dtype]
+
+    class _Cai:
+        __cuda_array_interface__ = {"shape": (count,), "typestr": typestr, "data": (int(ptr), False),
+                                    "version": 3, "strides": None}
+    return torch.as_tensor(_Cai(), device=device)
+
+
+class GpuShard:
+    """One row block on the GPU: the engine's fused step restricted to the owned nodes."""
+
+    def __init__(self, A_local: SparseMatrix, L: ShardLayout, b_local, device="cuda"):
+        import torch
+        self.torch, self.L = torch, L
+        self.eng = GabpEngine(A_local, Layout.Dia)
+        _raise(lib().bgabp_shard_set_range(self.eng.handle, L.own_lo, L.own_hi, L.glo), "shard_set_range")
+        self.S = int(self.eng.info["num_slots"])
+        self.device = torch.device(device)
+        self.stream = torch.cuda.ExternalStream(self.eng.stream(), device=self.device)
+        self.b = torch.as_tensor(np.ascontiguousarray(b_local, np.float64), device=self.device)
+        self.red4 = _device_view(lib().bgabp_shard_reduce_buffer(self.eng.handle), 4, torch.int64, self.device)
+        self.x = [_device_view(lib().bgabp_shard_x(self.eng.handle, k), L.n_local, torch.float64, self.device)
+                  for k in (0, 1)]
+
+    def begin(self, opt: GabpOptions, r0: float):
+        o = opt._c()
+        _raise(lib().bgabp_shard_solve_begin(self.eng.handle, C.c_void_p(self.b.data_ptr()), C.byref(o),
+                                             C.c_double(r0)), "shard_solve_begin")
+
+    def compute(self):
+        _raise(lib().bgabp_shard_step_compute(self.eng.handle), "shard_step_compute")
+
+    def decide(self):
+        _raise(lib().bgabp_shard_step_decide(self.eng.handle), "shard_step_decide")
+
+    def pack(self, which, lo, length):
+        out = self.torch.empty(self.S * length * 2, dtype=self.torch.float64, device=self.device)
+        _raise(lib().bgabp_shard_pack(self.eng.handle, which, lo, length, C.c_void_p(out.data_ptr())), "pack")
+        return out
+
+    def unpack(self, which, buf, lo, length, sender_lo, sender_hi):
+        _raise(lib().bgabp_shard_unpack(self.eng.handle, which, C.c_void_p(buf.data_ptr()), lo, length,
+                                        sender_lo, sender_hi), "unpack")
+
+    def new_buffer(self, count):
+        return self.torch.empty(count, dtype=self.torch.float64, device=self.device)
+
+    def done(self):
+        d, _ = C.c_int(0), C.c_int(0)
+        _raise(lib().bgabp_shard_state(self.eng.handle, C.byref(d), C.byref(_)), "shard_state")
+        return bool(d.value)
+
+    def end(self, max_iter):
+        n = self.L.n_local
+        x = self.torch.empty(n, dtype=self.torch.float64, device=self.device)
+        hist = self.torch.empty(max_iter + 2, dtype=self.torch.float64, device=self.device)
+        status, its, flops, detail = self.eng.solve_device_end(x.data_ptr(), hist.data_ptr())
+        return (int(status), its, detail, x[self.L.own_lo:self.L.own_hi].cpu().numpy(),
+                hist[:its + 1].cpu().numpy())
+
+
+class Exchange:
+    """MAX all-reduce and neighbour halo exchange between shards: copies within a process,
+    torch.distributed point-to-point between processes."""
+
+    def __init__(self, shards: dict, layouts, owner, world):
+        self.shards, self.layouts, self.owner, self.world = shards, layouts, owner, world
+
+    def allreduce_max(self):
+        import torch
+        mine = list(self.shards.values())
+        acc = mine[0].red4.clone()
+        for s in mine[1:]:
+            acc = torch.maximum(acc, s.red4)
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(acc, op=dist.ReduceOp.MAX)
+        for s in mine:
+            s.red4.copy_(acc)
+
+    def halo(self, which_msg, which_x):
+        """Messages of sweep t (buffer which_msg) and x(t-1) (x buffer which_x)."""
+        ops, pending = [], []
+        P = len(self.layouts)
+        for p in range(P):
+            for q in (p - 1, p + 1):
+                if q < 0 or q >= P:
+                    continue
+                sp, sq = self.shards.get(p), self.shards.get(q)
+                if sp is None and sq is None:
+                    continue
+                Lp, Lq = self.layouts[p], self.layouts[q]
+                items = []
+                a, b = max(Lp.glo, Lq.lo), min(Lp.ghi, Lq.hi)  # q's nodes in p's halo: p computed their messages
+                if b > a:
+                    items.append(("msg", a, b))
+                a, b = max(Lq.glo, Lp.lo), min(Lq.ghi, Lp.hi)  # p's nodes in q's halo: q needs their x
+                if b > a:
+                    items.append(("x", a, b))
+                for kind, a, b in items:
+                    tag = 4 * p + 2 * (q > p) + (kind == "x")
+                    data = None
+                    if sp is not None:
+                        data = (sp.pack(which_msg, a - Lp.glo, b - a) if kind == "msg"
+                                else sp.x[which_x][a - Lp.glo:b - Lp.glo].clone())
+                    if sp is not None and sq is not None:
+                        self._deliver(sq, kind, data, a, b, Lp, Lq, which_msg, which_x)
+                    elif sp is not None:
+                        import torch.distributed as dist
+                        ops.append(dist.P2POp(dist.isend, data, self.owner[q], tag=tag))
+                    else:
+                        import torch.distributed as dist
+                        buf = sq.new_buffer(sq.S * (b - a) * 2 if kind == "msg" else b - a)
+                        ops.append(dist.P2POp(dist.irecv, buf, self.owner[p], tag=tag))
+                        pending.append((sq, kind, buf, a, b, Lp, Lq))
+        if ops:
+            import torch.distributed as dist
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        for sq, kind, buf, a, b, Lp, Lq in pending:
+            self._deliver(sq, kind, buf, a, b, Lp, Lq, which_msg, which_x)
+
+    @staticmethod
+    def _deliver(sq, kind, data, a, b, Lp, Lq, which_msg, which_x):
+        if kind == "msg":  # only the in-slots whose sender p owns
+            sq.unpack(which_msg, data, a - Lq.glo, b - a, Lp.lo - Lq.glo, Lp.hi - Lq.glo)
+        else:
+            sq.x[which_x][a - Lq.glo:b - Lq.glo].copy_(data)
+
+
+def sharded_solve(shards: dict, layouts, owner, world, b_inf, opt: GabpOptions, poll_every=16):
+    """Flood solve over all shards to the reference's stop rule.  `shards` maps global shard
+    index -> shard object for this process; `owner` maps every shard index to its rank.
+    Returns (status, iterations, detail, {shard: owned x}, residual history)."""
+    import torch
+    ex = Exchange(shards, layouts, owner, world)
+    first = next(iter(shards.values()))
+    gpu = isinstance(first, GpuShard)
+    single = len(shards) == 1
+    ctx = torch.cuda.stream(first.stream) if (gpu and single) else contextlib.nullcontext()
+    sync = torch.cuda.synchronize if (gpu and not single) else (lambda: None)
+    with ctx:
+        for s in shards.values():
+            s.begin(opt, b_inf)
+        sync()
+        t, cap = 1, opt.max_iter + 2
+        done = first.done()
+        while not done and t <= cap:
+            for s in shards.values():
+                s.compute()
+            sync()
+            ex.allreduce_max()
+            sync()
+            for s in shards.values():
+                s.decide()
+            sync()
+            ex.halo(t & 1, (t - 1) & 1)
+            sync()
+            t += 1
+            if t % poll_every == 0 or t > cap:
+                done = first.done()
+        out, res = {}, None
+        for k, s in shards.items():
+            status, its, detail, x, hist = s.end(opt.max_iter)
+            out[k] = x
+            res = (status, its, detail, hist)
+    return res[0], res[1], res[2], out, res[3]

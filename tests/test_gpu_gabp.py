@@ -110,7 +110,10 @@ def test_solve_report_matches_golden(orc, golden, name, layout):
     assert (int(rep.status), rep.iterations, rep.detail) == (rec["status"], rec["iterations"], rec["detail"])
     assert [float(v).hex() for v in rep.residual_history] == rec["history"]
     assert rep.flop_estimate == rec["flops"]
-    if rec["status"] != 1 or rec["detail"] == "residual blowup":
+    # on a pivot stop the reference returns a partly updated x; the fused DIA flood solve
+    # reproduces it exactly (x(k) below the pivot node, x(k-1) from it on)
+    fused = sched.kind == OSched.parallel_flood().kind and eng.info["layout"] == int(g.Layout.Dia)
+    if rec["status"] != 1 or rec["detail"] == "residual blowup" or fused:
         assert digest(rep.solution) == rec["x"]
 
 
