@@ -179,11 +179,41 @@ int bgabp_solve_error_correction(bgabp_engine* e, const double* b, const bgabp_s
                                  int sweeps, const bgabp_options* opt, bgabp_report* rep,
                                  double* x_out, double* history, char* detail, size_t detaillen);
 
+/* ---- line GaBP: region GaBP over grid lines (region_gabp.hpp:41-94, region_gabp.cpp:30-198 with
+ * grid_line_regions, region.cpp:208-221) ---------------------------------------------------------
+ * RegionGabpEngine(A, build_two_layer_region_graph(A, grid_line_regions(nx, ny))) for a 5-point
+ * operator on an nx x ny grid (x fastest): large regions are the rows then the columns, children
+ * the single nodes; bglin_create rejects the inputs build_two_layer_region_graph rejects, with its
+ * messages.  Block messages are scalars, 2n edges in the reference's edge order (row edges by node,
+ * then column edges column by column).  mode: 0 RegionSweepMode::Sequential, 1 Flood.  Local
+ * systems are solved in O(N) per line (tridiagonal) instead of the reference's dense FullPivLU,
+ * so results agree to rounding, not bitwise. */
+typedef struct bglin_engine bglin_engine;
+typedef struct {
+    double tol;               /* RegionSolveOptions (region_gabp.hpp:25-30): default 2e-4 */
+    int max_iter;             /* default 10000 */
+    int mode;                 /* default 0 (Sequential) */
+    double divergence_factor; /* default 1e12 */
+} bglin_options;
+int bglin_create(int n, const int* row_offsets, const int* col_indices, const double* values, int nx, int ny,
+                 bglin_engine** out, char* err, size_t errlen);
+void bglin_destroy(bglin_engine* e);
+int bglin_num_edges(const bglin_engine* e);
+double bglin_sweep_flops(const bglin_engine* e); /* flop_count_region(SharedInverse) */
+void* bglin_stream(bglin_engine* e);
+int bglin_reset_state(bglin_engine* e);
+int bglin_set_state(bglin_engine* e, const double* lambda, const double* m);
+int bglin_get_state(bglin_engine* e, double* lambda, double* m);
+/* RegionGabpEngine::sweep: BGABP_EPIVOT with the reference's message on a singular local system */
+int bglin_sweep(bglin_engine* e, const double* b, int mode, double* x, char* err, size_t errlen);
+int bglin_solve(bglin_engine* e, const double* b, const bglin_options* opt, bgabp_report* rep, double* x_out,
+                double* history, char* detail, size_t detaillen);
+
 /* ---- multigrid with the GaBP smoother (multigrid.hpp:17-103, multigrid.cpp:54-318) ----------------
  * Levels are supplied by the caller finest first (the reference rediscretises a named problem per
  * level, multigrid.cpp:79-83; bgmg_create_named does that with the built-in assembly).  Smoother
  * numbering = MgSmoother (multigrid.hpp:17-31): 0 GabpSequential 1 GabpRedBlack 2 GabpFourColor
- * 3 GabpFlood 5 Jacobi 6 GsLex 7 GsRedBlack 8 GsFourColor.  Coarsening stops where the
+ * 3 GabpFlood 4 GabpLine 5 Jacobi 6 GsLex 7 GsRedBlack 8 GsFourColor.  Coarsening stops where the
  * sweeps_expand probe fires (multigrid.cpp:54-70, 89-93); the coarsest level is solved directly. */
 typedef struct bgmg bgmg;
 typedef struct {

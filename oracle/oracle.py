@@ -169,6 +169,18 @@ class Oracle:
             "orc_mg_prolong": (None, [_dp, C.c_int, _dp]),
             "orc_gs_sweeps": (C.c_int, [vp, _dp, _dp, _Sched, C.c_int, C.c_char_p, C.c_size_t]),
             "orc_dense_solve": (C.c_int, [vp, _dp, _dp]),
+            "orc_region_create": (vp, [vp, C.c_int, _ip, _ip, C.c_char_p, C.c_size_t]),
+            "orc_region_free": (None, [vp]),
+            "orc_region_num_edges": (C.c_int, [vp]),
+            "orc_region_num_small": (C.c_int, [vp]),
+            "orc_region_state_size": (C.c_long, [vp, C.POINTER(C.c_long)]),
+            "orc_region_edges": (None, [vp, _ip, _ip]),
+            "orc_region_small": (C.c_long, [vp, _ip, _ip, _ip, _ip, _ip]),
+            "orc_region_sweep": (C.c_int, [vp, _dp, C.c_int, _dp, _dp, _dp, C.c_char_p, C.c_size_t]),
+            "orc_region_solve": (C.c_int, [vp, _dp, C.c_double, C.c_int, C.c_int, C.c_double, _dp, _dp, _ip, _ip,
+                                           _dp, C.c_char_p, C.c_size_t]),
+            "orc_region_direct_message": (C.c_int, [vp, _dp, _dp, _dp, C.c_int, _dp, _dp, C.c_char_p, C.c_size_t]),
+            "orc_region_flops": (C.c_double, [vp, C.c_int]),
         }
         gens = {
             "orc_rng_new": (vp, [C.c_uint]),
@@ -185,6 +197,10 @@ class Oracle:
         self.has_generators = hasattr(L, "orc_rng_new")
         if self.has_generators:
             sig.update(gens)
+        self.has_region_graph = hasattr(L, "ref_region_graph")
+        if self.has_region_graph:  # the reference's own region.cpp builder (reference build only)
+            sig["ref_region_graph"] = (C.c_long, [vp, C.c_int, _ip, _ip, _ip, _ip, _ip, _ip, _ip, C.c_char_p,
+                                                  C.c_size_t])
         self.has_assemble = hasattr(L, "ref_assemble")
         if self.has_assemble:
             sig["ref_assemble"] = (vp, [C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_char_p), _dp,
@@ -344,6 +360,35 @@ class Oracle:
     # ---- engine ---------------------------------------------------------------------------
     def engine(self, A: Csr):
         return _Engine(self, A)
+
+    def region(self, A: Csr, large):
+        """RegionGabpEngine(A, build_two_layer_region_graph(A, large)) (region_gabp.cpp:30-198)."""
+        return _Region(self, A, large)
+
+    def grid_lines(self, nx, ny):
+        """grid_line_regions(nx, ny) (region.cpp:208-221)."""
+        rows = [[iy * nx + ix for ix in range(nx)] for iy in range(ny)]
+        cols = [[iy * nx + ix for iy in range(ny)] for ix in range(nx)]
+        return rows + cols
+
+    def region_graph_ref(self, A: Csr, large):
+        """The reference's own build_two_layer_region_graph (ref build): (small, parents, counting)."""
+        offs, idx = _flatten_lists(large)
+        h = self._handle(A)
+        err = C.create_string_buffer(512)
+        try:
+            ns = self.lib.ref_region_graph(h, len(large), _i(offs), _i(idx), None, None, None, None, None, err, 512)
+            if ns < 0:
+                raise ValueError(err.value.decode())
+            cap = sum(len(r) for r in large) * 2 + 1
+            so, sv, po, pv, cnt = (np.zeros(ns + 1, np.int32), np.zeros(cap, np.int32), np.zeros(ns + 1, np.int32),
+                                   np.zeros(cap, np.int32), np.zeros(max(ns, 1), np.int32))
+            self.lib.ref_region_graph(h, len(large), _i(offs), _i(idx), _i(so), _i(sv), _i(po), _i(pv), _i(cnt),
+                                      err, 512)
+        finally:
+            self.lib.orc_matrix_free(h)
+        return ([list(sv[so[k]:so[k + 1]]) for k in range(ns)], [list(pv[po[k]:po[k + 1]]) for k in range(ns)],
+                list(cnt[:ns]))
 
     def hierarchy(self, levels, nx, smoother):
         return _Hierarchy(self, levels, nx, smoother)
@@ -526,3 +571,83 @@ class _Hierarchy:
         self.o.lib.orc_mg_solve(self.h, pre, post, int(frozen), _d(f64(b)), tol, max_cycles,
                                 divergence_factor, _d(x), _d(hist), C.byref(it), C.byref(st), det, 512)
         return Report(st.value, it.value, hist[: it.value + 1].copy(), 0.0, x, det.value.decode())
+
+
+def _flatten_lists(lists):
+    offs = np.zeros(len(lists) + 1, np.int32)
+    offs[1:] = np.cumsum([len(r) for r in lists])
+    idx = np.array([v for r in lists for v in r] or [0], np.int32)
+    return offs, idx
+
+
+class _Region:
+    """Region GaBP restatement (region_gabp.cpp:30-198, region_restate.inc).  State is flat:
+    Lambda blocks (row-major |l| x |l|) and m blocks per edge, in the engine's edge order."""
+
+    def __init__(self, orc: Oracle, A: Csr, large):
+        self.o = orc
+        offs, idx = _flatten_lists(large)
+        h = orc._handle(A)
+        err = C.create_string_buffer(512)
+        self.h = orc.lib.orc_region_create(h, len(large), _i(offs), _i(idx), err, 512)
+        orc.lib.orc_matrix_free(h)
+        if not self.h:
+            raise ValueError(err.value.decode())
+        self.n = A.n
+        ms = C.c_long(0)
+        self.lam_size = orc.lib.orc_region_state_size(self.h, C.byref(ms))
+        self.m_size = ms.value
+
+    def __del__(self):
+        try:
+            self.o.lib.orc_region_free(self.h)
+        except Exception:
+            pass
+
+    @property
+    def num_edges(self):
+        return self.o.lib.orc_region_num_edges(self.h)
+
+    def edges(self):
+        E = self.num_edges
+        el, es = np.zeros(max(E, 1), np.int32), np.zeros(max(E, 1), np.int32)
+        self.o.lib.orc_region_edges(self.h, _i(el), _i(es))
+        return el[:E], es[:E]
+
+    def small(self):
+        ns = self.o.lib.orc_region_num_small(self.h)
+        nv = self.o.lib.orc_region_small(self.h, None, None, None, None, None)
+        so, sv, po, pv, cnt = (np.zeros(ns + 1, np.int32), np.zeros(max(nv, 1), np.int32), np.zeros(ns + 1, np.int32),
+                               np.zeros(max(nv * 8, 1), np.int32), np.zeros(max(ns, 1), np.int32))
+        self.o.lib.orc_region_small(self.h, _i(so), _i(sv), _i(po), _i(pv), _i(cnt))
+        return ([list(sv[so[k]:so[k + 1]]) for k in range(ns)], [list(pv[po[k]:po[k + 1]]) for k in range(ns)],
+                list(cnt[:ns]))
+
+    def make_state(self):
+        return np.zeros(self.lam_size), np.zeros(self.m_size)
+
+    def sweep(self, b, lam, m, x, mode=0):
+        """One sweep (mode 0 Sequential, 1 Flood), in place; returns (ok, err)."""
+        err = C.create_string_buffer(512)
+        rc = self.o.lib.orc_region_sweep(self.h, _d(f64(b)), mode, _d(lam), _d(m), _d(x), err, 512)
+        return rc == 1, err.value.decode()
+
+    def solve(self, b, tol=2e-4, max_iter=10000, mode=0, divergence_factor=1e12):
+        x = np.zeros(self.n)
+        hist = np.zeros(max_iter + 1)
+        it, st, fl = C.c_int(0), C.c_int(0), C.c_double(0)
+        det = C.create_string_buffer(512)
+        self.o.lib.orc_region_solve(self.h, _d(f64(b)), tol, max_iter, mode, divergence_factor, _d(x), _d(hist),
+                                    C.byref(it), C.byref(st), C.byref(fl), det, 512)
+        return Report(st.value, it.value, hist[: it.value + 1].copy(), fl.value, x, det.value.decode())
+
+    def direct_message(self, b, lam, m, edge, nl=1):
+        lo, mo = np.zeros(nl * nl), np.zeros(nl)
+        err = C.create_string_buffer(512)
+        if self.o.lib.orc_region_direct_message(self.h, _d(f64(b)), _d(f64(lam)), _d(f64(m)), edge, _d(lo), _d(mo),
+                                                err, 512) != 1:
+            raise RuntimeError(err.value.decode())
+        return lo, mo
+
+    def flops(self, per_child=False):
+        return self.o.lib.orc_region_flops(self.h, int(per_child))

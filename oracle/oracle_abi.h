@@ -125,6 +125,25 @@ orc_matrix* orc_poisson5(int nx, int ny);
 orc_matrix* orc_example7x7(void);
 int orc_tree_diameter(int n, const int* edges);
 
+/* ---- region (line) GaBP restatement (region.cpp, region_gabp.cpp; see region_restate.inc) ---- */
+typedef struct orc_region orc_region;
+orc_region* orc_region_create(const orc_matrix* A, int nlarge, const int* offs, const int* idx, char* err,
+                              size_t errlen);
+void orc_region_free(orc_region* h);
+int orc_region_num_edges(const orc_region* h);
+int orc_region_num_small(const orc_region* h);
+long orc_region_state_size(const orc_region* h, long* m_size);
+void orc_region_edges(const orc_region* h, int* edge_large, int* edge_small);
+long orc_region_small(const orc_region* h, int* offs, int* vars, int* poffs, int* parents, int* counting);
+int orc_region_sweep(const orc_region* h, const double* b, int mode, double* lam, double* m, double* x, char* err,
+                     size_t errlen);
+int orc_region_solve(const orc_region* h, const double* b, double tol, int max_iter, int mode,
+                     double divergence_factor, double* x_out, double* history, int* iterations, int* status,
+                     double* flops, char* detail, size_t detaillen);
+int orc_region_direct_message(const orc_region* h, const double* b, const double* lam, const double* m, int edge,
+                              double* lam_out, double* m_out, char* err, size_t errlen);
+double orc_region_flops(const orc_region* h, int per_child);
+
 #ifdef __cplusplus
 }
 #endif

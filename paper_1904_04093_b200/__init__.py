@@ -5,7 +5,7 @@ The product is the C-ABI library `libgabp_b200.so` (include/gabp_b200.h) built f
 package is its Python host mirror of the reference's proj/core API (see gabp.py).
 """
 from .gabp import (AssembledProblem, CycleSpec, FrozenLambda, GabpEngine, GabpOptions, Hierarchy, Layout,  # noqa: F401
-                   MessageState, MgSmoother, MgSolveOptions, Schedule, ScheduleKind, SolveReport, SolveStatus,
+                   LineGabpEngine, MessageState, RegionSolveOptions, RegionSweepMode, MgSmoother, MgSolveOptions, Schedule, ScheduleKind, SolveReport, SolveStatus,
                    SparseMatrix, StopCriterion, assemble, config5_level, config_problem, lib, load_matrix_market, mg_prolong,
                    mg_restrict, mg_solve, mg_solve_device, poisson5)
 

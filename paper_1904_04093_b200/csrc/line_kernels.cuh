@@ -1,0 +1,215 @@
+// Line GaBP on a 5-point grid: the two-layer region GaBP of region_gabp.cpp:64-157 with the grid
+// lines of region.cpp:208-221 as large regions (rows first, then columns) and the single grid
+// nodes as children (parent sets {row, column}, counting number -1).
+//
+// A line is a tridiagonal local system T (diagonal A_vv + Lambda_other, right-hand side
+// b_v + m_other, where "other" is the node's message from its crossing line).  The reference
+// factors T densely (Eigen FullPivLU), solves it, inverts it and inverts each 1x1 child block of
+// the inverse.  Here each thread owns one line and runs the O(N) equivalent:
+//   forward   d_k = a_k - (l_k / d_{k-1}) u_{k-1},  y_k = b0_k - (l_k / d_{k-1}) y_{k-1}
+//   backward  x_k = (y_k - u_k x_{k+1}) / d_k,      g_k = a_k - u_k (l_{k+1} / g_{k+1})
+//   child precision  W_k = 1 / (T^-1)_kk = d_k + g_k - a_k
+//   outgoing message Lambda_k = W_k - A_vv - Lambda_other,  m_k = W_k x_k - b_v - m_other
+// (l_k = T(k,k-1), u_k = T(k,k+1)).  The result equals the reference's to rounding (it is not
+// the same sequence of operations), so parity is a tolerance, not bits.
+//
+// Rows phase: thread per row, columns phase: thread per column (coalesced across the warp).
+// Sequential mode runs rows then columns on the freshest messages (rows read column messages and
+// write row messages, so all rows are independent, and likewise the columns); flood mode reads
+// both from the previous sweep.  x is the column phase's solution (the reference's later regions
+// overwrite earlier ones).
+#pragma once
+
+#include "kernels.cuh"
+
+namespace bgabp {
+
+struct LineP {
+    int nx, ny, n;
+    const double* diag;  // A_vv
+    const double* w;     // A_{v,v-1} (same row), 0 when absent
+    const double* e;     // A_{v,v+1}
+    const double* s;     // A_{v,v-nx}
+    const double* nn;    // A_{v,v+nx}
+    const uint32_t* mask;  // bits 0..3: A_{v,v-nx}, A_{v,v-1}, A_{v,v+1}, A_{v,v+nx} stored
+};
+
+// failure key: (region << 32) | 0 for a singular local system, | (1 + child position) for a
+// singular child block; atomicMin gives the reference's first failure in region order
+template <bool ROW>
+static __global__ void __launch_bounds__(64) k_line_phase(LineP P, const double* __restrict__ b,
+                                                         const double* __restrict__ lam_o,
+                                                         const double* __restrict__ m_o, double* __restrict__ lam_n,
+                                                         double* __restrict__ m_n, double* __restrict__ x,
+                                                         double* __restrict__ fd, double* __restrict__ fy,
+                                                         unsigned long long* fail, const int* done) {
+    if (done && *(volatile const int*)done) return;
+    // a region already failed (rows of this sweep, or an earlier sweep of a smoothing call): the
+    // reference stopped there
+    if (*(volatile unsigned long long*)fail != kNone) return;
+    const int line = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nlines = ROW ? P.ny : P.nx, N = ROW ? P.nx : P.ny;
+    if (line >= nlines) return;
+    const int stride = ROW ? 1 : P.nx;
+    const int base = ROW ? line * P.nx : line;
+    const double* lo = ROW ? P.w : P.s;   // T(k, k-1)
+    const double* up = ROW ? P.e : P.nn;  // T(k, k+1)
+    const unsigned long long region = (unsigned long long)(ROW ? line : P.ny + line);
+    // Loads do not depend on the recurrences: each chunk of kLC steps issues all of its loads
+    // first, so one memory latency is paid per chunk instead of per step (one warp holds 32
+    // lines and there are only nx + ny lines, so other warps cannot hide it).
+    constexpr int kLC = 8;
+    bool singular = false;
+    double dprev = 0.0, yprev = 0.0, uprev = 0.0;
+    for (int k0 = 0; k0 < N; k0 += kLC) {
+        double av[kLC], bv[kLC], lv[kLC], uv[kLC];
+#pragma unroll
+        for (int q = 0; q < kLC; ++q) {
+            const int k = k0 + q;
+            const int v = base + (k < N ? k : N - 1) * stride;
+            av[q] = dadd(__ldg(P.diag + v), lam_o[v]);
+            bv[q] = dadd(__ldg(b + v), m_o[v]);
+            lv[q] = __ldg(lo + v);
+            uv[q] = __ldg(up + v);
+        }
+#pragma unroll
+        for (int q = 0; q < kLC; ++q) {
+            const int k = k0 + q;
+            if (k >= N) break;
+            const int v = base + k * stride;
+            double d, y;
+            if (k == 0) {
+                d = av[q];
+                y = bv[q];
+            } else {
+                const double f = ddiv(lv[q], dprev);
+                d = dsub(av[q], dmul(f, uprev));
+                y = dsub(bv[q], dmul(f, yprev));
+            }
+            if (d == 0.0 || !isfinite(d)) singular = true;
+            fd[v] = d;
+            fy[v] = y;
+            dprev = d;
+            yprev = y;
+            uprev = uv[q];
+        }
+    }
+    if (singular) {
+        atomicMin(fail, region << 32);
+        return;
+    }
+    double xnext = 0.0, gnext = 0.0, lnext = 0.0;
+    unsigned long long bad = kNone;
+    for (int k1 = N - 1; k1 >= 0; k1 -= kLC) {
+        double lo_v[kLC], mo_v[kLC], dv[kLC], bb[kLC], dd[kLC], yy[kLC], uu[kLC], ll[kLC];
+#pragma unroll
+        for (int q = 0; q < kLC; ++q) {
+            const int k = k1 - q;
+            const int v = base + (k >= 0 ? k : 0) * stride;
+            lo_v[q] = lam_o[v];
+            mo_v[q] = m_o[v];
+            dv[q] = __ldg(P.diag + v);
+            bb[q] = __ldg(b + v);
+            dd[q] = fd[v];
+            yy[q] = fy[v];
+            uu[q] = __ldg(up + v);
+            ll[q] = __ldg(lo + v);
+        }
+#pragma unroll
+        for (int q = 0; q < kLC; ++q) {
+            const int k = k1 - q;
+            if (k < 0) break;
+            const int v = base + k * stride;
+            const double a = dadd(dv[q], lo_v[q]);
+            double xk, g;
+            if (k == N - 1) {
+                xk = ddiv(yy[q], dd[q]);
+                g = a;
+            } else {
+                xk = ddiv(dsub(yy[q], dmul(uu[q], xnext)), dd[q]);
+                g = dsub(a, dmul(uu[q], ddiv(lnext, gnext)));
+            }
+            const double W = dsub(dadd(dd[q], g), a);
+            if (W == 0.0 || !isfinite(W)) bad = (region << 32) | (unsigned long long)(1 + k);
+            lam_n[v] = dsub(dsub(W, dv[q]), lo_v[q]);
+            m_n[v] = dsub(dsub(dmul(W, xk), bb[q]), mo_v[q]);
+            if (x) x[v] = xk;
+            xnext = xk;
+            gnext = g;
+            lnext = ll[q];
+        }
+    }
+    if (bad != kNone) atomicMin(fail, bad);
+}
+
+// r = b - A x in CSR column order (sparse.cpp:104-115) and its NaN-skipping inf-norm
+static __global__ void k_line_residual(LineP P, const double* __restrict__ b, const double* __restrict__ x,
+                                       double* __restrict__ r, unsigned long long* rmax, const int* done) {
+    if (done && *(volatile const int*)done) return;
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    double ra = 0.0;
+    if (v < P.n) {
+        const uint32_t mk = P.mask[v];
+        double acc = b[v];
+        if (mk & 1u) acc = dsub(acc, dmul(P.s[v], x[v - P.nx]));
+        if (mk & 2u) acc = dsub(acc, dmul(P.w[v], x[v - 1]));
+        acc = dsub(acc, dmul(P.diag[v], x[v]));
+        if (mk & 4u) acc = dsub(acc, dmul(P.e[v], x[v + 1]));
+        if (mk & 8u) acc = dsub(acc, dmul(P.nn[v], x[v + P.nx]));
+        if (r) r[v] = acc;
+        ra = nan_skip_abs(acc);
+    }
+    if (rmax) warp_max_commit(rmax, ra);
+}
+
+struct LineCtrl {
+    int done, status, iterations, step;
+    unsigned long long rmax, fail, detail_key;
+    double r0, tol, divergence;
+    int max_iter, mode;
+};
+
+// RegionGabpEngine::solve's per-iteration test (region_gabp.cpp:172-197)
+static __global__ void k_line_decide(LineCtrl* c, double* history, int kind_stop_on_fail) {
+    if (c->done) return;
+    const int it = c->step;
+    c->iterations = it;
+    if (c->fail != kNone) {
+        c->status = 1;
+        c->detail_key = c->fail;
+        c->done = 1;
+        return;
+    }
+    const double r = __longlong_as_double((long long)c->rmax);
+    history[it] = r;
+    c->rmax = 0ull;
+    if (!isfinite(r) || r > c->divergence * c->r0) {
+        c->status = 1;
+        c->detail_key = kNone - 1;  // residual blowup
+        c->done = 1;
+        return;
+    }
+    if (r <= c->tol) {
+        c->status = 0;
+        c->done = 1;
+        return;
+    }
+    if (it >= c->max_iter) {
+        c->status = 2;
+        c->done = 1;
+        return;
+    }
+    c->step = it + 1;
+    (void)kind_stop_on_fail;
+}
+
+// x += e, and the multigrid failure record for the level (see Engine::decode_failure kinds 6, 7)
+static __global__ void k_line_check(Ctrl* c, const unsigned long long* fail, int seq) {
+    if (c->halt || *fail == kNone) return;
+    c->halt = 1;
+    c->fail_seq = seq;
+    c->detail_kind = (*fail & 0xffffffffull) ? 7 : 6;
+    c->detail_key = *fail;
+}
+
+}  // namespace bgabp

@@ -13,15 +13,16 @@
 #include <vector>
 
 #include "engine.h"
+#include "line.h"
 #include "problems.h"
 
 using namespace bgabp;
 
 namespace {
 
-enum { GabpSeq = 0, GabpRB = 1, GabpFC = 2, GabpFlood = 3, Jacobi = 5, GsLex = 6, GsRB = 7, GsFC = 8 };
+enum { GabpSeq = 0, GabpRB = 1, GabpFC = 2, GabpFlood = 3, GabpLine = 4, Jacobi = 5, GsLex = 6, GsRB = 7, GsFC = 8 };
 bool is_gabp(int s) { return s >= 0 && s <= 3; }
-bool supported(int s) { return is_gabp(s) || (s >= 5 && s <= 8); }
+bool supported(int s) { return s >= 0 && s <= 8; }
 
 struct MgLevel {
     std::unique_ptr<Engine> E;
@@ -30,6 +31,7 @@ struct MgLevel {
     bool frozen_ok = false;
     bool frozen_pending = false;  // precompute_lambda deferred to first use
     double *d_b = nullptr, *d_x = nullptr;  // this level's right-hand side and iterate (coarse levels)
+    std::unique_ptr<LineEngine> line;        // GabpLine: grid-line region GaBP (multigrid.cpp:96-100)
 };
 
 // dense partial-pivot LU + explicit inverse of the coarsest operator (host, setup only)
@@ -121,6 +123,16 @@ struct bgmg {
             k_axpy1<<<g, 256, 0, st>>>(x, L.d_e, L.n);
             return;
         }
+        if (smoother == GabpLine) {  // multigrid.cpp:189-204: fresh block messages, sequential sweeps
+            LineEngine& G = *levels[k].line;
+            L.launch_residual(b, x, L.d_r, nullptr, MODE_PLAIN);
+            G.reset_state();
+            ck(cudaMemsetAsync(G.d_fail, 0xff, sizeof(unsigned long long), st), "memset");
+            for (int s = 0; s < sweeps; ++s) G.sweep(L.d_r, 0, L.d_e);
+            k_line_check<<<1, 1, 0, st>>>(L.d_ctrl, G.d_fail, seq);
+            k_axpy1<<<g, 256, 0, st>>>(x, L.d_e, L.n);
+            return;
+        }
         // point relaxations in place (classic.cpp:99-146)
         k_plain_reset<<<1, 1, 0, st>>>(L.d_ctrl);
         if (smoother == Jacobi) {
@@ -173,12 +185,18 @@ struct bgmg {
             if (h_ctrl->halt && h_ctrl->fail_seq < best_seq) {
                 best_seq = h_ctrl->fail_seq;
                 best = k;
-                const Levels* lv = levels[k].sched.kind == BGABP_SCHED_FLOOD ? nullptr : &E(k).levels_for(levels[k].sched);
-                msg = E(k).decode_failure(*h_ctrl, lv ? &lv->order : nullptr);
+                if (smoother == GabpLine) {
+                    msg = levels[k].line->fail_message(h_ctrl->detail_key);
+                } else {
+                    const Levels* lv =
+                        levels[k].sched.kind == BGABP_SCHED_FLOOD ? nullptr : &E(k).levels_for(levels[k].sched);
+                    msg = E(k).decode_failure(*h_ctrl, lv ? &lv->order : nullptr);
+                }
             }
         }
         if (best < 0) return "";
-        if (is_gabp(smoother)) return "smoother breakdown on level " + std::to_string(best) + ": " + msg;
+        if (is_gabp(smoother) || smoother == GabpLine)
+            return "smoother breakdown on level " + std::to_string(best) + ": " + msg;
         return msg;  // relax() throws its own message (classic.cpp:27,43)
     }
 
@@ -309,6 +327,10 @@ static void build_hierarchy(bgmg* h, int nlevels, const int* n, const int* const
         L.E->build(n[k], ro[k], ci[k], v[k], BGABP_LAYOUT_AUTO, h->st);
         L.nx = nx[k];
         L.sched = schedule_for(smoother, nx[k]);
+        if (smoother == GabpLine) {  // RegionGabpEngine over grid_line_regions(nx, nx) per level
+            L.line = std::make_unique<LineEngine>();
+            L.line->build(n[k], ro[k], ci[k], v[k], nx[k], nx[k], h->st);
+        }
         if (k > 0) {
             L.d_b = static_cast<double*>(L.E->dalloc(sizeof(double) * std::max(n[k], 1)));
             L.d_x = static_cast<double*>(L.E->dalloc(sizeof(double) * std::max(n[k], 1)));

@@ -39,6 +39,10 @@ class _Rep(C.Structure):
     _fields_ = [("status", C.c_int), ("iterations", C.c_int), ("flop_estimate", C.c_double)]
 
 
+class _LinOpts(C.Structure):
+    _fields_ = [("tol", C.c_double), ("max_iter", C.c_int), ("mode", C.c_int), ("divergence_factor", C.c_double)]
+
+
 class _Info(C.Structure):
     _fields_ = [("n", C.c_int), ("nnz", C.c_longlong), ("num_edges", C.c_longlong), ("layout", C.c_int),
                 ("num_slots", C.c_int), ("symmetric_values", C.c_int), ("bytes_per_sweep", C.c_double),
@@ -125,6 +129,18 @@ def lib():
             "bgabp_problem_values": (_dp, [_vp]),
             "bgabp_problem_rhs": (_dp, [_vp]),
             "bgabp_problem_exact": (_dp, [_vp]),
+            "bglin_create": (C.c_int, [C.c_int, _ip, _ip, _dp, C.c_int, C.c_int, C.POINTER(_vp), C.c_char_p,
+                                       C.c_size_t]),
+            "bglin_destroy": (None, [_vp]),
+            "bglin_num_edges": (C.c_int, [_vp]),
+            "bglin_sweep_flops": (C.c_double, [_vp]),
+            "bglin_stream": (_vp, [_vp]),
+            "bglin_reset_state": (C.c_int, [_vp]),
+            "bglin_set_state": (C.c_int, [_vp, _dp, _dp]),
+            "bglin_get_state": (C.c_int, [_vp, _dp, _dp]),
+            "bglin_sweep": (C.c_int, [_vp, _dp, C.c_int, _dp, C.c_char_p, C.c_size_t]),
+            "bglin_solve": (C.c_int, [_vp, _dp, C.POINTER(_LinOpts), C.POINTER(_Rep), _dp, _dp, C.c_char_p,
+                                      C.c_size_t]),
             "bgabp_shard_set_range": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int]),
             "bgabp_shard_solve_begin": (C.c_int, [_vp, _vp, C.POINTER(_Opts), C.c_double]),
             "bgabp_shard_step_compute": (C.c_int, [_vp]),
@@ -476,6 +492,86 @@ class GabpEngine:
 
 
 # ---------------------------------------------------------------------------------------------
+# line GaBP: region GaBP over grid lines (region_gabp.hpp:41-94, region.cpp:208-221)
+# ---------------------------------------------------------------------------------------------
+class RegionSweepMode(enum.IntEnum):  # region_gabp.hpp:20-23
+    Sequential = 0
+    Flood = 1
+
+
+@dataclass
+class RegionSolveOptions:  # region_gabp.hpp:25-30
+    tol: float = 2e-4
+    max_iter: int = 10000
+    mode: int = RegionSweepMode.Sequential
+    divergence_factor: float = 1e12
+
+    def _c(self):
+        return _LinOpts(self.tol, self.max_iter, int(self.mode), self.divergence_factor)
+
+
+class LineGabpEngine:
+    """RegionGabpEngine(A, build_two_layer_region_graph(A, grid_line_regions(nx, ny))) on the device
+    for a 5-point operator (x fastest).  Block messages are scalars: 2n edges in the reference's
+    edge order (row edges by node, then column edges column by column)."""
+
+    def __init__(self, A, nx, ny):
+        L = lib()
+        self.A = SparseMatrix.of(A)
+        self.nx, self.ny = int(nx), int(ny)
+        h = _vp()
+        err = C.create_string_buffer(512)
+        rc = L.bglin_create(self.A.n, _i(self.A.row_offsets), _i(self.A.col_indices), _d(self.A.values), self.nx,
+                            self.ny, C.byref(h), err, 512)
+        _raise(rc, err.value.decode())
+        self._h = h
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                lib().bglin_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    @property
+    def num_edges(self):
+        return lib().bglin_num_edges(self._h)
+
+    def sweep_flops(self):
+        return lib().bglin_sweep_flops(self._h)
+
+    def make_state(self):
+        return np.zeros(self.num_edges), np.zeros(self.num_edges)
+
+    def sweep(self, b, lam, m, x, mode=RegionSweepMode.Sequential):
+        """RegionGabpEngine::sweep (region_gabp.cpp:145-157): state and x in place; (ok, err)."""
+        L = lib()
+        _raise(L.bglin_set_state(self._h, _d(lam), _d(m)), "set_state")
+        err = C.create_string_buffer(512)
+        rc = L.bglin_sweep(self._h, _d(_f64(b)), int(mode), _d(x), err, 512)
+        if rc not in (OK, EPIVOT):
+            _raise(rc, err.value.decode())
+        _raise(L.bglin_get_state(self._h, _d(lam), _d(m)), "get_state")
+        return rc == OK, err.value.decode()
+
+    def solve(self, b, opt: RegionSolveOptions = RegionSolveOptions()) -> SolveReport:
+        """RegionGabpEngine::solve (region_gabp.cpp:159-198)."""
+        n = self.A.n
+        x = np.zeros(n)
+        hist = np.zeros(max(opt.max_iter, 0) + 2)
+        rep = _Rep()
+        det = C.create_string_buffer(512)
+        o = opt._c()
+        rc = lib().bglin_solve(self._h, _d(_f64(b)), C.byref(o), C.byref(rep), _d(x), _d(hist), det, 512)
+        _raise(rc, det.value.decode())
+        good = rep.iterations - (1 if rep.status == SolveStatus.Diverged and det.value
+                                 and det.value != b"residual blowup" else 0)
+        return SolveReport(SolveStatus(rep.status), rep.iterations, hist[:good + 1].copy(), rep.flop_estimate, x,
+                           det.value.decode())
+
+
+# ---------------------------------------------------------------------------------------------
 # multigrid (multigrid.hpp:17-103)
 # ---------------------------------------------------------------------------------------------
 class MgSmoother(enum.IntEnum):
@@ -483,7 +579,7 @@ class MgSmoother(enum.IntEnum):
     GabpRedBlack = 1
     GabpFourColor = 2
     GabpFlood = 3
-    GabpLine = 4  # not on this path (region GaBP, SURVEY.md §2.1 out of scope)
+    GabpLine = 4  # grid-line region GaBP (multigrid.cpp:96-100, 189-204), see LineGabpEngine
     Jacobi = 5
     GsLex = 6
     GsRedBlack = 7

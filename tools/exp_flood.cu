@@ -38,6 +38,9 @@ void run(int N) {
     DiaP P;
     std::memset(&P, 0, sizeof(P));
     P.n = n;
+    P.j0 = 0;
+    P.j1 = n;
+    P.gofs = 0;
     P.S = S;
     P.nneg = S / 2;
     std::vector<int> st;
