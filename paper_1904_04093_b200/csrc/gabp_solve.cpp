@@ -2,8 +2,9 @@
 // following the reference CLI's single-run contract (proj/tools/belief_solve.cpp:79-165,392-462):
 // the same options for a GaBP or multigrid run, the `iteration,residual_inf` CSV with %.17g
 // (belief_solve.cpp:149-156), the stderr summary line and the exit codes 0 converged / 2 diverged
-// / 3 max_iter / 1 error (belief_solve.cpp:158-165).  Suites, the classical solvers and region
-// GaBP are outside this path.  Inputs: a named model problem (--problem/--J/--param), a Matrix
+// / 3 max_iter / 1 error (belief_solve.cpp:158-165).  Solvers: gabp, generalized-gabp (line-region
+// GaBP, belief_solve.cpp:115-124) and mg:<smoother> incl. mg:line-gabp; suites and the classical
+// solvers are outside this path.  Inputs: a named model problem (--problem/--J/--param), a Matrix
 // Market file (--matrix, with --rhs ones|random|<file>), or a BASELINE.json config (--config).
 // Every solve runs on the GPU; there is no CPU fallback.
 #include <cstdio>
@@ -62,8 +63,9 @@ void write_csv(const std::vector<double>& hist, std::ostream& os) {  // belief_s
 
 int smoother_id(const std::string& name) {  // belief_solve.cpp:58-75 (point smoothers)
     static const std::map<std::string, int> t = {
-        {"sequential-gabp", 0}, {"red-black-gabp", 1}, {"4-color-gabp", 2}, {"parallel-gabp", 3},
-        {"jacobi", 5},          {"gs", 6},             {"red-black-gs", 7}, {"4-color-gs", 8}};
+        {"sequential-gabp", 0}, {"red-black-gabp", 1}, {"4-color-gabp", 2}, {"flood-gabp", 3},
+        {"line-gabp", 4},       {"jacobi", 5},         {"gs", 6},           {"red-black-gs", 7},
+        {"4-color-gs", 8}};
     auto it = t.find(name);
     if (it == t.end()) throw std::invalid_argument("unknown multigrid smoother '" + name + "'");
     return it->second;
@@ -134,7 +136,7 @@ int main(int argc, char** argv) {
             bgmg_destroy(h);
             if (rc != BGABP_OK) throw std::runtime_error(det);
             detail = det;
-        } else if (s.solver == "gabp") {  // belief_solve.cpp:101-106
+        } else if (s.solver == "gabp" || s.solver == "generalized-gabp") {  // belief_solve.cpp:101-106, 115-124
             Problem P;
             if (!s.matrix.empty())
                 P.p = bgabp_problem_matrix_market(s.matrix.c_str(), err, sizeof err);
@@ -165,28 +167,45 @@ int main(int argc, char** argv) {
                 for (auto& v : b)
                     if (!(f >> v)) throw std::runtime_error("right-hand side file too short");
             }
-            bgabp_schedule sch{};
             const int nx = bgabp_problem_nx(P.p);
-            if (s.schedule == "sequential") sch.kind = BGABP_SCHED_SEQUENTIAL;
-            else if (s.schedule == "parallel-flood") sch.kind = BGABP_SCHED_FLOOD;
-            else if (s.schedule == "red-black") sch = {BGABP_SCHED_RED_BLACK_GRID, nx, nx, nullptr};
-            else if (s.schedule == "four-color") sch = {BGABP_SCHED_FOUR_COLOR_GRID, nx, nx, nullptr};
-            else throw std::invalid_argument("unknown schedule '" + s.schedule + "'");
-            if ((sch.kind == BGABP_SCHED_RED_BLACK_GRID || sch.kind == BGABP_SCHED_FOUR_COLOR_GRID) && nx == 0)
-                sch.kind = sch.kind == BGABP_SCHED_RED_BLACK_GRID ? BGABP_SCHED_RED_BLACK : BGABP_SCHED_FOUR_COLOR;
-            bgabp_engine* e = nullptr;
-            int rc = bgabp_create(n, bgabp_problem_row_offsets(P.p), bgabp_problem_col_indices(P.p),
-                                  bgabp_problem_values(P.p), BGABP_LAYOUT_AUTO, &e, err, sizeof err);
-            if (rc != BGABP_OK) throw std::invalid_argument(err);
-            hist.assign((size_t)std::max(s.max_iter, 0) + 2, 0.0);
-            bgabp_options o{s.tol, s.max_iter, BGABP_STOP_RESIDUAL, 1e12};
-            char det[512] = {0};
-            rc = bgabp_solve(e, b.data(), &sch, &o, &rep, x.data(), hist.data(), det, sizeof det);
-            bgabp_destroy(e);
-            if (rc != BGABP_OK) throw std::runtime_error(det);
-            detail = det;
+            if (s.solver == "generalized-gabp") {  // RegionGabpEngine over grid_line_regions
+                if (nx <= 0 || (long long)nx * nx != n)
+                    throw std::invalid_argument("generalized-gabp needs a square grid problem");
+                bglin_engine* le = nullptr;
+                int rc = bglin_create(n, bgabp_problem_row_offsets(P.p), bgabp_problem_col_indices(P.p),
+                                      bgabp_problem_values(P.p), nx, nx, &le, err, sizeof err);
+                if (rc != BGABP_OK) throw std::invalid_argument(err);
+                hist.assign((size_t)std::max(s.max_iter, 0) + 2, 0.0);
+                bglin_options o{s.tol, s.max_iter, s.schedule == "parallel-flood" ? 1 : 0, 1e12};
+                char det[512] = {0};
+                rc = bglin_solve(le, b.data(), &o, &rep, x.data(), hist.data(), det, sizeof det);
+                bglin_destroy(le);
+                if (rc != BGABP_OK) throw std::runtime_error(det);
+                detail = det;
+            } else {
+                bgabp_schedule sch{};
+                if (s.schedule == "sequential") sch.kind = BGABP_SCHED_SEQUENTIAL;
+                else if (s.schedule == "parallel-flood") sch.kind = BGABP_SCHED_FLOOD;
+                else if (s.schedule == "red-black") sch = {BGABP_SCHED_RED_BLACK_GRID, nx, nx, nullptr};
+                else if (s.schedule == "four-color") sch = {BGABP_SCHED_FOUR_COLOR_GRID, nx, nx, nullptr};
+                else throw std::invalid_argument("unknown schedule '" + s.schedule + "'");
+                if ((sch.kind == BGABP_SCHED_RED_BLACK_GRID || sch.kind == BGABP_SCHED_FOUR_COLOR_GRID) && nx == 0)
+                    sch.kind = sch.kind == BGABP_SCHED_RED_BLACK_GRID ? BGABP_SCHED_RED_BLACK : BGABP_SCHED_FOUR_COLOR;
+                bgabp_engine* e = nullptr;
+                int rc = bgabp_create(n, bgabp_problem_row_offsets(P.p), bgabp_problem_col_indices(P.p),
+                                      bgabp_problem_values(P.p), BGABP_LAYOUT_AUTO, &e, err, sizeof err);
+                if (rc != BGABP_OK) throw std::invalid_argument(err);
+                hist.assign((size_t)std::max(s.max_iter, 0) + 2, 0.0);
+                bgabp_options o{s.tol, s.max_iter, BGABP_STOP_RESIDUAL, 1e12};
+                char det[512] = {0};
+                rc = bgabp_solve(e, b.data(), &sch, &o, &rep, x.data(), hist.data(), det, sizeof det);
+                bgabp_destroy(e);
+                if (rc != BGABP_OK) throw std::runtime_error(det);
+                detail = det;
+            }
         } else {
-            throw std::invalid_argument("solver '" + s.solver + "' is not on the GPU path (gabp | mg:<smoother>)");
+            throw std::invalid_argument("solver '" + s.solver +
+                                        "' is not on the GPU path (gabp | generalized-gabp | mg:<smoother>)");
         }
         hist.resize((size_t)rep.iterations + 1);
         if (!s.out.empty()) {

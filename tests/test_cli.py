@@ -86,3 +86,25 @@ def test_cli_multigrid_and_matrix_market(tmp_path):
     r = _cli("--matrix", mtx, "--rhs", "random", "--seed", 3, "--schedule", "parallel-flood", "--tol", 1e-8,
              "--max-iter", 5)
     assert r.returncode == 3 and "status=max_iter iterations=5" in r.stderr
+
+
+def test_cli_smoother_names_follow_the_reference():
+    # belief_solve.cpp:58-75: flood-gabp / line-gabp are accepted names; unknown ones are errors
+    r = _cli("--problem", "poisson", "--solver", "mg:parallel-gabp", "--cycle", "V:4,3")
+    assert r.returncode == 1 and "unknown multigrid smoother" in r.stderr
+
+
+@pytest.mark.gpu
+def test_cli_generalized_gabp_and_line_smoother(orc):
+    r = _cli("--problem", "poisson", "--J", 5, "--solver", "generalized-gabp", "--tol", 1e-8, "--max-iter", 500)
+    p = g.assemble("poisson", 5)
+    from oracle.oracle import Csr
+    want = orc.region(Csr(p.A.n, p.A.row_offsets, p.A.col_indices, p.A.values),
+                      orc.grid_lines(p.nx, p.nx)).solve(p.b, tol=1e-8, max_iter=500)
+    assert r.returncode == 0 and f"iterations={want.iterations}" in r.stderr
+    got = [float(l.split(",")[1]) for l in r.stdout.strip().splitlines()[1:]]
+    np.testing.assert_allclose(got, want.residual_history, rtol=1e-9, atol=1e-15)
+    r = _cli("--problem", "poisson", "--solver", "mg:line-gabp", "--cycle", "V:6,4", "--tol", 1e-9)
+    assert r.returncode == 0 and "status=converged" in r.stderr
+    r = _cli("--problem", "poisson", "--solver", "mg:flood-gabp", "--cycle", "V:5,3", "--max-iter", 3)
+    assert r.returncode in (0, 2, 3) and "iterations=" in r.stderr
