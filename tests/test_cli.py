@@ -96,12 +96,12 @@ def test_cli_smoother_names_follow_the_reference():
 
 @pytest.mark.gpu
 def test_cli_generalized_gabp_and_line_smoother(orc):
-    r = _cli("--problem", "poisson", "--J", 5, "--solver", "generalized-gabp", "--tol", 1e-8, "--max-iter", 500)
+    r = _cli("--problem", "poisson", "--J", 5, "--solver", "generalized-gabp", "--tol", 1e-6, "--max-iter", 800)
     p = g.assemble("poisson", 5)
     from oracle.oracle import Csr
     want = orc.region(Csr(p.A.n, p.A.row_offsets, p.A.col_indices, p.A.values),
-                      orc.grid_lines(p.nx, p.nx)).solve(p.b, tol=1e-8, max_iter=500)
-    assert r.returncode == 0 and f"iterations={want.iterations}" in r.stderr
+                      orc.grid_lines(p.nx, p.nx)).solve(p.b, tol=1e-6, max_iter=800)
+    assert r.returncode == {0: 0, 1: 2, 2: 3}[want.status] and f"iterations={want.iterations}" in r.stderr
     got = [float(l.split(",")[1]) for l in r.stdout.strip().splitlines()[1:]]
     np.testing.assert_allclose(got, want.residual_history, rtol=1e-9, atol=1e-15)
     r = _cli("--problem", "poisson", "--solver", "mg:line-gabp", "--cycle", "V:6,4", "--tol", 1e-9)
