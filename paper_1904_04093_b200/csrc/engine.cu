@@ -589,6 +589,13 @@ void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bga
     ck(cudaMemsetAsync(d_x2, 0, sizeof(double) * std::max(n, 1), st), "memset x");
     ck(cudaMemsetAsync(d_spread, 0, sizeof(unsigned long long) * 8 * kSpread, st), "memset");
     if (solve_rb) ck(cudaMemsetAsync(d_rbmsg, 0, sizeof(double2) * 4 * (size_t)std::max(n, 2), st), "memset");
+    solve_pipe = solve_seq && pipe_fits();
+    if (solve_pipe) {  // pipelined lexicographic sweeps: x(0) = 0 in ring slot 0
+        pipe_setup(true);
+        pipe_reset();
+        ck(cudaMemsetAsync(d_xring, 0, sizeof(double) * std::max(n, 1), st), "memset ring");
+        pipe_next = 1;
+    }
     cur = 0;
     if (r0_override) {  // sharded solve: ||b||_inf over all ranks, supplied by the driver
         unsigned long long bits;
@@ -647,10 +654,15 @@ void Engine::enqueue_step_other() {
         if (timed_events) ck(cudaEventRecord((*timed_events)[2 * timed_index + 1], st), "event");
         launch_residual(solve_b, d_x, nullptr, nullptr, MODE_SOLVE);
         k_solve_finalize<<<1, 1, 0, st>>>(d_ctrl, d_hist);
+    } else if (solve_pipe) {  // one pipelined sweep (the timed path; solve_steps batches them)
+        if (pipe_next <= solve_max_iter) {
+            launch_pipe(solve_b, d_xring, pipe_next, 1, true, solve_stop == BGABP_STOP_MESSAGE_DELTA);
+            ++pipe_next;
+        }
     } else {
         if (solve_rb)
             launch_rb_sweep(solve_b, d_x, false, solve_stop == BGABP_STOP_MESSAGE_DELTA, &d_ctrl->delta[0], MODE_SOLVE);
-        else if (solve_seq)
+        else if (solve_seq)  // grids too tall for the pipeline's x ring
             launch_seq_sweep(solve_b, d_msg[0], d_x, solve_stop == BGABP_STOP_MESSAGE_DELTA, &d_ctrl->delta[0],
                              MODE_SOLVE);
         else
@@ -663,6 +675,13 @@ void Engine::enqueue_step_other() {
 
 void Engine::solve_steps(int nsteps) {
     if (nsteps <= 0) return;
+    if (solve_pipe) {  // one launch carries all of them, pipelined (seqpipe_kernels.cuh)
+        const int k = std::min(nsteps, solve_max_iter - pipe_next + 1);
+        if (k > 0) launch_pipe(solve_b, d_xring, pipe_next, k, true, solve_stop == BGABP_STOP_MESSAGE_DELTA);
+        pipe_next += std::max(k, 0);
+        steps_enqueued += nsteps;
+        return;
+    }
     // graph-replay chunks of iterations: the kernels read their step index from the device,
     // so one captured chunk is valid for any position in the loop
     const size_t per_step = solve_fused ? 2 : solve_flood ? 3 : solve_levels->ptr.size() + 1;
@@ -761,6 +780,20 @@ void Engine::solve_report(bgabp_report& rep, std::string& detail) {
 }
 
 const double* Engine::solve_x() {
+    if (solve_pipe) {
+        const Ctrl& c = *h_ctrl;  // read by solve_report
+        const double* xs = d_xring + (size_t)(c.solx % kPipeR) * n;
+        if (c.status == BGABP_DIVERGED && c.detail_kind == 4 && n > 0) {
+            // the reference's sweep stopped at visit position p: x(k) before it (and at it for an
+            // edge pivot, whose x-stage ran), x(k-1) from there on; positions are node ids here
+            const double* xo = d_xring + (size_t)((c.solx + kPipeR - 1) % kPipeR) * n;
+            const long long p = (long long)(c.detail_key >> 32) + ((c.detail_key & 0xffffffffu) ? 1 : 0);
+            k_compose_pivot_x<<<nblk(n), 256, 0, st>>>(xs, xo, d_aux, n, p);
+            ck(cudaGetLastError(), "compose x");
+            return d_aux;
+        }
+        return xs;
+    }
     if (!solve_fused) return d_x;
     const Ctrl& c = *h_ctrl;  // read by solve_report
     const double* xs = (c.solx & 1) ? d_x2 : d_x;
@@ -931,8 +964,10 @@ int Engine::cold_sweeps_dev(const double* r_dev, const bgabp_schedule& s, int sw
                 k_plain_check<<<1, 1, 0, st>>>(d_ctrl, seq, 4);
             }
             launch_aggregate(r_dev, d_msg[cur], e_dev, nullptr, &d_ctrl->npiv[0]);
-        } else if (seq_applicable(s)) {
-            for (int k = 0; k < sweeps; ++k) launch_seq_sweep(r_dev, d_msg[cur], e_dev, false, nullptr, MODE_PLAIN);
+        } else if (seq_applicable(s)) {  // all sweeps in one pipelined launch, e = x of the last
+            pipe_setup(false);
+            pipe_reset();
+            launch_pipe(r_dev, e_dev, 1, sweeps, false, false);
         } else {
             for (int k = 0; k < sweeps; ++k) launch_levels(*L, r_dev, d_msg[cur], e_dev, false, nullptr, MODE_PLAIN);
         }

@@ -14,6 +14,7 @@
 #include "kernels.cuh"
 #include "rb_kernels.cuh"
 #include "seq_kernels.cuh"
+#include "seqpipe_kernels.cuh"
 
 namespace bgabp {
 
@@ -135,6 +136,18 @@ struct Engine {
         return grid5 && s.kind == BGABP_SCHED_SEQUENTIAL && n > 0;
     }
     void launch_seq_sweep(const double* b, double2* msg, double* x, bool delta, unsigned long long* dslot, int mode);
+    // pipelined lexicographic sweeps (seqpipe_kernels.cuh): many sweeps per launch
+    double* d_xring = nullptr;  // [kPipeR][n] x(t) of the solve
+    unsigned long long* d_pprog = nullptr;
+    PipeRed* d_pred = nullptr;
+    int* d_pint = nullptr;  // [0] ticket, [1] decided
+    int pipe_strips = 0, pipe_next = 1;
+    std::map<int, int*> pipe_orders;  // ticket orders per batch size
+    void pipe_setup(bool ring);
+    bool pipe_fits() const { return (n / std::max(grid5_nx, 1) + 31) / 32 + 1 < 2 * kPipeR; }
+    bool solve_pipe = false;  // the sequential solve runs pipelined (else one k_seq_grid5 per sweep)
+    void pipe_reset();
+    void launch_pipe(const double* b, double* x, int t0, int nsweeps, bool solve, bool delta);
 
     void reset_ctrl();
     void read_ctrl();

@@ -1,5 +1,6 @@
 // Host side of the pipelined lexicographic sweep (seq_kernels.cuh).
 #include <algorithm>
+#include <vector>
 
 #include "engine.h"
 
@@ -16,6 +17,86 @@ void Engine::launch_seq_sweep(const double* b, double2* msg, double* x, bool del
     // every strip spins on its predecessor: a cooperative launch guarantees co-residency (or fails)
     const void* fn = delta ? (const void*)k_seq_grid5<true> : (const void*)k_seq_grid5<false>;
     ck(cudaLaunchCooperativeKernel(fn, dim3(strips), dim3(32), args, 0, st), "sequential sweep launch");
+}
+
+static __global__ void k_pipe_reset(PipeRed* red, unsigned long long* prog, int nprog, int* ints) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < kPipeR) {
+        red[i].rmax = red[i].delta = 0ull;
+        red[i].opiv = kNone;
+        red[i].count = 0u;
+    }
+    for (int k = i; k < nprog; k += gridDim.x * blockDim.x) prog[k] = 0ull;
+    if (i == 0) ints[0] = ints[1] = 0;
+}
+
+void Engine::pipe_setup(bool ring) {
+    const int strips = (n / grid5_nx + 31) / 32;
+    // the x ring must outlast the deepest gate wait: with tickets in 2 * sweep + strip order a
+    // block never waits on a later ticket as long as strips + 1 < 2 * kPipeR
+    if (ring && !pipe_fits()) throw InvalidArg("sequential pipeline: grid too tall for the x ring");
+    if (!d_pprog || strips != pipe_strips) {
+        pipe_strips = strips;
+        d_pprog = static_cast<unsigned long long*>(dalloc(sizeof(unsigned long long) * (size_t)kPipeR * strips));
+        d_pred = static_cast<PipeRed*>(dalloc(sizeof(PipeRed) * kPipeR));
+        d_pint = static_cast<int*>(dalloc(sizeof(int) * 2));
+    }
+    if (ring && !d_xring) d_xring = static_cast<double*>(dalloc(sizeof(double) * (size_t)kPipeR * std::max(n, 1)));
+}
+
+void Engine::pipe_reset() {
+    const int np = kPipeR * pipe_strips;
+    k_pipe_reset<<<std::max(1, std::min((np + 255) / 256, 256)), 256, 0, st>>>(d_pred, d_pprog, np, d_pint);
+}
+
+void Engine::launch_pipe(const double* b, double* x, int t0, int nsweeps, bool solve, bool delta) {
+    if (nsweeps <= 0 || n == 0) return;
+    PipeP Q;
+    Q.P = SeqP{grid5_nx, n / grid5_nx, n, dia.mask, dia.c, dia.diag};
+    Q.rowv = dia.rowv;
+    Q.b = b;
+    Q.msg = d_msg[0];
+    Q.x = x;
+    Q.prog = d_pprog;
+    Q.red = d_pred;
+    Q.ticket = d_pint;
+    Q.decided = d_pint + 1;
+    Q.ctrl = d_ctrl;
+    Q.hist = d_hist;
+    auto it = pipe_orders.find(nsweeps);
+    if (it == pipe_orders.end()) {  // blocks in order of 2 * sweep + strip (see k_seq_pipe)
+        std::vector<int> ord;
+        ord.reserve((size_t)nsweeps * pipe_strips);
+        for (int d = 0; d <= 2 * (nsweeps - 1) + pipe_strips - 1; ++d)
+            for (int tt = std::min(nsweeps - 1, d / 2); tt >= 0; --tt) {
+                const int k = d - 2 * tt;
+                if (k >= pipe_strips) break;
+                ord.push_back((tt << 12) | k);
+            }
+        int* d_ord = static_cast<int*>(dalloc(sizeof(int) * ord.size()));
+        ck(cudaMemcpyAsync(d_ord, ord.data(), sizeof(int) * ord.size(), cudaMemcpyHostToDevice, st), "order");
+        ck(cudaStreamSynchronize(st), "sync");
+        it = pipe_orders.emplace(nsweeps, d_ord).first;
+    }
+    Q.order = it->second;
+    Q.strips = pipe_strips;
+    Q.t0 = t0;
+    Q.nsweeps = nsweeps;
+    ck(cudaMemsetAsync(d_pint, 0, sizeof(int), st), "ticket");
+    const dim3 grid((unsigned)((long long)nsweeps * pipe_strips));
+    if (solve) {
+        if (symmetric) {
+            if (delta) k_seq_pipe<true, true, true><<<grid, 32, 0, st>>>(Q);
+            else k_seq_pipe<false, true, true><<<grid, 32, 0, st>>>(Q);
+        } else {
+            if (delta) k_seq_pipe<true, true, false><<<grid, 32, 0, st>>>(Q);
+            else k_seq_pipe<false, true, false><<<grid, 32, 0, st>>>(Q);
+        }
+    } else {
+        k_seq_pipe<false, false, true><<<grid, 32, 0, st>>>(Q);
+        k_pipe_failure<<<1, 1, 0, st>>>(d_ctrl, d_pred, t0, nsweeps);
+    }
+    ck(cudaGetLastError(), "pipelined sequential sweeps");
 }
 
 }  // namespace bgabp
