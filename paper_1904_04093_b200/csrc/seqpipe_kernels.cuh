@@ -48,6 +48,7 @@ struct PipeP {
     double* hist;
     const int* order;  // ticket -> (sweep - t0) << 12 | strip, in order of 2 * sweep + strip
     int strips, t0, nsweeps;
+    int gate;  // sweeps that may run ahead of the last stop decision (<= kPipeR)
 };
 
 __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
@@ -65,16 +66,19 @@ __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned l
 }
 
 // wait (lane 0) until `p` shows sweep `t` with at least `cols` columns; returns the columns seen.
-// Acquire load: the producer's release store orders its message / x writes before the flag; the
-// caller's __syncwarp then orders the rest of the warp's reads after this acquire.  Waiting warps
-// back off so they do not steal issue slots from the working ones.
+// The flag is read with a volatile (L2) load, not ld.acquire: on sm_100 an acquire invalidates the
+// SM's whole L1 (CCTL.IVALL), which wiped the read-only operands every other block on the SM keeps
+// there (ncu: L1 hit rate 0.8 %).  The data the flag guards is only ever read through L2 (ld.cg)
+// after the loop exits (no load is issued before the branch that depends on the flag resolves),
+// and the producer's fence orders its writes before the flag.  Waiting warps back off.
 __device__ __forceinline__ int pipe_wait(const unsigned long long* p, int t, int cols) {
     const unsigned long long want = ((unsigned long long)t << 32) | (unsigned)cols;
     unsigned long long v;
     int spins = 0;
-    while ((v = ld_acquire_u64(p)) < want) {
+    while ((v = ld_volatile_u64(p)) < want) {
         if (++spins > 16) __nanosleep(64);
     }
+    asm volatile("" ::: "memory");
     const unsigned long long got = v & 0xffffffffull;  // 0xffffffff: that block stopped early
     return (v >> 32) == (unsigned long long)t && got < 0x7fffffffull ? (int)got : 0x7fffffff;
 }
@@ -166,8 +170,8 @@ __device__ __forceinline__ void pipe_decide(volatile Ctrl* c, double* history, i
 }
 
 // SYMR: A is bit-symmetric, so the residual's row coefficients are the out-edge coefficients
-template <bool DELTA, bool SOLVE, bool SYMR>
-static __global__ void __launch_bounds__(32) k_seq_pipe(PipeP Q) {
+template <bool DELTA, bool SOLVE, bool SYMR, int MINB = 1>
+static __global__ void __launch_bounds__(32, MINB) k_seq_pipe(PipeP Q) {
     constexpr unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x;
     // Tickets follow 2 * sweep + strip: every dependency of a block -- (t, k-1), (t-1, k),
@@ -200,7 +204,7 @@ static __global__ void __launch_bounds__(32) k_seq_pipe(PipeP Q) {
                     go = 0;
                     break;
                 }
-                if (*(volatile int*)Q.decided >= t - kPipeR + 1) break;
+                if (*(volatile int*)Q.decided >= t - Q.gate + 1) break;
                 __nanosleep(256);
             }
         }
