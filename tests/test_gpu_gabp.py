@@ -328,3 +328,55 @@ def test_fused_solve_every_slot_count(orc, ref, kind):
         assert got.residual_history.tobytes() == want.residual_history.tobytes()
         if want.status != 1:
             assert got.solution.tobytes() == want.solution.tobytes()
+
+
+# ---- pipelined lexicographic solve (seqpipe_kernels.cuh): many sweeps per launch ---------------
+def _ocsr(orc, A):
+    from oracle.oracle import Csr
+    return Csr(A.n, A.row_offsets, A.col_indices, A.values)
+
+
+def _same_report(got, want):
+    assert (int(got.status), got.iterations, got.detail) == (want.status, want.iterations, want.detail)
+    assert got.residual_history.tobytes() == want.residual_history.tobytes()
+    assert got.solution.tobytes() == want.solution.tobytes()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("stop,tol", [(0, 1e-8), (1, 1e-9)])
+def test_sequential_pipeline_nonsymmetric_grid(orc, ref, stop, tol):
+    """Config-3 style upwind operator (bit-nonsymmetric): residual rows read A_{j,k}, not A_{k,j}."""
+    o = ref or orc
+    p = g.config_problem(3, size=40)
+    want = o.engine(_ocsr(o, p.A)).solve(p.b, OSched.sequential(), tol=tol, max_iter=5000, stop=stop)
+    got = g.GabpEngine(p.A).solve(p.b, g.Schedule.sequential(), g.GabpOptions(tol=tol, max_iter=5000, stop=stop))
+    assert want.status == 0
+    _same_report(got, want)
+
+
+@pytest.mark.gpu
+def test_sequential_pipeline_long_solve_wraps_the_ring(orc, ref):
+    """Poisson 64^2 to 1e-8: ~2900 pipelined sweeps over many launches and ring wrap-arounds."""
+    o = ref or orc
+    A = orc.poisson5(64, 64)
+    b = orc.rng(0).vector(A.n)
+    want = o.engine(A).solve(b, OSched.sequential(), tol=1e-8, max_iter=20000)
+    got = g.GabpEngine(A).solve(b, g.Schedule.sequential(), g.GabpOptions(tol=1e-8, max_iter=20000))
+    assert want.status == 0 and want.iterations > 1000
+    _same_report(got, want)
+
+
+@pytest.mark.gpu
+def test_sequential_pipeline_pivot_stop_returns_the_partial_x(orc, ref):
+    """Node 1's precision cancels in sweep 1 (A_11 = A_10 A_01 / A_00): the reference stops there
+    with x updated at node 0 only; the pipeline composes exactly that x from its ring."""
+    o = ref or orc
+    D = orc.poisson5(3, 3).dense()
+    D[1, 1] = 0.25
+    r, c = np.nonzero(D)
+    A = orc.make_csr(9, r, c, D[r, c])
+    b = np.linspace(1.0, 2.0, 9)
+    want = o.engine(A).solve(b, OSched.sequential(), tol=1e-10, max_iter=100)
+    got = g.GabpEngine(A).solve(b, g.Schedule.sequential(), g.GabpOptions(tol=1e-10, max_iter=100))
+    assert want.status == 1 and "pivot" in want.detail
+    _same_report(got, want)
