@@ -270,6 +270,26 @@ def run_gpu(args, world, rank, local):
     h2d = 8 * n  # b per solve call
     d2h = 8 * n + 8 * (e2e_sweeps + 1)  # x + residual history per call
 
+    # ---- the other schedules on the same system: solve iterations per ms, device-resident -------
+    schedules = {}
+    if info["num_slots"] == 4 and not args.no_schedules:
+        nxg = P.nx
+        for name, sch, k in (("red_black", g.Schedule.red_black_grid(nxg, nxg), 128),
+                             ("sequential_pipelined", g.Schedule.sequential(), 256)):
+            eng.solve_device_begin(b_dev.data_ptr(), sch, g.GabpOptions(tol=0.0, max_iter=k + 8))
+            eng.solve_device_steps(4)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            eng.solve_device_steps(k)
+            e1.record(stream)
+            e1.synchronize()
+            st_, its_, _, _ = eng.solve_device_end()
+            assert its_ == k + 4, (name, st_, its_)
+            schedules[name] = {"ms_per_iteration": e0.elapsed_time(e1) / k, "iterations_timed": k,
+                               "edge_updates_per_s": E * k / (e0.elapsed_time(e1) / 1e3)}
+        schedules["flood"] = {"ms_per_iteration": ms_max / args.steps}
+
     # ---- the configuration's own run: solve to 1e-8 (cap 20000) or the fixed 300 sweeps ---------
     cap = 300 if args.config == 4 else 20000
     tts = None
@@ -300,6 +320,8 @@ def run_gpu(args, world, rank, local):
             "gpu_launches": 2 * args.steps, "clocks": clk.summary()}
     if tts is not None:
         line["solve"] = tts
+    if schedules:
+        line["schedules"] = schedules  # same system, sweep + residual + stop test per iteration
     if args.config != 2:
         line["data"] = f"synthetic (BASELINE.json config {args.config})"
         line["roofline"]["kernel"] = line["roofline"]["kernel"].replace("<4>", f"<{info['num_slots']}>")
@@ -413,6 +435,7 @@ def main():
     ap.add_argument("--e2e-calls", type=int, default=3)
     ap.add_argument("--ref-iters", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-schedules", action="store_true", help="skip the red-black / sequential timings")
     ap.add_argument("--mg-J", type=int, default=12)
     ap.add_argument("--mg-cycles", type=int, default=100)
     ap.add_argument("--mg-cpu-J", type=int, default=9)
