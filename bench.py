@@ -244,6 +244,9 @@ def run_gpu(args, world, rank, local):
     bytes_sweep = float(info["bytes_per_sweep"]) + 8.0 * n + (0.0 if info["symmetric_values"] else 8.0 * E)
     peak, peak_src = peaks()
     achieved = bytes_sweep / t_sweep / 1e9
+    # a constant-coefficient stencil (config 2) runs the variant with the coefficients and the
+    # diagonal as kernel parameters: it moves 32E + 28n, less than the SURVEY formula counts
+    kernel_bytes = 32.0 * E + 28.0 * n if info.get("uniform_coefficients") else bytes_sweep
     traffic = None
     tp = os.path.join(ROOT, "profiles", "flood_traffic.json")
     if os.path.exists(tp):
@@ -312,7 +315,12 @@ def run_gpu(args, world, rank, local):
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "peak_source": peak_src, "bytes_per_launch": bytes_sweep,
                          "bytes_formula": "40*E + 24*n (B_sweep, SURVEY.md 8(d)) + 8*n (x read of the fused residual)", "us_per_launch": t_sweep * 1e6,
-                         "frac_of_8TBs": achieved / 8000.0, "share_of_step": t_sweep * 1e3 / (ms_max / args.steps)},
+                         "frac_of_8TBs": achieved / 8000.0, "share_of_step": t_sweep * 1e3 / (ms_max / args.steps),
+                         "kernel_bytes_per_launch": kernel_bytes,
+                         "kernel_frac": kernel_bytes / t_sweep / 1e9 / peak,
+                         "kernel_bytes_note": ("uniform-coefficient variant (A's coefficients and diagonal are kernel "
+                                               "parameters): 32*E + 28*n per launch; frac counts SURVEY bytes")
+                         if info.get("uniform_coefficients") else "same as bytes_per_launch"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / e2e_sweeps,
                     "d2h_bytes_per_step": d2h / e2e_sweeps,
                     "how": f"{args.e2e_calls} x bgabp_solve(pinned host b and x, max_iter={e2e_sweeps}) incl. H2D b, "

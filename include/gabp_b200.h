@@ -78,6 +78,8 @@ typedef struct {
     double bytes_per_sweep;       /* algorithmic B_sweep = 40 E + 24 n */
     double bytes_per_residual;    /* algorithmic B_res = 8 nnz + 16 n */
     long long device_bytes;       /* device memory held by the handle */
+    int uniform_coefficients;     /* DIA constant-coefficient stencil: coefficients and diagonal are
+                                     kernel parameters, not arrays (the solve step reads 32 E + 28 n) */
 } bgabp_info;
 
 typedef struct bgabp_engine bgabp_engine;

@@ -213,6 +213,38 @@ void Engine::build(int n_, const int* ro_, const int* ci_, const double* v_, int
             grid5 = clean;
             grid5_nx = gx;
         }
+        // constant-coefficient stencil: one bit pattern per slot over every out-edge, one for the
+        // diagonal, and bit-symmetric A (the residual reads the same values)
+        dia.uniform = 0;
+        if (symmetric && n > 0) {
+            bool unif = true;
+            for (int s2 = 0; s2 < S && unif; ++s2) {
+                bool have = false;
+                unsigned long long ref = 0ull;
+                for (int i = 0; i < n && unif; ++i) {
+                    if (!(mask[i] & (1u << (16 + s2)))) continue;
+                    unsigned long long v;
+                    std::memcpy(&v, &c[(size_t)s2 * n + i], sizeof v);
+                    if (!have) {
+                        ref = v;
+                        have = true;
+                        dia.cu[s2] = c[(size_t)s2 * n + i];
+                    } else if (v != ref) {
+                        unif = false;
+                    }
+                }
+                if (!have) dia.cu[s2] = 0.0;
+            }
+            unsigned long long d0;
+            std::memcpy(&d0, &diag[0], sizeof d0);
+            for (int i = 1; i < n && unif; ++i) {
+                unsigned long long v;
+                std::memcpy(&v, &diag[i], sizeof v);
+                unif = v == d0;
+            }
+            dia.uniform = unif ? 1 : 0;
+            dia.du = diag[0];
+        }
         dia.mask = upload(mask);
         dia.c = upload(c);
         dia.rowv = symmetric ? dia.c : upload(rowv);
@@ -624,8 +656,11 @@ void Engine::enqueue_fused_kernel() {
         const bool dl = solve_stop == BGABP_STOP_MESSAGE_DELTA;
         const unsigned g = nblk(std::max(dia.j1 - dia.j0, 1));
         // register cap per slot count: 4 resident blocks for 2-4 slots, fewer for 6-8 (no spills)
-#define FUSED(SS_, MB_, DF_)                                                                                       \
-    if (symmetric) {                                                                                               \
+#define FUSED(SS_, MB_, DF_, MBU_, DFU_)                                                                            \
+    if (dia.uniform) {                                                                                             \
+        if (dl) k_flood_solve_dia<SS_, true, true, MBU_, DFU_, true, false, true, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_x, d_x2, d_ctrl, d_spread); \
+        else k_flood_solve_dia<SS_, false, true, MBU_, DFU_, true, false, true, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_x, d_x2, d_ctrl, d_spread); \
+    } else if (symmetric) {                                                                                        \
         if (dl) k_flood_solve_dia<SS_, true, true, MB_, DF_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_x, d_x2, d_ctrl, d_spread); \
         else k_flood_solve_dia<SS_, false, true, MB_, DF_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_x, d_x2, d_ctrl, d_spread); \
     } else {                                                                                                       \
@@ -635,11 +670,13 @@ void Engine::enqueue_fused_kernel() {
         if (timed_events) ck(cudaEventRecord((*timed_events)[2 * timed_index], st), "event");
         // (resident blocks, deferred x loads) per slot count, from tools/exp_flood.cu on the B200:
         // S=4 2048^2: (3, early) 133 us vs (4, deferred) 135; S=6 256^3: (4, deferred) 696 us vs (3, early) 725
+        // uniform-coefficient variants (no coefficient / diagonal loads): S=4 2048^2 112.6 us with
+        // (4, early), S=6 256^3 602 us with (4, deferred)
         switch (S) {
-            case 2: FUSED(2, 4, true) break;
-            case 4: FUSED(4, 3, false) break;
-            case 6: FUSED(6, 4, true) break;
-            case 8: FUSED(8, 2, true) break;
+            case 2: FUSED(2, 4, true, 4, true) break;
+            case 4: FUSED(4, 3, false, 4, false) break;
+            case 6: FUSED(6, 4, true, 4, true) break;
+            case 8: FUSED(8, 2, true, 2, true) break;
             default: throw InvalidArg("gabp: unsupported DIA slot count");
         }
 #undef FUSED
@@ -1098,6 +1135,7 @@ int bgabp_get_info(const bgabp_engine* h, bgabp_info* info) {
     info->num_slots = E.S;
     info->symmetric_values = E.symmetric ? 1 : 0;
     info->bytes_per_sweep = 40.0 * (double)E.num_edges + 24.0 * E.n;
+    info->uniform_coefficients = (E.layout == BGABP_LAYOUT_DIA && E.dia.uniform) ? 1 : 0;
     info->bytes_per_residual = 8.0 * (double)E.nnz + 16.0 * E.n;
     info->device_bytes = E.device_bytes;
     return BGABP_OK;

@@ -103,7 +103,8 @@ def test_cli_generalized_gabp_and_line_smoother(orc):
                       orc.grid_lines(p.nx, p.nx)).solve(p.b, tol=1e-6, max_iter=800)
     assert r.returncode == {0: 0, 1: 2, 2: 3}[want.status] and f"iterations={want.iterations}" in r.stderr
     got = [float(l.split(",")[1]) for l in r.stdout.strip().splitlines()[1:]]
-    np.testing.assert_allclose(got, want.residual_history, rtol=1e-9, atol=1e-15)
+    # line solves agree to rounding (O(N) vs dense local solves): relative to r0 for small residuals
+    np.testing.assert_allclose(got, want.residual_history, rtol=1e-9, atol=1e-10 * want.residual_history[0])
     r = _cli("--problem", "poisson", "--solver", "mg:line-gabp", "--cycle", "V:6,4", "--tol", 1e-9)
     assert r.returncode == 0 and "status=converged" in r.stderr
     r = _cli("--problem", "poisson", "--solver", "mg:flood-gabp", "--cycle", "V:5,3", "--max-iter", 3)

@@ -132,6 +132,21 @@ void run(int N) {
                                                                                     ctrl, spread);           \
         k_solve_decide_lag2<<<1, 64>>>(ctrl, hist, spread);                                                   \
     });
+#define U(NAME, MINB, DEFER)                                                                                 \
+    timeit(NAME, [&] {                                                                                        \
+        P.uniform = 1;                                                                                        \
+        k_flood_solve_dia<S, false, true, MINB, DEFER, true, false, true, true><<<g, 256>>>(P, db, m0, m1, x0, \
+                                                                                           x1, ctrl, spread); \
+        k_solve_decide_lag2<<<1, 64>>>(ctrl, hist, spread);                                                   \
+        P.uniform = 0;                                                                                        \
+    });
+    for (int s = 0; s < S; ++s) P.cu[s] = -1.0;
+    P.du = 2.0 * dims + 0.01;
+    U("UNIF MINB=4 DEFER", 4, true)
+    U("UNIF MINB=3 DEFER", 3, true)
+    U("UNIF MINB=4 early-x", 4, false)
+    U("UNIF MINB=3 early-x", 3, false)
+    U("UNIF MINB=2 early-x", 2, false)
     W("MINB=4 DEFER predicated", 4, true, false)
     W("MINB=4 DEFER unconditional", 4, true, true)
     W("MINB=3 DEFER unconditional", 3, true, true)
