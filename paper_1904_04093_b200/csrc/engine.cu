@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -298,7 +299,6 @@ void Engine::build(int n_, const int* ro_, const int* ci_, const double* v_, int
     d_r = static_cast<double*>(dalloc(vb));
     d_e = static_cast<double*>(dalloc(vb));
     d_aux = static_cast<double*>(dalloc(vb));
-    d_x2 = static_cast<double*>(dalloc(vb));
     d_spread = static_cast<unsigned long long*>(dalloc(sizeof(unsigned long long) * 8 * kSpread));
     cur = 0;
     ck(cudaStreamSynchronize(st), "setup sync");
@@ -618,7 +618,10 @@ void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bga
     for (int k = 0; k < 2; ++k)
         ck(cudaMemsetAsync(d_msg[k], 0, sizeof(double2) * (size_t)std::max<long long>(nslots, 1), st), "memset");
     ck(cudaMemsetAsync(d_x, 0, sizeof(double) * std::max(n, 1), st), "memset x");
-    ck(cudaMemsetAsync(d_x2, 0, sizeof(double) * std::max(n, 1), st), "memset x");
+    if (solve_fused) {
+        if (!d_xf) d_xf = static_cast<double*>(dalloc(sizeof(double) * 4 * (size_t)std::max(n, 1)));
+        ck(cudaMemsetAsync(d_xf, 0, sizeof(double) * 4 * (size_t)std::max(n, 1), st), "memset x ring");
+    }
     ck(cudaMemsetAsync(d_spread, 0, sizeof(unsigned long long) * 8 * kSpread, st), "memset");
     if (solve_rb) ck(cudaMemsetAsync(d_rbmsg, 0, sizeof(double2) * 4 * (size_t)std::max(n, 2), st), "memset");
     solve_pipe = solve_seq && pipe_fits();
@@ -658,14 +661,14 @@ void Engine::enqueue_fused_kernel() {
         // register cap per slot count: 4 resident blocks for 2-4 slots, fewer for 6-8 (no spills)
 #define FUSED(SS_, MB_, DF_, MBU_, DFU_)                                                                            \
     if (dia.uniform) {                                                                                             \
-        if (dl) k_flood_solve_dia<SS_, true, true, MBU_, DFU_, true, false, true, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_x, d_x2, d_ctrl, d_spread); \
-        else k_flood_solve_dia<SS_, false, true, MBU_, DFU_, true, false, true, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_x, d_x2, d_ctrl, d_spread); \
+        if (dl) k_flood_solve_dia<SS_, true, true, MBU_, DFU_, true, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread); \
+        else k_flood_solve_dia<SS_, false, true, MBU_, DFU_, true, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread); \
     } else if (symmetric) {                                                                                        \
-        if (dl) k_flood_solve_dia<SS_, true, true, MB_, DF_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_x, d_x2, d_ctrl, d_spread); \
-        else k_flood_solve_dia<SS_, false, true, MB_, DF_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_x, d_x2, d_ctrl, d_spread); \
+        if (dl) k_flood_solve_dia<SS_, true, true, MB_, DF_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread); \
+        else k_flood_solve_dia<SS_, false, true, MB_, DF_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread); \
     } else {                                                                                                       \
-        if (dl) k_flood_solve_dia<SS_, true, false, MB_, DF_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_x, d_x2, d_ctrl, d_spread); \
-        else k_flood_solve_dia<SS_, false, false, MB_, DF_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_x, d_x2, d_ctrl, d_spread); \
+        if (dl) k_flood_solve_dia<SS_, true, false, MB_, DF_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread); \
+        else k_flood_solve_dia<SS_, false, false, MB_, DF_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread); \
     }
         if (timed_events) ck(cudaEventRecord((*timed_events)[2 * timed_index], st), "event");
         // (resident blocks, deferred x loads) per slot count, from tools/exp_flood.cu on the B200:
@@ -833,10 +836,10 @@ const double* Engine::solve_x() {
     }
     if (!solve_fused) return d_x;
     const Ctrl& c = *h_ctrl;  // read by solve_report
-    const double* xs = (c.solx & 1) ? d_x2 : d_x;
+    const double* xs = d_xf + (size_t)(c.solx & 3) * n;
     if (c.status == BGABP_DIVERGED && c.detail_kind == 1 && n > 0) {
         // the reference stops its x-stage at the pivot node: x(k) below it, x(k-1) from it on
-        const double* xo = (c.solx & 1) ? d_x : d_x2;
+        const double* xo = d_xf + (size_t)((c.solx - 1) & 3) * n;
         k_compose_pivot_x<<<nblk(n), 256, 0, st>>>(xs, xo, d_aux, n, (long long)c.detail_key - dia.gofs);
         ck(cudaGetLastError(), "compose x");
         return d_aux;
@@ -1270,6 +1273,7 @@ int bgabp_solve_device_steps_timed(bgabp_engine* h, int nsteps, double* hot_ms) 
         std::vector<cudaEvent_t> ev(2 * (size_t)std::max(nsteps, 0));
         for (auto& e : ev) ck(cudaEventCreate(&e), "event");
         E.timed_events = &ev;
+        const int launches = nsteps;
         for (int k = 0; k < nsteps; ++k) {
             E.timed_index = k;
             E.enqueue_step();
@@ -1278,7 +1282,7 @@ int bgabp_solve_device_steps_timed(bgabp_engine* h, int nsteps, double* hot_ms) 
         ck(cudaGetLastError(), "timed steps");
         ck(cudaStreamSynchronize(E.st), "sync");
         double total = 0.0;
-        for (int k = 0; k < nsteps; ++k) {
+        for (int k = 0; k < launches; ++k) {
             float ms = 0.f;
             ck(cudaEventElapsedTime(&ms, ev[2 * k], ev[2 * k + 1]), "elapsed");
             total += ms;
@@ -1502,7 +1506,11 @@ int bgabp_shard_step_decide(bgabp_engine* h) {
 }
 
 void* bgabp_shard_msg(bgabp_engine* h, int which) { return (void*)h->E.d_msg[which & 1]; }
-void* bgabp_shard_x(bgabp_engine* h, int which) { return (void*)((which & 1) ? h->E.d_x2 : h->E.d_x); }
+void* bgabp_shard_x(bgabp_engine* h, int which) {  // x(k) ring slot k & 3 (allocated by shard_solve_begin)
+    Engine& E = h->E;
+    if (!E.d_xf) E.d_xf = static_cast<double*>(E.dalloc(sizeof(double) * 4 * (size_t)std::max(E.n, 1)));
+    return (void*)(E.d_xf + (size_t)(which & 3) * E.n);
+}
 
 int bgabp_shard_pack(bgabp_engine* h, int which, int lo, int len, void* out_dev) {
     ABI_GUARD(nullptr, 0, {

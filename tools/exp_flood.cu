@@ -80,13 +80,13 @@ void run(int N) {
     P.diag = up(diag);
     double* db = up(b);
     double2 *m0, *m1;
-    double *x0, *x1, *hist;
+    double *xr, *hist;
     CK(cudaMalloc(&m0, sizeof(double2) * S * n));
     CK(cudaMalloc(&m1, sizeof(double2) * S * n));
     CK(cudaMemset(m0, 0, sizeof(double2) * S * n));
     CK(cudaMemset(m1, 0, sizeof(double2) * S * n));
-    CK(cudaMalloc(&x0, sizeof(double) * n));
-    CK(cudaMalloc(&x1, sizeof(double) * n));
+    CK(cudaMalloc(&xr, sizeof(double) * 4 * n));
+    CK(cudaMemset(xr, 0, sizeof(double) * 4 * n));
     CK(cudaMalloc(&hist, sizeof(double) * 100000));
     Ctrl* ctrl;
     unsigned long long* spread;
@@ -128,15 +128,13 @@ void run(int N) {
     };
 #define W(NAME, MINB, DEFER, UNC)                                                                             \
     timeit(NAME, [&] {                                                                                        \
-        k_flood_solve_dia<S, false, true, MINB, DEFER, true, false, UNC><<<g, 256>>>(P, db, m0, m1, x0, x1, \
-                                                                                    ctrl, spread);           \
+        k_flood_solve_dia<S, false, true, MINB, DEFER, UNC><<<g, 256>>>(P, db, m0, m1, xr, ctrl, spread); \
         k_solve_decide_lag2<<<1, 64>>>(ctrl, hist, spread);                                                   \
     });
 #define U(NAME, MINB, DEFER)                                                                                 \
     timeit(NAME, [&] {                                                                                        \
         P.uniform = 1;                                                                                        \
-        k_flood_solve_dia<S, false, true, MINB, DEFER, true, false, true, true><<<g, 256>>>(P, db, m0, m1, x0, \
-                                                                                           x1, ctrl, spread); \
+        k_flood_solve_dia<S, false, true, MINB, DEFER, true, true><<<g, 256>>>(P, db, m0, m1, xr, ctrl, spread); \
         k_solve_decide_lag2<<<1, 64>>>(ctrl, hist, spread);                                                   \
         P.uniform = 0;                                                                                        \
     });
@@ -154,7 +152,7 @@ void run(int N) {
     W("MINB=3 early-x unconditional", 3, false, true)
     W("MINB=2 early-x unconditional", 2, false, true)
     timeit("MINB=3 early-x unconditional DELTA", [&] {
-        k_flood_solve_dia<S, true, true, 3, false, true, false, true><<<g, 256>>>(P, db, m0, m1, x0, x1, ctrl, spread);
+        k_flood_solve_dia<S, true, true, 3, false, true><<<g, 256>>>(P, db, m0, m1, xr, ctrl, spread);
         k_solve_decide_lag2<<<1, 64>>>(ctrl, hist, spread);
     });
     cudaFree(m0);
