@@ -619,8 +619,8 @@ void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bga
         ck(cudaMemsetAsync(d_msg[k], 0, sizeof(double2) * (size_t)std::max<long long>(nslots, 1), st), "memset");
     ck(cudaMemsetAsync(d_x, 0, sizeof(double) * std::max(n, 1), st), "memset x");
     if (solve_fused) {
-        if (!d_xf) d_xf = static_cast<double*>(dalloc(sizeof(double) * 4 * (size_t)std::max(n, 1)));
-        ck(cudaMemsetAsync(d_xf, 0, sizeof(double) * 4 * (size_t)std::max(n, 1), st), "memset x ring");
+        if (!d_xf) d_xf = static_cast<double*>(dalloc(sizeof(double) * kXRing * (size_t)std::max(n, 1)));
+        ck(cudaMemsetAsync(d_xf, 0, sizeof(double) * kXRing * (size_t)std::max(n, 1), st), "memset x ring");
     }
     ck(cudaMemsetAsync(d_spread, 0, sizeof(unsigned long long) * 8 * kSpread, st), "memset");
     if (solve_rb) ck(cudaMemsetAsync(d_rbmsg, 0, sizeof(double2) * 4 * (size_t)std::max(n, 2), st), "memset");
@@ -658,9 +658,18 @@ void Engine::enqueue_fused_kernel() {
     {
         const bool dl = solve_stop == BGABP_STOP_MESSAGE_DELTA;
         const unsigned g = nblk(std::max(dia.j1 - dia.j0, 1));
+        const bool sharded = dia.j0 != 0 || dia.j1 != n || dia.gofs != 0;
         // register cap per slot count: 4 resident blocks for 2-4 slots, fewer for 6-8 (no spills)
 #define FUSED(SS_, MB_, DF_, MBU_, DFU_)                                                                            \
-    if (dia.uniform) {                                                                                             \
+    if (sharded) {                                                                                                 \
+        if (symmetric) {                                                                                           \
+            if (dl) k_flood_solve_dia<SS_, true, true, MB_, DF_, true, false, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread); \
+            else k_flood_solve_dia<SS_, false, true, MB_, DF_, true, false, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread); \
+        } else {                                                                                                   \
+            if (dl) k_flood_solve_dia<SS_, true, false, MB_, DF_, true, false, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread); \
+            else k_flood_solve_dia<SS_, false, false, MB_, DF_, true, false, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread); \
+        }                                                                                                          \
+    } else if (dia.uniform) {                                                                                      \
         if (dl) k_flood_solve_dia<SS_, true, true, MBU_, DFU_, true, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread); \
         else k_flood_solve_dia<SS_, false, true, MBU_, DFU_, true, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread); \
     } else if (symmetric) {                                                                                        \
@@ -836,10 +845,10 @@ const double* Engine::solve_x() {
     }
     if (!solve_fused) return d_x;
     const Ctrl& c = *h_ctrl;  // read by solve_report
-    const double* xs = d_xf + (size_t)(c.solx & 3) * n;
+    const double* xs = xslot(d_xf, n, c.solx);
     if (c.status == BGABP_DIVERGED && c.detail_kind == 1 && n > 0) {
         // the reference stops its x-stage at the pivot node: x(k) below it, x(k-1) from it on
-        const double* xo = d_xf + (size_t)((c.solx - 1) & 3) * n;
+        const double* xo = xslot(d_xf, n, c.solx - 1);
         k_compose_pivot_x<<<nblk(n), 256, 0, st>>>(xs, xo, d_aux, n, (long long)c.detail_key - dia.gofs);
         ck(cudaGetLastError(), "compose x");
         return d_aux;
@@ -1506,10 +1515,10 @@ int bgabp_shard_step_decide(bgabp_engine* h) {
 }
 
 void* bgabp_shard_msg(bgabp_engine* h, int which) { return (void*)h->E.d_msg[which & 1]; }
-void* bgabp_shard_x(bgabp_engine* h, int which) {  // x(k) ring slot k & 3 (allocated by shard_solve_begin)
+void* bgabp_shard_x(bgabp_engine* h, int which) {  // the slot holding x(which)
     Engine& E = h->E;
-    if (!E.d_xf) E.d_xf = static_cast<double*>(E.dalloc(sizeof(double) * 4 * (size_t)std::max(E.n, 1)));
-    return (void*)(E.d_xf + (size_t)(which & 3) * E.n);
+    if (!E.d_xf) E.d_xf = static_cast<double*>(E.dalloc(sizeof(double) * kXRing * (size_t)std::max(E.n, 1)));
+    return (void*)xslot(E.d_xf, E.n, which);
 }
 
 int bgabp_shard_pack(bgabp_engine* h, int which, int lo, int len, void* out_dev) {

@@ -111,8 +111,9 @@ class GpuShard:
         self.stream = torch.cuda.ExternalStream(self.eng.stream(), device=self.device)
         self.b = torch.as_tensor(np.ascontiguousarray(b_local, np.float64), device=self.device)
         self.red4 = _device_view(lib().bgabp_shard_reduce_buffer(self.eng.handle), 4, torch.int64, self.device)
+        # x(k) lives in slot k % 2 (kXRing in kernels.cuh); views of both slots
         self.x = [_device_view(lib().bgabp_shard_x(self.eng.handle, k), L.n_local, torch.float64, self.device)
-                  for k in range(4)]  # x(k) in ring slot k & 3
+                  for k in range(2)]
 
     def begin(self, opt: GabpOptions, r0: float):
         o = opt._c()
@@ -171,7 +172,7 @@ class Exchange:
             s.red4.copy_(acc)
 
     def halo(self, which_msg, which_x):
-        """Messages of sweep t (buffer which_msg) and x(t-1) (x ring slot which_x)."""
+        """Messages of sweep t (buffer which_msg) and x(t-1) (x slot which_x)."""
         ops, pending = [], []
         P = len(self.layouts)
         for p in range(P):
@@ -246,7 +247,7 @@ def sharded_solve(shards: dict, layouts, owner, world, b_inf, opt: GabpOptions, 
             for s in shards.values():
                 s.decide()
             sync()
-            ex.halo(t & 1, (t - 1) & 3)
+            ex.halo(t & 1, (t - 1) & 1)
             sync()
             t += 1
             if t % poll_every == 0 or t > cap:

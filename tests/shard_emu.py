@@ -63,7 +63,7 @@ class CpuShard:
         self.b = np.ascontiguousarray(b_local, np.float64)
         self.msg = [np.zeros((S, n, 2)), np.zeros((S, n, 2))]
         self.red4 = torch.zeros(4, dtype=torch.int64)
-        self.x = [torch.zeros(n, dtype=torch.float64) for _ in range(4)]  # x(k) in slot k & 3
+        self.x = [torch.zeros(n, dtype=torch.float64) for _ in range(2)]  # x(k) in slot k & 1
 
     # ---- control block (Ctrl) --------------------------------------------------------------
     def begin(self, opt, r0):
@@ -86,8 +86,8 @@ class CpuShard:
         t = self.step
         mi = self.msg[0] if t & 1 else self.msg[1]
         mo = self.msg[1] if t & 1 else self.msg[0]
-        xw = self.x[(t - 1) & 3].numpy()
-        xr = self.x[(t - 2) & 3].numpy()
+        xw = self.x[(t - 1) & 1].numpy()
+        xr = self.x[(t - 2) & 1].numpy()
         L, S, n, g = self.L, self.S, self.n, self.L.glo
         J = np.arange(L.own_lo, L.own_hi)
         IN, OUT = self.IN[:, J], self.OUT[:, J]
@@ -211,9 +211,9 @@ class CpuShard:
         detail = {1: f"zero pivot at node {self.detail_key}",
                   2: f"zero pivot on edge {self.detail_key >> 32}->{self.detail_key & 0xffffffff}",
                   3: "residual blowup"}.get(self.detail_kind, "") if self.status == 1 else ""
-        x = self.x[self.solx & 3].numpy().copy()
+        x = self.x[self.solx & 1].numpy().copy()
         if self.status == 1 and self.detail_kind == 1:  # x(k) below the pivot node, x(k-1) from it on
             glob = np.arange(self.n) + self.L.glo
-            x = np.where(glob < self.detail_key, x, self.x[(self.solx - 1) & 3].numpy())
+            x = np.where(glob < self.detail_key, x, self.x[(self.solx - 1) & 1].numpy())
         x = x[self.L.own_lo:self.L.own_hi]
         return self.status, self.iterations, detail, x, self.hist[:self.iterations + 1].copy()

@@ -85,8 +85,8 @@ void run(int N) {
     CK(cudaMalloc(&m1, sizeof(double2) * S * n));
     CK(cudaMemset(m0, 0, sizeof(double2) * S * n));
     CK(cudaMemset(m1, 0, sizeof(double2) * S * n));
-    CK(cudaMalloc(&xr, sizeof(double) * 4 * n));
-    CK(cudaMemset(xr, 0, sizeof(double) * 4 * n));
+    CK(cudaMalloc(&xr, sizeof(double) * kXRing * n));
+    CK(cudaMemset(xr, 0, sizeof(double) * kXRing * n));
     CK(cudaMalloc(&hist, sizeof(double) * 100000));
     Ctrl* ctrl;
     unsigned long long* spread;
@@ -145,6 +145,10 @@ void run(int N) {
     U("UNIF MINB=4 early-x", 4, false)
     U("UNIF MINB=3 early-x", 3, false)
     U("UNIF MINB=2 early-x", 2, false)
+    timeit("NONSYM MINB=3 early-x", [&] {
+        k_flood_solve_dia<S, false, false, 3, false, true><<<g, 256>>>(P, db, m0, m1, xr, ctrl, spread);
+        k_solve_decide_lag2<<<1, 64>>>(ctrl, hist, spread);
+    });
     W("MINB=4 DEFER predicated", 4, true, false)
     W("MINB=4 DEFER unconditional", 4, true, true)
     W("MINB=3 DEFER unconditional", 3, true, true)
