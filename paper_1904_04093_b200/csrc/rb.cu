@@ -6,10 +6,11 @@
 namespace bgabp {
 
 // red_black_grid(nx, ny) on a DIA matrix whose neighbour offsets are exactly the 5-point stencil
-// {-nx, -1, +1, +nx} with nx odd: the colour is then the parity of the node index.
+// {-nx, -1, +1, +nx} (nx >= 2; odd nx: the colour is the index parity, even nx: one node of each
+// colour per natural pair, rb_kernels.cuh)
 bool Engine::rb_applicable(const bgabp_schedule& s) const {
     if (s.kind != BGABP_SCHED_RED_BLACK_GRID || layout != BGABP_LAYOUT_DIA || S != 4) return false;
-    if (s.nx <= 0 || s.ny <= 0 || (s.nx & 1) == 0 || (long long)s.nx * s.ny != n) return false;
+    if (s.nx <= 1 || s.ny <= 0 || (long long)s.nx * s.ny != n) return false;
     return dia.off[0] == -s.nx && dia.off[1] == -1 && dia.off[2] == 1 && dia.off[3] == s.nx && dia.nneg == 2;
 }
 
@@ -30,7 +31,7 @@ void Engine::rb_build(int nx) {
     }
     double* dR = static_cast<double*>(dalloc(sizeof(double) * std::max(nR, 1)));
     double* dB = static_cast<double*>(dalloc(sizeof(double) * std::max(nB, 1)));
-    k_rb_split<<<nblk_host(n), 256, 0, st>>>(n, nR, dia.mask, dia.c, dia.rowv, dia.diag, mR, mB, cR, cB, rR, rB, dR,
+    k_rb_split<<<nblk_host(n), 256, 0, st>>>(n, nR, nx, dia.mask, dia.c, dia.rowv, dia.diag, mR, mB, cR, cB, rR, rB, dR,
                                              dB);
     ck(cudaGetLastError(), "rb split");
     rb.mask[0] = mR;
@@ -127,9 +128,9 @@ void Engine::rb_smooth_add(const double* r, int sweeps, double* x) {
 void Engine::rb_state(bool to_compact, double2* natural) {
     if (n == 0) return;
     if (to_compact)
-        k_rb_convert<true><<<nblk_host(n), 256, 0, st>>>(n, rb.nR, natural, d_rbmsg);
+        k_rb_convert<true><<<nblk_host(n), 256, 0, st>>>(n, rb.nR, rb.nx, natural, d_rbmsg);
     else
-        k_rb_convert<false><<<nblk_host(n), 256, 0, st>>>(n, rb.nR, natural, d_rbmsg);
+        k_rb_convert<false><<<nblk_host(n), 256, 0, st>>>(n, rb.nR, rb.nx, natural, d_rbmsg);
 }
 
 }  // namespace bgabp

@@ -1,11 +1,10 @@
-// Colour-compact red-black GaBP sweep for 5-point grids with an odd number of columns
-// (every multigrid level: 2^J - 1 points per axis), SURVEY.md §2.2 K2 specialised.
+// Colour-compact red-black GaBP sweep for 5-point grids, SURVEY.md §2.2 K2 specialised.
 //
-// With nx odd the red-black colour (ix+iy) mod 2 equals the parity of the natural index g, so
-// red node q is g = 2q and black node q is g = 2q+1, and every neighbour of a node sits at a
-// constant offset in the other colour's compact numbering:
-//     red q   -> black {q-(nx+1)/2, q-1, q, q+(nx-1)/2}     (natural offsets -nx, -1, +1, +nx)
-//     black q -> red   {q-(nx-1)/2, q, q+1, q+(nx+1)/2}
+// With nx odd (every multigrid level: 2^J - 1 points per axis) the red-black colour (ix+iy) mod 2
+// equals the parity of the natural index g, so red node q is g = 2q and black node q is g = 2q+1.
+// With nx even each natural pair (2q, 2q+1) holds one node of each colour, which one depending on
+// the row.  Either way node g has compact index g >> 1 in its colour, so a neighbour g + off
+// sits at (g + off) >> 1 in the other colour's numbering.
 // Messages and coefficients are stored per colour, slot-major ([4][n_colour]), so the red phase
 // and the black phase each read and write fully coalesced lines instead of every other element
 // of the natural-order arrays (the generic level kernel wastes half of every 32-byte sector).
@@ -26,11 +25,18 @@ struct RbP {
     const double* diag[2];    // [colour][n_c]
 };
 
-__device__ __forceinline__ int rb_other(int colour, int q, int s, int nx) {
-    // compact index in the other colour of neighbour slot s of node q of `colour`
-    const int h = (nx - 1) / 2;
-    if (colour == 0) return s == 0 ? q - h - 1 : s == 1 ? q - 1 : s == 2 ? q : q + h;
-    return s == 0 ? q - h : s == 1 ? q : s == 2 ? q + 1 : q + h + 1;
+// Even nx: natural pair (2q, 2q+1) lies in one row and holds one red and one black node, so the
+// compact index of natural node g is g >> 1 for both colours and for both parities of nx; which
+// element of the pair has colour C depends on the row when nx is even.
+__device__ __forceinline__ int rb_nat(const RbP& P, int q, int colour) {
+    return 2 * q + ((P.nx & 1) ? colour : ((colour + (2 * q) / P.nx) & 1));
+}
+__host__ __device__ __forceinline__ int rb_colour(int g, int nx) { return (nx & 1) ? (g & 1) : ((g + g / nx) & 1); }
+
+__device__ __forceinline__ int rb_other(int g, int s, int nx) {
+    // compact index (in the other colour) of neighbour slot s of natural node g
+    const int off = s == 0 ? -nx : s == 1 ? -1 : s == 2 ? 1 : nx;
+    return (g + off) >> 1;
 }
 
 // One colour phase of a red-black sweep.  COLD: first sweep of a cold start on the red phase
@@ -45,7 +51,7 @@ static __global__ void __launch_bounds__(256) k_rb_half(RbP P, const double* __r
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     double dmax = 0.0;
     if (q < nc) {
-        const int g = 2 * q + COLOUR;
+        const int g = rb_nat(P, q, COLOUR);
         const uint32_t mk = P.mask[COLOUR][q];
         const double dj = P.diag[COLOUR][q];
         double sig = 0.0, acc = b[g];
@@ -77,7 +83,7 @@ static __global__ void __launch_bounds__(256) k_rb_half(RbP P, const double* __r
             if (fabs(den) < kPivotFloor) atomicMin(&ctrl->opiv, pk | (unsigned)(g + off[s] + 1));
             const double nl = ddiv(-cc[s], den);
             const double nm = dmul(nl, dsub(acc, in[s].y));
-            double2* dst = other + (3 - s) * no + rb_other(COLOUR, q, s, P.nx);
+            double2* dst = other + (3 - s) * no + rb_other(g, s, P.nx);
             if (DELTA) {
                 const double2 o = *dst;
                 dmax = fmax(dmax, fmax(nan_skip_abs(dsub(nl, o.x)), nan_skip_abs(dsub(nm, o.y))));
@@ -89,13 +95,13 @@ static __global__ void __launch_bounds__(256) k_rb_half(RbP P, const double* __r
 }
 
 // colour-split copies of the DIA arrays (natural slots -nx, -1, +1, +nx)
-static __global__ void k_rb_split(int n, int nR, const uint32_t* __restrict__ mask, const double* __restrict__ c,
+static __global__ void k_rb_split(int n, int nR, int nx, const uint32_t* __restrict__ mask, const double* __restrict__ c,
                                   const double* __restrict__ rowv, const double* __restrict__ diag, uint32_t* mR,
                                   uint32_t* mB, double* cR, double* cB, double* rR, double* rB, double* dR, double* dB) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
     const int q = g >> 1, nB = n - nR;
-    const bool red = !(g & 1);
+    const bool red = rb_colour(g, nx) == 0;
     (red ? mR : mB)[q] = mask[g];
     (red ? dR : dB)[q] = diag[g];
     for (int s = 0; s < 4; ++s) {
@@ -122,7 +128,7 @@ static __global__ void __launch_bounds__(256) k_rb_lambda_half(RbP P, double* la
     const int nc = COLOUR == 0 ? P.nR : P.nB, no = COLOUR == 0 ? P.nB : P.nR;
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nc) return;
-    const int g = 2 * q + COLOUR;
+    const int g = rb_nat(P, q, COLOUR);
     const uint32_t mk = P.mask[COLOUR][q];
     double sig = 0.0, in[4], cc[4];
 #pragma unroll
@@ -146,7 +152,7 @@ static __global__ void __launch_bounds__(256) k_rb_lambda_half(RbP P, double* la
             const double den = dsub(sig, dmul(in[s], cc[s]));
             if (fabs(den) < kPivotFloor) atomicMin(&ctrl->opiv, pk | (unsigned)(g + off[s] + 1));
             nl = ddiv(-cc[s], den);
-            lam_other[(3 - s) * no + rb_other(COLOUR, q, s, P.nx)] = nl;
+            lam_other[(3 - s) * no + rb_other(g, s, P.nx)] = nl;
         }
         lam_rec[s * nc + q] = nl;
     }
@@ -163,7 +169,7 @@ static __global__ void __launch_bounds__(256) k_rb_mean_half(RbP P, const double
     const int nc = COLOUR == 0 ? P.nR : P.nB, no = COLOUR == 0 ? P.nB : P.nR;
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nc) return;
-    const int g = 2 * q + COLOUR;
+    const int g = rb_nat(P, q, COLOUR);
     const uint32_t mk = P.mask[COLOUR][q];
     double acc = r[g], in[4];
 #pragma unroll
@@ -175,16 +181,16 @@ static __global__ void __launch_bounds__(256) k_rb_mean_half(RbP P, const double
 #pragma unroll
     for (int s = 0; s < 4; ++s)
         if (mk & (1u << (16 + s)))
-            m_other[(3 - s) * no + rb_other(COLOUR, q, s, P.nx)] = dmul(__ldg(lam_rec + s * nc + q), dsub(acc, in[s]));
+            m_other[(3 - s) * no + rb_other(g, s, P.nx)] = dmul(__ldg(lam_rec + s * nc + q), dsub(acc, in[s]));
 }
 
 // message state natural DIA [4][n] <-> colour-compact ([4][nR] reds, then [4][nB] blacks)
 template <bool TO_COMPACT>
-static __global__ void k_rb_convert(int n, int nR, double2* nat, double2* cmp) {
+static __global__ void k_rb_convert(int n, int nR, int nx, double2* nat, double2* cmp) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
     const int q = g >> 1, nB = n - nR;
-    const bool red = !(g & 1);
+    const bool red = rb_colour(g, nx) == 0;
     double2* base = red ? cmp : cmp + 4 * (size_t)nR;
     const int nc = red ? nR : nB;
     for (int s = 0; s < 4; ++s) {
