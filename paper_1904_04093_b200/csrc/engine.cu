@@ -8,6 +8,10 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <omp.h>
+
+#include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -65,6 +69,15 @@ Engine::~Engine() {
 // ---------------------------------------------------------------------------------------------
 void Engine::build(int n_, const int* ro_, const int* ci_, const double* v_, int want_layout,
                    cudaStream_t shared_stream) {
+    static const bool timing = getenv("BGABP_TIMING") != nullptr;
+    auto t_last = std::chrono::steady_clock::now();
+    auto phase = [&](const char* what) {
+        if (!timing) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[build] %-28s %8.1f ms\n", what,
+                     std::chrono::duration<double, std::milli>(now - t_last).count());
+        t_last = now;
+    };
     if (n_ < 0) throw InvalidArg("gabp: negative dimension");
     n = n_;
     ro.assign(ro_, ro_ + n + 1);
@@ -72,18 +85,39 @@ void Engine::build(int n_, const int* ro_, const int* ci_, const double* v_, int
     for (int i = 0; i < n; ++i)
         if (ro[i + 1] < ro[i]) throw InvalidArg("gabp: row_offsets not monotone");
     nnz = ro[n];
-    ci.assign(ci_, ci_ + nnz);
-    val.assign(v_, v_ + nnz);
+    ci.resize(nnz);
+    val.resize(nnz);
+#pragma omp parallel for schedule(static)
+    for (long long c0 = 0; c0 < nnz; c0 += (1 << 20)) {  // parallel copies of the CSR arrays
+        const long long c1 = std::min<long long>(nnz, c0 + (1 << 20));
+        std::memcpy(ci.data() + c0, ci_ + c0, sizeof(int) * (size_t)(c1 - c0));
+        std::memcpy(val.data() + c0, v_ + c0, sizeof(double) * (size_t)(c1 - c0));
+    }
     std::vector<int> diag_pos(n, -1);
-    for (int i = 0; i < n; ++i)
+    int bad = 0;  // first failure kind in row order: 1 range, 2 order, 3 zero diagonal
+    long long bad_row = n;
+#pragma omp parallel for schedule(static) reduction(min : bad_row)
+    for (int i = 0; i < n; ++i) {
+        for (int p = ro[i]; p < ro[i + 1]; ++p) {
+            if (ci[p] < 0 || ci[p] >= n || (p > ro[i] && ci[p] <= ci[p - 1])) {
+                bad_row = std::min<long long>(bad_row, i);
+                break;
+            }
+            if (ci[p] == i) diag_pos[i] = p;
+        }
+    }
+    for (int i = 0; i < n && !bad; ++i) {  // the reference's messages, first offending row first
+        if (i < bad_row && diag_pos[i] >= 0) continue;
         for (int p = ro[i]; p < ro[i + 1]; ++p) {
             if (ci[p] < 0 || ci[p] >= n) throw InvalidArg("gabp: column index out of range");
             if (p > ro[i] && ci[p] <= ci[p - 1]) throw InvalidArg("gabp: CSR is not canonical (columns must increase)");
-            if (ci[p] == i) diag_pos[i] = p;
         }
+        if (i >= bad_row) break;
+    }
     for (int i = 0; i < n; ++i)  // gabp.cpp:29-33
         if (diag_pos[i] < 0) throw InvalidArg("gabp: matrix has a structurally zero diagonal entry");
     num_edges = nnz - n;
+    phase("copy + validate");
 
     // transpose partner of every entry (sparse.cpp:70-74)
     tpos.assign(nnz, -1);
@@ -101,47 +135,79 @@ void Engine::build(int n_, const int* ro_, const int* ci_, const double* v_, int
             if (tpos[p] < 0 || std::memcmp(&val[tpos[p]], &val[p], sizeof(double)) != 0) sym = 0;
         }
     symmetric = sym != 0;
+    phase("transpose positions");
 
-    // union neighbour lists (row j and column j, sorted): the dependency graph of the schedules
+    // union neighbour lists (row j and column j, sorted): the dependency graph of the schedules.
+    // Row part in parallel; the entries whose transpose is absent (one-way couplings) add the
+    // reverse neighbour, counted and placed with atomics, then each list is sorted.
     std::vector<int> ucount(n + 1, 0);
-    for (int i = 0; i < n; ++i)
+    long long oneway = 0;
+#pragma omp parallel for schedule(static) reduction(+ : oneway)
+    for (int i = 0; i < n; ++i) {
+        int c = 0;
         for (int p = ro[i]; p < ro[i + 1]; ++p) {
-            const int j = ci[p];
-            if (j == i) continue;
-            ucount[i + 1]++;                 // i has neighbour j (in-edge j->i)
-            if (tpos[p] < 0) ucount[j + 1]++;  // j has neighbour i only through the out-edge j->i
+            if (ci[p] == i) continue;
+            ++c;
+            if (tpos[p] < 0) ++oneway;
         }
+        ucount[i + 1] = c;
+    }
+    if (oneway) {
+        for (int i = 0; i < n; ++i)
+            for (int p = ro[i]; p < ro[i + 1]; ++p)
+                if (ci[p] != i && tpos[p] < 0) ucount[ci[p] + 1]++;  // j has neighbour i only via j->i
+    }
     uptr.assign(n + 1, 0);
     for (int i = 0; i < n; ++i) uptr[i + 1] = uptr[i] + ucount[i + 1];
     const long long U = uptr[n];
     unbr.assign(U, 0);
     std::vector<int> fill(uptr.begin(), uptr.end() - 1);
-    for (int i = 0; i < n; ++i)
-        for (int p = ro[i]; p < ro[i + 1]; ++p) {
-            const int j = ci[p];
-            if (j == i) continue;
-            unbr[fill[i]++] = j;
-            if (tpos[p] < 0) unbr[fill[j]++] = i;
-        }
 #pragma omp parallel for schedule(static)
-    for (int i = 0; i < n; ++i) std::sort(unbr.begin() + uptr[i], unbr.begin() + uptr[i + 1]);
+    for (int i = 0; i < n; ++i) {
+        int f = fill[i];
+        for (int p = ro[i]; p < ro[i + 1]; ++p)
+            if (ci[p] != i) unbr[f++] = ci[p];
+        fill[i] = f;
+    }
+    if (oneway) {
+        for (int i = 0; i < n; ++i)
+            for (int p = ro[i]; p < ro[i + 1]; ++p)
+                if (ci[p] != i && tpos[p] < 0) unbr[fill[ci[p]]++] = i;
+#pragma omp parallel for schedule(static)
+        for (int i = 0; i < n; ++i) std::sort(unbr.begin() + uptr[i], unbr.begin() + uptr[i + 1]);
+    }
+    phase("union neighbour lists");
 
     // offsets of the union structure decide the layout
     std::vector<int> offs;
     {
         // distinct offsets, stopping at kMaxDia + 1 (a linear scan over <= 9 values per entry; a
         // map insertion per entry took seconds on the 84M-entry config-5 level)
-        for (int i = 0; i < n && (int)offs.size() <= kMaxDia; ++i)
-            for (long long s = uptr[i]; s < uptr[i + 1]; ++s) {
-                const int d = unbr[s] - i;
-                if (std::find(offs.begin(), offs.end(), d) == offs.end()) offs.push_back(d);
+        const int T = std::max(1, omp_get_max_threads());
+        std::vector<std::vector<int>> part(T);
+#pragma omp parallel num_threads(T)
+        {
+            std::vector<int>& mine = part[omp_get_thread_num()];
+#pragma omp for schedule(static)
+            for (int i = 0; i < n; ++i) {
+                if ((int)mine.size() > kMaxDia) continue;
+                for (long long s = uptr[i]; s < uptr[i + 1]; ++s) {
+                    const int d = unbr[s] - i;
+                    if (std::find(mine.begin(), mine.end(), d) == mine.end()) mine.push_back(d);
+                }
             }
+        }
+        for (const auto& m : part)
+            for (int d : m)
+                if ((int)offs.size() <= kMaxDia && std::find(offs.begin(), offs.end(), d) == offs.end())
+                    offs.push_back(d);
         std::sort(offs.begin(), offs.end());
     }
     const bool dia_ok = !offs.empty() && (int)offs.size() <= kMaxDia && offs.size() % 2 == 0;
     if (want_layout == BGABP_LAYOUT_DIA && !dia_ok)
         throw InvalidArg("gabp: DIA layout needs 1..8 symmetric neighbour offsets");
     layout = (want_layout == BGABP_LAYOUT_CSR || !dia_ok) ? BGABP_LAYOUT_CSR : BGABP_LAYOUT_DIA;
+    phase("offsets");
 
     if (shared_stream) {
         st = shared_stream;
@@ -220,32 +286,40 @@ void Engine::build(int n_, const int* ro_, const int* ci_, const double* v_, int
         if (symmetric && n > 0) {
             bool unif = true;
             for (int s2 = 0; s2 < S && unif; ++s2) {
-                bool have = false;
-                unsigned long long ref = 0ull;
-                for (int i = 0; i < n && unif; ++i) {
+                int first = -1;  // first node with this out-edge: the reference value
+                for (int i = 0; i < n; ++i)
+                    if (mask[i] & (1u << (16 + s2))) {
+                        first = i;
+                        break;
+                    }
+                dia.cu[s2] = first >= 0 ? c[(size_t)s2 * n + first] : 0.0;
+                if (first < 0) continue;
+                unsigned long long ref;
+                std::memcpy(&ref, &c[(size_t)s2 * n + first], sizeof ref);
+                int same = 1;
+#pragma omp parallel for schedule(static) reduction(min : same)
+                for (int i = first; i < n; ++i) {
                     if (!(mask[i] & (1u << (16 + s2)))) continue;
                     unsigned long long v;
                     std::memcpy(&v, &c[(size_t)s2 * n + i], sizeof v);
-                    if (!have) {
-                        ref = v;
-                        have = true;
-                        dia.cu[s2] = c[(size_t)s2 * n + i];
-                    } else if (v != ref) {
-                        unif = false;
-                    }
+                    if (v != ref) same = 0;
                 }
-                if (!have) dia.cu[s2] = 0.0;
+                unif = same != 0;
             }
             unsigned long long d0;
             std::memcpy(&d0, &diag[0], sizeof d0);
-            for (int i = 1; i < n && unif; ++i) {
+            int same_d = 1;
+#pragma omp parallel for schedule(static) reduction(min : same_d)
+            for (int i = 1; i < n; ++i) {
                 unsigned long long v;
                 std::memcpy(&v, &diag[i], sizeof v);
-                unif = v == d0;
+                if (v != d0) same_d = 0;
             }
+            unif = unif && same_d;
             dia.uniform = unif ? 1 : 0;
             dia.du = diag[0];
         }
+        phase("DIA arrays");
         dia.mask = upload(mask);
         dia.c = upload(c);
         dia.rowv = symmetric ? dia.c : upload(rowv);
@@ -288,7 +362,8 @@ void Engine::build(int n_, const int* ro_, const int* ci_, const double* v_, int
         csr.ci = upload(ci);
         csr.val = upload(val);
     }
-    d_csr2slot = upload(csr2slot);
+    d_csr2slot = nullptr;  // uploaded on first use (state gather / scatter): parity paths only
+    phase("uploads");
     for (int k = 0; k < 2; ++k) {
         d_msg[k] = static_cast<double2*>(dalloc(sizeof(double2) * (size_t)std::max<long long>(nslots, 1)));
         ck(cudaMemsetAsync(d_msg[k], 0, sizeof(double2) * (size_t)std::max<long long>(nslots, 1), st), "memset");
@@ -1175,6 +1250,7 @@ int bgabp_set_state(bgabp_engine* h, const double* lam, const double* m) {
         ck(cudaMemcpyAsync(dl, lam, sizeof(double) * E.nnz, cudaMemcpyHostToDevice, E.st), "H2D");
         ck(cudaMemcpyAsync(dm, m, sizeof(double) * E.nnz, cudaMemcpyHostToDevice, E.st), "H2D");
         ck(cudaMemsetAsync(E.d_msg[E.cur], 0, sizeof(double2) * (size_t)E.nslots, E.st), "memset");
+        E.ensure_csr2slot();
         k_state_scatter<<<nblk(E.nnz), 256, 0, E.st>>>(E.d_msg[E.cur], E.d_csr2slot, E.nnz, dl, dm);
         ck(cudaFreeAsync(dl, E.st), "free");
         ck(cudaFreeAsync(dm, E.st), "free");
@@ -1190,6 +1266,7 @@ int bgabp_get_state(bgabp_engine* h, double* lam, double* m) {
         double *dl = nullptr, *dm = nullptr;
         ck(cudaMallocAsync((void**)&dl, sizeof(double) * E.nnz, E.st), "malloc");
         ck(cudaMallocAsync((void**)&dm, sizeof(double) * E.nnz, E.st), "malloc");
+        E.ensure_csr2slot();
         k_state_gather<<<nblk(E.nnz), 256, 0, E.st>>>(E.d_msg[E.cur], E.d_csr2slot, E.nnz, dl, dm);
         ck(cudaMemcpyAsync(lam, dl, sizeof(double) * E.nnz, cudaMemcpyDeviceToHost, E.st), "D2H");
         ck(cudaMemcpyAsync(m, dm, sizeof(double) * E.nnz, cudaMemcpyDeviceToHost, E.st), "D2H");
@@ -1341,6 +1418,7 @@ int bgabp_precompute_lambda(bgabp_engine* h, const bgabp_schedule* s, double tol
         if (lam_out && E.nnz > 0) {
             double* dl = nullptr;
             ck(cudaMallocAsync((void**)&dl, sizeof(double) * E.nnz, E.st), "malloc");
+            E.ensure_csr2slot();
             k_lambda_gather<<<nblk(E.nnz), 256, 0, E.st>>>(E.d_lam, E.d_csr2slot, E.nnz, dl);
             ck(cudaMemcpyAsync(lam_out, dl, sizeof(double) * E.nnz, cudaMemcpyDeviceToHost, E.st), "D2H");
             ck(cudaFreeAsync(dl, E.st), "free");
@@ -1361,6 +1439,7 @@ int bgabp_set_frozen(bgabp_engine* h, const double* lam, const double* sigma) {
             double* dl = nullptr;
             ck(cudaMallocAsync((void**)&dl, sizeof(double) * E.nnz, E.st), "malloc");
             ck(cudaMemcpyAsync(dl, lam, sizeof(double) * E.nnz, cudaMemcpyHostToDevice, E.st), "H2D");
+            E.ensure_csr2slot();
             k_lambda_scatter<<<nblk(E.nnz), 256, 0, E.st>>>(E.d_lam, E.d_csr2slot, E.nnz, dl);
             ck(cudaFreeAsync(dl, E.st), "free");
         }

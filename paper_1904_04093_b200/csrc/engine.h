@@ -63,6 +63,9 @@ struct Engine {
     Ctrl* d_ctrl = nullptr;
     Ctrl* h_ctrl = nullptr;
     long long* d_csr2slot = nullptr;
+    void ensure_csr2slot() {
+        if (!d_csr2slot && nnz > 0) d_csr2slot = upload(csr2slot);
+    }
     double2* d_msg[2] = {nullptr, nullptr};
     int cur = 0;
     double *d_b = nullptr, *d_x = nullptr, *d_r = nullptr, *d_e = nullptr, *d_aux = nullptr;
