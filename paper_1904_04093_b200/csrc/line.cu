@@ -150,12 +150,63 @@ void LineEngine::clear_fail() {
 void LineEngine::sweep(const double* b, int mode, double* x, const int* done) {
     if (n == 0) return;
     const int c = cur, o = mode == 1 ? cur ^ 1 : cur;  // flood writes the other buffer
-    k_line_phase<true><<<lblk(ny, 64), 64, 0, st>>>(P, b, lc[c], mc[c], lr[o], mr[o], nullptr, d_fd, d_fy, d_fail,
+    k_line_phase<true><<<lblk(ny, 32), 32, 0, st>>>(P, b, lc[c], mc[c], lr[o], mr[o], nullptr, d_fd, d_fy, d_fail,
                                                     done);
-    k_line_phase<false><<<lblk(nx, 64), 64, 0, st>>>(P, b, mode == 1 ? lr[c] : lr[o], mode == 1 ? mr[c] : mr[o],
+    k_line_phase<false><<<lblk(nx, 32), 32, 0, st>>>(P, b, mode == 1 ? lr[c] : lr[o], mode == 1 ? mr[c] : mr[o],
                                                      lc[o], mc[o], x, d_fd, d_fy, d_fail, done);
     cur = o;
     ck(cudaGetLastError(), "line sweep");
+}
+
+bool LineEngine::record(int sweeps) {
+    if (rec_failed) return false;
+    if (rec_sweeps >= sweeps || n == 0) return true;
+    const size_t vb = sizeof(double) * std::max(n, 1);
+    auto one = [&]() {
+        LineRec r;
+        r.f = static_cast<double*>(dalloc(vb));
+        r.rd = static_cast<double*>(dalloc(vb));
+        r.W = static_cast<double*>(dalloc(vb));
+        return r;
+    };
+    while ((int)rec_rows.size() < sweeps) {
+        rec_rows.push_back(one());
+        rec_cols.push_back(one());
+    }
+    ck(cudaMemsetAsync(d_b, 0, vb, st), "memset b");  // the factors do not depend on b
+    reset_state();
+    clear_fail();
+    for (int s = 0; s < sweeps; ++s) {  // sequential mode: rows then columns, in place
+        k_line_phase<true, true><<<lblk(ny, 32), 32, 0, st>>>(P, d_b, lc[0], mc[0], lr[0], mr[0], nullptr, d_fd, d_fy,
+                                                             d_fail, nullptr, rec_rows[s]);
+        k_line_phase<false, true><<<lblk(nx, 32), 32, 0, st>>>(P, d_b, lr[0], mr[0], lc[0], mc[0], nullptr, d_fd,
+                                                              d_fy, d_fail, nullptr, rec_cols[s]);
+    }
+    ck(cudaGetLastError(), "line record");
+    if (read_fail() != kNone) {
+        rec_failed = true;
+        clear_fail();
+        return false;
+    }
+    rec_sweeps = sweeps;
+    return true;
+}
+
+void LineEngine::smooth_add(const double* r, int sweeps, double* x) {
+    if (n == 0 || sweeps <= 0) return;
+    ck(cudaMemsetAsync(mc[0], 0, sizeof(double) * n, st), "memset");  // cold start
+    for (int s = 0; s < sweeps; ++s) {
+        const bool last = s + 1 == sweeps;
+        k_line_mean_phase<true, false><<<lblk(ny, 32), 32, 0, st>>>(P, r, mc[0], mr[0], nullptr, d_fy, rec_rows[s].f,
+                                                                   rec_rows[s].rd, rec_rows[s].W);
+        if (last)
+            k_line_mean_phase<false, true><<<lblk(nx, 32), 32, 0, st>>>(P, r, mr[0], mc[0], x, d_fy, rec_cols[s].f,
+                                                                       rec_cols[s].rd, rec_cols[s].W);
+        else
+            k_line_mean_phase<false, false><<<lblk(nx, 32), 32, 0, st>>>(P, r, mr[0], mc[0], nullptr, d_fy,
+                                                                        rec_cols[s].f, rec_cols[s].rd, rec_cols[s].W);
+    }
+    ck(cudaGetLastError(), "line smooth");
 }
 
 unsigned long long LineEngine::read_fail() {

@@ -43,6 +43,14 @@ struct LineEngine {
     double sweep_flops() const;
     void set_state(const double* lam, const double* m);  // host, reference edge order
     void get_state(double* lam, double* m);
+    // multigrid smoothing fast path: the factors of `sweeps` cold sweeps recorded once (false if
+    // the recursion breaks down within them: the full sweep then reports it), then mean-only
+    // sweeps on r with x += e folded into the last column phase
+    std::vector<LineRec> rec_rows, rec_cols;
+    int rec_sweeps = 0;
+    bool rec_failed = false;
+    bool record(int sweeps);
+    void smooth_add(const double* r, int sweeps, double* x);
 };
 
 }  // namespace bgabp

@@ -36,13 +36,19 @@ struct LineP {
 
 // failure key: (region << 32) | 0 for a singular local system, | (1 + child position) for a
 // singular child block; atomicMin gives the reference's first failure in region order
-template <bool ROW>
-static __global__ void __launch_bounds__(64) k_line_phase(LineP P, const double* __restrict__ b,
+// REC: also record, per node, the right-hand-side independent factors of this phase -- the forward
+// multiplier f_k, 1/d_k and the child precision W_k -- for the mean-only phases below
+struct LineRec {
+    double *f, *rd, *W;  // [n] each, natural node order
+};
+
+template <bool ROW, bool REC = false>
+static __global__ void __launch_bounds__(32) k_line_phase(LineP P, const double* __restrict__ b,
                                                          const double* __restrict__ lam_o,
                                                          const double* __restrict__ m_o, double* __restrict__ lam_n,
                                                          double* __restrict__ m_n, double* __restrict__ x,
                                                          double* __restrict__ fd, double* __restrict__ fy,
-                                                         unsigned long long* fail, const int* done) {
+                                                         unsigned long long* fail, const int* done, LineRec rec = {}) {
     if (done && *(volatile const int*)done) return;
     // a region already failed (rows of this sweep, or an earlier sweep of a smoothing call): the
     // reference stopped there
@@ -81,12 +87,15 @@ static __global__ void __launch_bounds__(64) k_line_phase(LineP P, const double*
             if (k == 0) {
                 d = av[q];
                 y = bv[q];
+                if (REC) rec.f[v] = 0.0;
             } else {
                 const double f = ddiv(lv[q], dprev);
                 d = dsub(av[q], dmul(f, uprev));
                 y = dsub(bv[q], dmul(f, yprev));
+                if (REC) rec.f[v] = f;
             }
             if (d == 0.0 || !isfinite(d)) singular = true;
+            if (REC) rec.rd[v] = ddiv(1.0, d);
             fd[v] = d;
             fy[v] = y;
             dprev = d;
@@ -131,6 +140,7 @@ static __global__ void __launch_bounds__(64) k_line_phase(LineP P, const double*
             }
             const double W = dsub(dadd(dd[q], g), a);
             if (W == 0.0 || !isfinite(W)) bad = (region << 32) | (unsigned long long)(1 + k);
+            if (REC) rec.W[v] = W;
             lam_n[v] = dsub(dsub(W, dv[q]), lo_v[q]);
             m_n[v] = dsub(dsub(dmul(W, xk), bb[q]), mo_v[q]);
             if (x) x[v] = xk;
@@ -140,6 +150,70 @@ static __global__ void __launch_bounds__(64) k_line_phase(LineP P, const double*
         }
     }
     if (bad != kNone) atomicMin(fail, bad);
+}
+
+// Mean-only phase with the recorded factors of a cold start (multigrid smoothing: every call
+// restarts the block messages at zero, multigrid.cpp:195, and the precision recursion never reads
+// the means, so f, 1/d and W of sweep s depend on A alone).  The forward and backward recurrences
+// are then one multiply-add each: y_k = b0_k - f_k y_{k-1}, x_k = (y_k - u_k x_{k+1}) / d_k (as a
+// product with the recorded reciprocal, so the smoother's x agrees with the full line solve to
+// rounding), m_k = W_k x_k - b_k - m_other_k.  ADDX: the call's last column phase adds x into the
+// iterate (Hierarchy::smooth's x += e) instead of writing e.
+template <bool ROW, bool ADDX>
+static __global__ void __launch_bounds__(32) k_line_mean_phase(LineP P, const double* __restrict__ b,
+                                                              const double* __restrict__ m_o,
+                                                              double* __restrict__ m_n, double* __restrict__ x,
+                                                              double* __restrict__ fy, const double* __restrict__ f,
+                                                              const double* __restrict__ rd,
+                                                              const double* __restrict__ W) {
+    const int line = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nlines = ROW ? P.ny : P.nx, N = ROW ? P.nx : P.ny;
+    if (line >= nlines) return;
+    const int stride = ROW ? 1 : P.nx;
+    const int base = ROW ? line * P.nx : line;
+    const double* up = ROW ? P.e : P.nn;
+    constexpr int kLC = 16;
+    double yprev = 0.0;
+    for (int k0 = 0; k0 < N; k0 += kLC) {
+        double bv[kLC], fv[kLC];
+#pragma unroll
+        for (int q = 0; q < kLC; ++q) {
+            const int v = base + min(k0 + q, N - 1) * stride;
+            bv[q] = dadd(__ldg(b + v), m_o[v]);
+            fv[q] = __ldg(f + v);
+        }
+#pragma unroll
+        for (int q = 0; q < kLC; ++q) {
+            if (k0 + q >= N) break;
+            yprev = dsub(bv[q], dmul(fv[q], yprev));
+            fy[base + (k0 + q) * stride] = yprev;
+        }
+    }
+    double xnext = 0.0;
+    for (int k1 = N - 1; k1 >= 0; k1 -= kLC) {
+        double yy[kLC], uu[kLC], rr[kLC], ww[kLC], bb[kLC], mo[kLC], xo[ADDX ? kLC : 1];
+#pragma unroll
+        for (int q = 0; q < kLC; ++q) {
+            const int v = base + max(k1 - q, 0) * stride;
+            yy[q] = fy[v];
+            uu[q] = __ldg(up + v);
+            rr[q] = __ldg(rd + v);
+            ww[q] = __ldg(W + v);
+            bb[q] = __ldg(b + v);
+            mo[q] = m_o[v];
+            if (ADDX) xo[ADDX ? q : 0] = x[v];  // the iterate, read with the chunk (not per step)
+        }
+#pragma unroll
+        for (int q = 0; q < kLC; ++q) {
+            const int k = k1 - q;
+            if (k < 0) break;
+            const int v = base + k * stride;
+            const double xk = dmul(k == N - 1 ? yy[q] : dsub(yy[q], dmul(uu[q], xnext)), rr[q]);
+            m_n[v] = dsub(dsub(dmul(ww[q], xk), bb[q]), mo[q]);
+            if (x) x[v] = ADDX ? dadd(xo[ADDX ? q : 0], xk) : xk;
+            xnext = xk;
+        }
+    }
 }
 
 // r = b - A x in CSR column order (sparse.cpp:104-115) and its NaN-skipping inf-norm

@@ -126,6 +126,10 @@ struct bgmg {
         if (smoother == GabpLine) {  // multigrid.cpp:189-204: fresh block messages, sequential sweeps
             LineEngine& G = *levels[k].line;
             L.launch_residual(b, x, L.d_r, nullptr, MODE_PLAIN);
+            if (G.record(sweeps)) {  // recorded factors: mean-only sweeps, x += e in the last phase
+                G.smooth_add(L.d_r, sweeps, x);
+                return;
+            }
             G.reset_state();
             ck(cudaMemsetAsync(G.d_fail, 0xff, sizeof(unsigned long long), st), "memset");
             for (int s = 0; s < sweeps; ++s) G.sweep(L.d_r, 0, L.d_e);
