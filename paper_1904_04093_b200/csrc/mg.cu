@@ -101,14 +101,14 @@ struct bgmg {
     int nl() const { return (int)levels.size(); }
 
     // Hierarchy::smooth (multigrid.cpp:163-208)
-    void smooth(int k, const double* b, double* x, int sweeps, bool frozen) {
+    void smooth(int k, const double* b, double* x, int sweeps, bool frozen, bool have_r = false) {
         if (sweeps <= 0) return;
         Engine& L = E(k);
         if (L.n == 0) return;
         const unsigned g = nblk_host(L.n);
         ++seq;
         if (is_gabp(smoother)) {
-            L.launch_residual(b, x, L.d_r, nullptr, MODE_PLAIN);
+            if (!have_r) L.launch_residual(b, x, L.d_r, nullptr, MODE_PLAIN);
             if (!(frozen && levels[k].frozen_ok) && L.rb_applicable(levels[k].sched) && L.rb_ready &&
                 L.rb_pre_sweeps >= sweeps) {
                 L.rb_smooth_add(L.d_r, sweeps, x);  // recorded lambda/sigma, x += e fused
@@ -125,7 +125,7 @@ struct bgmg {
         }
         if (smoother == GabpLine) {  // multigrid.cpp:189-204: fresh block messages, sequential sweeps
             LineEngine& G = *levels[k].line;
-            L.launch_residual(b, x, L.d_r, nullptr, MODE_PLAIN);
+            if (!have_r) L.launch_residual(b, x, L.d_r, nullptr, MODE_PLAIN);
             if (G.record(sweeps)) {  // recorded factors: mean-only sweeps, x += e in the last phase
                 G.smooth_add(L.d_r, sweeps, x);
                 return;
@@ -158,7 +158,10 @@ struct bgmg {
             if (L.n > 0) k_gemv_rows<<<nblk_host((long long)L.n * 32), 256, 0, st>>>(d_inv, b, x, L.n);
             return;
         }
-        smooth(k, b, x, spec.pre, spec.frozen != 0);
+        // the stop test of the previous cycle left r = b - A x of this very x in d_r
+        const bool reuse = k == 0 && fine_r_b == b && fine_r_x == x;
+        if (k == 0) fine_r_b = fine_r_x = nullptr;
+        smooth(k, b, x, spec.pre, spec.frozen != 0, reuse);
         MgLevel& C = levels[k + 1];
         L.launch_residual(b, x, L.d_r, nullptr, MODE_PLAIN);
         k_restrict<<<nblk_host(C.E->n), 256, 0, st>>>(L.d_r, levels[k].nx, C.d_b);
@@ -235,11 +238,17 @@ struct bgmg {
         ck(cudaGetLastError(), "v-cycle");
     }
 
+    // the stop test's residual r = b - A x also serves the next cycle's first smoothing call (same
+    // x, same kernel): fine_r_for records which (b, x) it belongs to
+    const double *fine_r_b = nullptr, *fine_r_x = nullptr;
+
     double residual_inf(const double* b, const double* x) {
         Engine& L = E(0);
         if (L.n == 0) return 0.0;
         ck(cudaMemsetAsync(&L.d_ctrl->red[2], 0, sizeof(unsigned long long), st), "memset");
-        L.launch_residual(b, x, nullptr, &L.d_ctrl->red[2], MODE_PLAIN);
+        L.launch_residual(b, x, L.d_r, &L.d_ctrl->red[2], MODE_PLAIN);
+        fine_r_b = b;
+        fine_r_x = x;
         unsigned long long r;
         ck(cudaMemcpyAsync(&r, &L.d_ctrl->red[2], sizeof(r), cudaMemcpyDeviceToHost, st), "D2H");
         ck(cudaStreamSynchronize(st), "sync");
@@ -260,6 +269,11 @@ struct bgmg {
     // mg_solve (multigrid.cpp:276-318) on device vectors; history on the host
     void solve_dev(const bgmg_cycle& spec, const double* b, double* x, const bgmg_options& o, bgabp_report& rep,
                    std::vector<double>& hist, std::string& detail) {
+        struct ClearR {  // the saved residual is only valid inside this loop
+            bgmg* h;
+            ~ClearR() { h->fine_r_b = h->fine_r_x = nullptr; }
+        } clear_r{this};
+        fine_r_b = fine_r_x = nullptr;
         const int n = E(0).n;
         ck(cudaMemsetAsync(x, 0, sizeof(double) * std::max(n, 1), st), "memset");
         const double r0 = inf_norm_dev(b, n);
@@ -442,6 +456,7 @@ int bgmg_vcycle(bgmg* h, const bgmg_cycle* spec, const double* b, double* x, cha
         h->ensure_fine_scratch();
         ck(cudaMemcpyAsync(h->d_fine_b, b, sizeof(double) * n, cudaMemcpyHostToDevice, h->st), "H2D");
         ck(cudaMemcpyAsync(h->d_fine_x, x, sizeof(double) * n, cudaMemcpyHostToDevice, h->st), "H2D");
+        h->fine_r_b = h->fine_r_x = nullptr;
         h->v_cycle_dev(*spec, h->d_fine_b, h->d_fine_x);
         ck(cudaMemcpyAsync(x, h->d_fine_x, sizeof(double) * n, cudaMemcpyDeviceToHost, h->st), "D2H");
         ck(cudaStreamSynchronize(h->st), "sync");
