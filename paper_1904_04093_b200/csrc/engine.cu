@@ -542,7 +542,11 @@ void Engine::launch_residual(const double* b, const double* x, double* r, unsign
     if (n == 0) return;
     const unsigned g = nblk(n);
     if (layout == BGABP_LAYOUT_DIA) {
-        DIA_SWITCH(S, k_residual_dia<SS><<<g, 256, 0, st>>>(dia, b, x, r, rmax, d_ctrl, mode));
+        if (symmetric) {
+            DIA_SWITCH(S, k_residual_dia<SS, true><<<g, 256, 0, st>>>(dia, b, x, r, rmax, d_ctrl, mode));
+        } else {
+            DIA_SWITCH(S, k_residual_dia<SS><<<g, 256, 0, st>>>(dia, b, x, r, rmax, d_ctrl, mode));
+        }
     } else {
         k_residual_csr<<<g, 256, 0, st>>>(csr, b, x, r, rmax, d_ctrl, mode);
     }
