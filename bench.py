@@ -125,8 +125,9 @@ def max_over_ranks(v, world, device="cuda"):
 # ------------------------------------------------------------------------------------------------
 # CPU baseline: the reference's own GabpEngine::solve on the host cores
 # ------------------------------------------------------------------------------------------------
-def cpu_reference_rate(P, iters):
-    """Time `iters` iterations of the reference's solve loop (sweep + residual) on config 2."""
+def cpu_reference_rate(P, iters, warmup=1):
+    """Time `iters` iterations of the reference's solve loop (sweep + residual) on config 2, after
+    `warmup` untimed iterations."""
     from oracle.oracle import Oracle, Csr, Schedule as OSched
     o = Oracle.reference()
     kind = "reference"
@@ -136,14 +137,15 @@ def cpu_reference_rate(P, iters):
     eng = o.engine(A)
     E = eng.num_edges
     tol = 1e-8 * float(np.abs(P.b).max())
-    eng.solve(P.b, OSched.parallel_flood(), tol=tol, max_iter=1)  # warm-up (page-in, allocator)
+    eng.solve(P.b, OSched.parallel_flood(), tol=tol, max_iter=max(1, warmup))  # warm-up (page-in, allocator)
     t0 = time.perf_counter()
     rep = eng.solve(P.b, OSched.parallel_flood(), tol=tol, max_iter=iters)
     dt = time.perf_counter() - t0
     assert rep.iterations == iters
     return {"value": E * iters / dt, "unit": UNIT, "cores": 1, "kind": kind,
             "sample": f"{iters} solve iterations (flood sweep + residual, gabp.cpp:187-218) of the full {P.A.n}-unknown "
-                      f"system, 1 thread (the reference is single-threaded), best of 1 after 1 warm-up iteration",
+                      f"system, 1 thread (the reference is single-threaded), best of 1 after {max(1, warmup)} warm-up "
+                      f"iteration(s)",
             "seconds": dt, "cpu": _cpu_name(), "nproc": os.cpu_count()}
 
 
@@ -163,9 +165,10 @@ def run_reference_arm(args, world, rank):
     import paper_1904_04093_b200 as g  # input generation only (host code, no device work)
     P = g.config_problem(args.config)
     iters = max(1, min(args.steps, args.ref_iters if args.config != 4 else min(args.ref_iters, 4)))
-    cb = cpu_reference_rate(P, iters)
+    cb = cpu_reference_rate(P, iters, args.warmup)
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
-            "steps": iters, "warmup": 1, "ms_per_step": cb["seconds"] * 1e3 / iters, "higher_is_better": True,
+            "steps": iters, "warmup": max(1, args.warmup), "ms_per_step": cb["seconds"] * 1e3 / iters,
+            "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE.json config 2)",
             "config": workload_config(P, args),
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
@@ -186,7 +189,8 @@ def workload_config(P, args, eng_info=None):
     cfg = {"workload": WORKLOADS[args.config],
            "n": n, "nnz": int(P.A.nnz), "edges": E, "tol": "1e-8*||b||_inf",
            "max_iter": 300 if args.config == 4 else 20000,
-           "l2": "inputs larger than L2: %.0f MB moved per sweep vs 126 MB L2" % ((40 * E + 24 * n) / 1e6),
+           "l2": "inputs larger than L2: %.0f MB (SURVEY B_sweep) per step vs 126 MB L2; no flush needed" % (
+               (40 * E + 24 * n) / 1e6),
            "parallelism": f"{args.gpus} independent replicas (one system per GPU)"}
     if eng_info:
         cfg["layout"] = {1: "DIA", 2: "CSR"}[eng_info["layout"]]
