@@ -292,3 +292,15 @@ def test_gpu_line_rejects_like_the_reference_on_the_device_path(orc):
     D[3, 4] = D[4, 3] = -1.0
     with pytest.raises(ValueError, match=r"edge \(3,4\) is covered by no large region"):
         g.Hierarchy.from_levels([_csr_from_dense(orc, D)], [4], g.MgSmoother.GabpLine)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pre,post", [(2, 2), (0, 3), (3, 1)])
+def test_gpu_line_smoother_multi_sweep_cycles(orc, pre, post):
+    """Recorded factors for several sweeps per smoothing call (mean-only fast path)."""
+    levels, nx, b = _poisson_levels((5, 4, 3))
+    want = orc.hierarchy(levels, nx, 4).solve(pre, post, b, tol=1e-9)
+    H = g.Hierarchy("poisson", 5, 3, smoother=g.MgSmoother.GabpLine)
+    got = g.mg_solve(H, g.CycleSpec(pre, post, g.MgSmoother.GabpLine), b, g.MgSolveOptions(tol=1e-9))
+    assert (int(got.status), got.iterations) == (want.status, want.iterations)
+    _close(got.solution, want.solution, "x")
