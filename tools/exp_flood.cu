@@ -145,6 +145,10 @@ void run(int N) {
     U("UNIF MINB=4 early-x", 4, false)
     U("UNIF MINB=3 early-x", 3, false)
     U("UNIF MINB=2 early-x", 2, false)
+    U("UNIF MINB=5 early-x", 5, false)
+    U("UNIF MINB=5 DEFER", 5, true)
+    U("UNIF MINB=6 early-x", 6, false)
+    U("UNIF MINB=6 DEFER", 6, true)
     timeit("NONSYM MINB=3 early-x", [&] {
         k_flood_solve_dia<S, false, false, 3, false, true><<<g, 256>>>(P, db, m0, m1, xr, ctrl, spread);
         k_solve_decide_lag2<<<1, 64>>>(ctrl, hist, spread);
