@@ -197,13 +197,14 @@ void LineEngine::smooth_add(const double* r, int sweeps, double* x) {
     ck(cudaMemsetAsync(mc[0], 0, sizeof(double) * n, st), "memset");  // cold start
     for (int s = 0; s < sweeps; ++s) {
         const bool last = s + 1 == sweeps;
-        k_line_mean_phase<true, false><<<lblk(ny, 32), 32, 0, st>>>(P, r, mc[0], mr[0], nullptr, d_fy, rec_rows[s].f,
-                                                                   rec_rows[s].rd, rec_rows[s].W);
+        // parallel affine scans (k_line_mean_rows / _cols); k_line_mean_phase is the serial form
+        k_line_mean_rows<false><<<lblk(ny, 4), 128, 0, st>>>(P, r, mc[0], mr[0], nullptr, d_fy, rec_rows[s].f,
+                                                             rec_rows[s].rd, rec_rows[s].W);
         if (last)
-            k_line_mean_phase<false, true><<<lblk(nx, 32), 32, 0, st>>>(P, r, mr[0], mc[0], x, d_fy, rec_cols[s].f,
+            k_line_mean_cols<true><<<lblk(nx, kCW), kCT, 0, st>>>(P, r, mr[0], mc[0], x, d_fy, rec_cols[s].f,
                                                                        rec_cols[s].rd, rec_cols[s].W);
         else
-            k_line_mean_phase<false, false><<<lblk(nx, 32), 32, 0, st>>>(P, r, mr[0], mc[0], nullptr, d_fy,
+            k_line_mean_cols<false><<<lblk(nx, kCW), kCT, 0, st>>>(P, r, mr[0], mc[0], nullptr, d_fy,
                                                                         rec_cols[s].f, rec_cols[s].rd, rec_cols[s].W);
     }
     ck(cudaGetLastError(), "line smooth");

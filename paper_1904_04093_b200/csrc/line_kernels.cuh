@@ -216,6 +216,177 @@ static __global__ void __launch_bounds__(32) k_line_mean_phase(LineP P, const do
     }
 }
 
+// ---- parallel-scan versions of the mean-only phases ------------------------------------------
+// The two recurrences are affine: forward y_k = -f_k y_{k-1} + c_k, backward
+// x_k = q_k x_{k+1} + p_k with q_k = -u_k / d_k, p_k = y_k / d_k.  Composing the affine maps with a
+// scan runs a line in O(N / P + log P) dependent steps instead of N (the association differs from
+// the sequential loop, so x agrees with it to rounding; each node is still evaluated by the serial
+// formula from its segment's carry-in).
+//  Rows: one warp per row; a lane owns kLV consecutive nodes of a 32·kLV tile, composes their maps
+//  serially, the warp scans the 32 lane maps with shuffles, a carry runs between tiles.
+//  Columns: a block owns kCW adjacent columns (kCW threads read 8·kCW contiguous bytes of a row:
+//  whole sectors) and splits each column into kSeg segments; the segment maps are scanned in
+//  shared memory.
+struct Aff {
+    double a, b;  // v -> a v + b
+};
+__device__ __forceinline__ Aff aff_then(Aff first, Aff second) {  // second(first(v))
+    return {dmul(second.a, first.a), dadd(dmul(second.a, first.b), second.b)};
+}
+__device__ __forceinline__ double aff_apply(Aff m, double v) { return dadd(dmul(m.a, v), m.b); }
+// exclusive scan of the lane maps in lane order
+__device__ __forceinline__ Aff warp_scan_aff_excl(Aff m) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        Aff p;
+        p.a = __shfl_up_sync(0xffffffffu, m.a, o);
+        p.b = __shfl_up_sync(0xffffffffu, m.b, o);
+        if (lane >= o) m = aff_then(p, m);
+    }
+    Aff e;
+    e.a = __shfl_up_sync(0xffffffffu, m.a, 1);
+    e.b = __shfl_up_sync(0xffffffffu, m.b, 1);
+    return lane == 0 ? Aff{1.0, 0.0} : e;
+}
+
+constexpr int kLV = 4;  // nodes per lane per row tile
+
+template <bool ADDX>
+static __global__ void __launch_bounds__(128) k_line_mean_rows(LineP P, const double* __restrict__ b,
+                                                              const double* __restrict__ m_o, double* __restrict__ m_n,
+                                                              double* __restrict__ x, double* __restrict__ fy,
+                                                              const double* __restrict__ f,
+                                                              const double* __restrict__ rd,
+                                                              const double* __restrict__ W) {
+    const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (row >= P.ny) return;  // warp-uniform
+    const int N = P.nx, base = row * P.nx;
+    double carry = 0.0;
+    for (int t0 = 0; t0 < N; t0 += 32 * kLV) {
+        const int k0 = t0 + lane * kLV;
+        double fk[kLV], ck[kLV];
+        Aff m{1.0, 0.0};
+#pragma unroll
+        for (int j = 0; j < kLV; ++j) {
+            const int k = k0 + j;
+            fk[j] = 0.0;
+            ck[j] = 0.0;
+            if (k < N) {
+                fk[j] = -__ldg(f + base + k);
+                ck[j] = dadd(__ldg(b + base + k), m_o[base + k]);
+                m = aff_then(m, Aff{fk[j], ck[j]});
+            }
+        }
+        double y = aff_apply(warp_scan_aff_excl(m), carry);
+#pragma unroll
+        for (int j = 0; j < kLV; ++j)
+            if (k0 + j < N) {
+                y = dadd(dmul(fk[j], y), ck[j]);
+                fy[base + k0 + j] = y;
+            }
+        carry = __shfl_sync(0xffffffffu, y, 31);
+    }
+    carry = 0.0;
+    for (int t0 = 0; t0 < N; t0 += 32 * kLV) {  // from the end of the row: lane 0 owns the highest k
+        const int k0 = N - 1 - (t0 + lane * kLV);
+        double qk[kLV], pk[kLV];
+        Aff m{1.0, 0.0};
+#pragma unroll
+        for (int j = 0; j < kLV; ++j) {
+            const int k = k0 - j;
+            qk[j] = 0.0;
+            pk[j] = 0.0;
+            if (k >= 0) {
+                const double r = __ldg(rd + base + k);
+                qk[j] = -dmul(__ldg(P.e + base + k), r);
+                pk[j] = dmul(fy[base + k], r);
+                m = aff_then(m, Aff{qk[j], pk[j]});
+            }
+        }
+        double xk = aff_apply(warp_scan_aff_excl(m), carry);
+#pragma unroll
+        for (int j = 0; j < kLV; ++j) {
+            const int k = k0 - j;
+            if (k >= 0) {
+                const int v = base + k;
+                xk = dadd(dmul(qk[j], xk), pk[j]);
+                m_n[v] = dsub(dsub(dmul(__ldg(W + v), xk), __ldg(b + v)), m_o[v]);
+                if (x) x[v] = ADDX ? dadd(x[v], xk) : xk;
+            }
+        }
+        carry = __shfl_sync(0xffffffffu, xk, 31);
+    }
+}
+
+constexpr int kCW = 8;                // columns per block
+constexpr int kCT = 1024;             // threads per block
+constexpr int kSeg = kCT / kCW;       // segments per column
+
+// inclusive scan over the kSeg segment maps of each column; REV: segment order kSeg-1 .. 0
+template <bool REV>
+__device__ __forceinline__ Aff seg_scan_excl(Aff m, int sgm, int c, Aff (*sh)[kCW]) {
+    for (int o = 1; o < kSeg; o <<= 1) {
+        sh[sgm][c] = m;
+        __syncthreads();
+        const int src = REV ? sgm + o : sgm - o;
+        if (REV ? src < kSeg : src >= 0) m = aff_then(sh[src][c], m);
+        __syncthreads();
+    }
+    sh[sgm][c] = m;
+    __syncthreads();
+    const int src = REV ? sgm + 1 : sgm - 1;
+    const Aff e = (REV ? src < kSeg : src >= 0) ? sh[src][c] : Aff{1.0, 0.0};
+    __syncthreads();
+    return e;
+}
+
+template <bool ADDX>
+static __global__ void __launch_bounds__(kCT) k_line_mean_cols(LineP P, const double* __restrict__ b,
+                                                              const double* __restrict__ m_o, double* __restrict__ m_n,
+                                                              double* __restrict__ x, double* __restrict__ fy,
+                                                              const double* __restrict__ f,
+                                                              const double* __restrict__ rd,
+                                                              const double* __restrict__ W) {
+    __shared__ Aff sh[kSeg][kCW];
+    const int c = threadIdx.x % kCW, sgm = threadIdx.x / kCW;
+    const int col = blockIdx.x * kCW + c;
+    const bool ok = col < P.nx;
+    const int nx = P.nx, N = P.ny, L = (N + kSeg - 1) / kSeg;
+    const int k0 = min(N, sgm * L), k1 = min(N, k0 + L);
+    Aff m{1.0, 0.0};
+    if (ok)
+#pragma unroll 4
+        for (int k = k0; k < k1; ++k) {
+            const int v = k * nx + col;
+            m = aff_then(m, Aff{-__ldg(f + v), dadd(__ldg(b + v), m_o[v])});
+        }
+    double y = aff_apply(seg_scan_excl<false>(m, sgm, c, sh), 0.0);
+    // the forward evaluation also builds the segment's backward map x_{k0} = C(x_{k1}), composed
+    // from k0 upward (C <- C o N_k), so fy is not re-read for it
+    m = Aff{1.0, 0.0};
+    if (ok)
+#pragma unroll 4
+        for (int k = k0; k < k1; ++k) {
+            const int v = k * nx + col;
+            y = dadd(dmul(-__ldg(f + v), y), dadd(__ldg(b + v), m_o[v]));
+            fy[v] = y;
+            const double r = __ldg(rd + v);
+            m = aff_then(Aff{-dmul(__ldg(P.nn + v), r), dmul(y, r)}, m);
+        }
+    double xn = aff_apply(seg_scan_excl<true>(m, sgm, c, sh), 0.0);
+    if (ok)
+#pragma unroll 4
+        for (int k = k1 - 1; k >= k0; --k) {
+            const int v = k * nx + col;
+            const double r = __ldg(rd + v);
+            const double xk = dadd(dmul(-dmul(__ldg(P.nn + v), r), xn), dmul(fy[v], r));
+            m_n[v] = dsub(dsub(dmul(__ldg(W + v), xk), __ldg(b + v)), m_o[v]);
+            if (x) x[v] = ADDX ? dadd(x[v], xk) : xk;
+            xn = xk;
+        }
+}
+
 // r = b - A x in CSR column order (sparse.cpp:104-115) and its NaN-skipping inf-norm
 static __global__ void k_line_residual(LineP P, const double* __restrict__ b, const double* __restrict__ x,
                                        double* __restrict__ r, unsigned long long* rmax, const int* done) {

@@ -7,6 +7,7 @@
 // reference's Eigen PartialPivLU; only that solve's rounding differs from the reference.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -74,6 +75,42 @@ std::vector<double> dense_inverse(const Engine& E) {
     return inv;
 }
 
+// reset every level's Ctrl the way the host template of Engine::reset_ctrl does; one block per level
+__global__ void k_mg_clear(Ctrl* const* c, int nl) {
+    if ((int)blockIdx.x >= nl) return;
+    Ctrl* t = c[blockIdx.x];
+    unsigned* w = reinterpret_cast<unsigned*>(t);
+    for (int i = threadIdx.x; i < (int)(sizeof(Ctrl) / sizeof(unsigned)); i += blockDim.x) w[i] = 0u;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < 4; ++q) t->epiv[q] = t->npiv[q] = kNone;
+        t->opiv = kNone;
+    }
+}
+
+// out[0] = *rres (the stop test's residual bits) or 0; out[1] = min over halted levels of
+// (fail_seq << 32 | level), kNone if no level halted: the first failure in execution order
+__global__ void k_mg_summary(Ctrl* const* c, int nl, const unsigned long long* rres, unsigned long long* out) {
+    unsigned long long best = kNone;
+    for (int k = 0; k < nl; ++k)
+        if (c[k]->halt) {
+            const unsigned long long key = ((unsigned long long)(unsigned)c[k]->fail_seq << 32) | (unsigned)k;
+            best = key < best ? key : best;
+        }
+    out[0] = rres ? *rres : 0ull;
+    out[1] = best;
+}
+
+// a captured V-cycle (cycle(0, ...) plus the Ctrl reset) for one (spec, b, x, reuse) key
+struct CycleGraph {
+    int pre = 0, post = 0, frozen = 0;
+    const double* b = nullptr;
+    const double* x = nullptr;
+    bool reuse = false;
+    int seen = 0;
+    cudaGraphExec_t exec = nullptr;
+};
+
 }  // namespace
 
 struct bgmg {
@@ -86,9 +123,19 @@ struct bgmg {
     std::vector<double> fine_rhs;  // named hierarchies: Hierarchy::fine_rhs
     Ctrl* h_ctrl = nullptr;
     int seq = 0;
+    Ctrl** d_ctrls = nullptr;               // every level's d_ctrl, for k_mg_clear / k_mg_summary
+    unsigned long long* d_sum = nullptr;    // k_mg_summary output
+    unsigned long long* h_sum = nullptr;    // pinned copy of it
+    std::vector<CycleGraph> graphs;
+    bool use_graphs = true;
 
     ~bgmg() {
         if (st) cudaStreamSynchronize(st);
+        for (auto& g : graphs)
+            if (g.exec) cudaGraphExecDestroy(g.exec);
+        if (d_ctrls) cudaFree(d_ctrls);
+        if (d_sum) cudaFree(d_sum);
+        if (h_sum) cudaFreeHost(h_sum);
         levels.clear();
         if (d_inv) cudaFree(d_inv);
         if (d_fine_b) cudaFree(d_fine_b);
@@ -172,18 +219,20 @@ struct bgmg {
     }
 
     void clear_failures() {
-        for (auto& lv : levels) {
-            Ctrl c;
-            std::memset(&c, 0, sizeof(c));
-            for (int q = 0; q < 4; ++q) c.epiv[q] = c.npiv[q] = kNone;
-            c.opiv = kNone;
-            ck(cudaMemcpyAsync(lv.E->d_ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, st), "ctrl");
-        }
+        k_mg_clear<<<nl(), 128, 0, st>>>(d_ctrls, nl());
         seq = 0;
     }
 
-    // first smoother failure of the last cycle, in execution order; "" if none
+    // first smoother failure of the last cycle, in execution order; "" if none (one summary read;
+    // the per-level scan only when some level halted)
     std::string failure() {
+        k_mg_summary<<<1, 1, 0, st>>>(d_ctrls, nl(), nullptr, d_sum);
+        ck(cudaMemcpyAsync(h_sum, d_sum, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaStreamSynchronize(st), "sync");
+        return h_sum[1] == kNone ? std::string() : failure_detail();
+    }
+
+    std::string failure_detail() {
         int best_seq = 0x7fffffff, best = -1;
         std::string msg;
         for (int k = 0; k < nl(); ++k) {
@@ -231,11 +280,66 @@ struct bgmg {
         }
     }
 
+    // One V-cycle.  The launch sequence of a cycle depends only on (spec, b, x, reuse of the stop
+    // test's residual): from the second cycle with a key on, the sequence is replayed from a CUDA
+    // graph captured once (host launch overhead dominates the coarse levels).  Anything a first
+    // call sets up (recorded factors, level orders, pipeline tables) exists by then; a capture
+    // that fails for any reason turns graphs off and the cycle runs as plain launches.
     void v_cycle_dev(const bgmg_cycle& spec, const double* b, double* x) {
         prepare(spec);
+        const bool reuse = fine_r_b == b && fine_r_x == x;
+        CycleGraph* g = nullptr;
+        if (use_graphs) {
+            for (auto& c : graphs)
+                if (c.pre == spec.pre && c.post == spec.post && c.frozen == spec.frozen && c.b == b && c.x == x &&
+                    c.reuse == reuse)
+                    g = &c;
+            if (!g) {
+                CycleGraph c;
+                c.pre = spec.pre;
+                c.post = spec.post;
+                c.frozen = spec.frozen;
+                c.b = b;
+                c.x = x;
+                c.reuse = reuse;
+                graphs.push_back(c);
+                g = &graphs.back();
+            }
+            if (!g->exec && ++g->seen >= 2) capture(*g, spec, b, x);
+        }
+        if (g && g->exec) {
+            fine_r_b = fine_r_x = nullptr;
+            seq = 0;
+            ck(cudaGraphLaunch(g->exec, st), "graph launch");
+            return;
+        }
         clear_failures();
         cycle(0, spec, b, x);
         ck(cudaGetLastError(), "v-cycle");
+    }
+
+    void capture(CycleGraph& g, const bgmg_cycle& spec, const double* b, double* x) {
+        const double *rb = fine_r_b, *rx = fine_r_x;
+        cudaGraph_t graph = nullptr;
+        bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+        if (ok) {
+            try {
+                clear_failures();
+                cycle(0, spec, b, x);
+            } catch (...) {
+                ok = false;
+            }
+            ok = cudaStreamEndCapture(st, &graph) == cudaSuccess && ok && graph;
+        }
+        if (ok) ok = cudaGraphInstantiate(&g.exec, graph, 0) == cudaSuccess;
+        if (graph) cudaGraphDestroy(graph);
+        if (!ok) {
+            g.exec = nullptr;
+            use_graphs = false;
+            cudaGetLastError();  // clear the capture error; the cycle runs uncaptured
+        }
+        fine_r_b = rb;  // cycle() consumed them during capture; the replay (or the plain cycle) needs them
+        fine_r_x = rx;
     }
 
     // the stop test's residual r = b - A x also serves the next cycle's first smoothing call (same
@@ -288,8 +392,17 @@ struct bgmg {
         }
         for (int it = 1; it <= o.max_cycles; ++it) {
             v_cycle_dev(spec, b, x);
-            const double r = residual_inf(b, x);
-            std::string f = failure();
+            // stop test and failure summary in one read
+            Engine& L = E(0);
+            ck(cudaMemsetAsync(&L.d_ctrl->red[2], 0, sizeof(unsigned long long), st), "memset");
+            L.launch_residual(b, x, L.d_r, &L.d_ctrl->red[2], MODE_PLAIN);
+            fine_r_b = b;
+            fine_r_x = x;
+            k_mg_summary<<<1, 1, 0, st>>>(d_ctrls, nl(), &L.d_ctrl->red[2], d_sum);
+            ck(cudaMemcpyAsync(h_sum, d_sum, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaStreamSynchronize(st), "sync");
+            const double r = bits2d(h_sum[0]);
+            std::string f = h_sum[1] == kNone ? std::string() : failure_detail();
             rep.iterations = it;
             if (!f.empty()) {
                 rep.status = BGABP_DIVERGED;
@@ -368,6 +481,13 @@ static void build_hierarchy(bgmg* h, int nlevels, const int* n, const int* const
             L.frozen_pending = true;
         }
     }
+    std::vector<Ctrl*> ctrls;
+    for (auto& L : h->levels) ctrls.push_back(L.E->d_ctrl);
+    ck(cudaMalloc(&h->d_ctrls, sizeof(Ctrl*) * ctrls.size()), "malloc");
+    ck(cudaMemcpyAsync(h->d_ctrls, ctrls.data(), sizeof(Ctrl*) * ctrls.size(), cudaMemcpyHostToDevice, h->st), "H2D");
+    ck(cudaMalloc(&h->d_sum, 2 * sizeof(unsigned long long)), "malloc");
+    ck(cudaMallocHost((void**)&h->h_sum, 2 * sizeof(unsigned long long)), "host sum");
+    if (const char* e = std::getenv("BGABP_MG_GRAPH")) h->use_graphs = std::atoi(e) != 0;
     Engine& C = *h->levels.back().E;
     std::vector<double> inv = dense_inverse(C);
     ck(cudaMalloc(&h->d_inv, sizeof(double) * std::max<size_t>(inv.size(), 1)), "malloc");
