@@ -742,21 +742,21 @@ void Engine::enqueue_fused_kernel() {
 #define FUSED(SS_, MB_, DF_, MBU_, DFU_)                                                                            \
     if (sharded) {                                                                                                 \
         if (symmetric) {                                                                                           \
-            if (dl) k_flood_solve_dia<SS_, true, true, MB_, DF_, true, false, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread); \
-            else k_flood_solve_dia<SS_, false, true, MB_, DF_, true, false, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread); \
+            if (dl) k_flood_solve_dia<SS_, true, true, MB_, DF_, true, false, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
+            else k_flood_solve_dia<SS_, false, true, MB_, DF_, true, false, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
         } else {                                                                                                   \
-            if (dl) k_flood_solve_dia<SS_, true, false, MB_, DF_, true, false, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread); \
-            else k_flood_solve_dia<SS_, false, false, MB_, DF_, true, false, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread); \
+            if (dl) k_flood_solve_dia<SS_, true, false, MB_, DF_, true, false, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
+            else k_flood_solve_dia<SS_, false, false, MB_, DF_, true, false, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
         }                                                                                                          \
     } else if (dia.uniform) {                                                                                      \
-        if (dl) k_flood_solve_dia<SS_, true, true, MBU_, DFU_, true, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread); \
-        else k_flood_solve_dia<SS_, false, true, MBU_, DFU_, true, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread); \
+        if (dl) k_flood_solve_dia<SS_, true, true, MBU_, DFU_, true, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
+        else k_flood_solve_dia<SS_, false, true, MBU_, DFU_, true, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
     } else if (symmetric) {                                                                                        \
-        if (dl) k_flood_solve_dia<SS_, true, true, MB_, DF_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread); \
-        else k_flood_solve_dia<SS_, false, true, MB_, DF_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread); \
+        if (dl) k_flood_solve_dia<SS_, true, true, MB_, DF_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
+        else k_flood_solve_dia<SS_, false, true, MB_, DF_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
     } else {                                                                                                       \
-        if (dl) k_flood_solve_dia<SS_, true, false, MB_, DF_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread); \
-        else k_flood_solve_dia<SS_, false, false, MB_, DF_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread); \
+        if (dl) k_flood_solve_dia<SS_, true, false, MB_, DF_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
+        else k_flood_solve_dia<SS_, false, false, MB_, DF_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
     }
         if (timed_events) ck(cudaEventRecord((*timed_events)[2 * timed_index], st), "event");
         // (resident blocks, deferred x loads) per slot count, from tools/exp_flood.cu on the B200:

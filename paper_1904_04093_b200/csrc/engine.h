@@ -70,7 +70,7 @@ struct Engine {
     int cur = 0;
     double *d_b = nullptr, *d_x = nullptr, *d_r = nullptr, *d_e = nullptr, *d_aux = nullptr;
     double* d_hist = nullptr;
-    double* d_xf = nullptr;          // fused flood solve: x(k) in ring slot k & 3 ([4][n])
+    double* d_xf = nullptr;          // fused flood solve: x(k) in ring slot k % kXRing ([kXRing][n])
 
     unsigned long long* d_spread = nullptr;  // per-warp max slots of the fused solve step
     long long hist_cap = 0;

@@ -21,6 +21,300 @@ using namespace bgabp;
         }                                                                                  \
     } while (0)
 
+// the fused step as of commit 05b7882 (x in two plain buffers), for A/B timing
+namespace bgabp {
+template <int S, bool DELTA, bool SYM, int MINB = 4, bool DEFER = true, bool RES = true, bool ASYNC = false,
+          bool UNC = true>
+static __global__ void __launch_bounds__(256, MINB) k_old_solve(DiaP P, const double* __restrict__ b, double2* m0,
+                                                              double2* m1, double* x0, double* x1, Ctrl* ctrl,
+                                                              unsigned long long* spread) {
+    if (ld_ctrl(&ctrl->done)) return;
+    const int t = ld_ctrl(&ctrl->step);
+    const double2* __restrict__ min = (t & 1) ? m0 : m1;
+    double2* __restrict__ mout = (t & 1) ? m1 : m0;
+    double* __restrict__ xw = ((t - 1) & 1) ? x1 : x0;        // x(t-1)
+    const double* __restrict__ xr = ((t - 2) & 1) ? x1 : x0;  // x(t-2)
+    const int n = P.n;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool res = RES && t >= 3;
+    double dmax = 0.0, rabs = 0.0;
+    // ASYNC: stage x(t-2) at j and j+off_s for the whole block into shared memory with LDGSTS
+    // before the sweep, so the residual's loads are in flight during the message work without
+    // holding registers.  Requires blockDim.x == 256.
+    __shared__ double xs[ASYNC ? (S + 1) * 256 : 1];
+    if (ASYNC && res) {
+#pragma unroll
+        for (int s = 0; s <= S; ++s) {
+            const int o = s < S ? P.off[s] : 0;
+            const long long q = (long long)j + o;
+            cp_async8(&xs[s * 256 + threadIdx.x], xr + (q >= 0 && q < n ? q : 0), q >= 0 && q < n);
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    }
+    if (j < n) {
+        const uint32_t mk = P.mask[j];
+        const double dj = P.diag[j];
+        const double bj = b[j];
+        double sig = 0.0, acc = bj;
+        double2 in[S];
+        double cc[S], xn[S], rv[S];
+        double xj = 0.0;
+        // UNC: issue every load at once, independent of the mask (slot-major arrays are full
+        // size, indices are clamped; the mask still selects every term below).  Predicating the
+        // loads on the mask serialises a second DRAM round trip behind the mask load (ncu: the
+        // mask test and the first message use were the two hottest stall sites).
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            in[s] = make_double2(0.0, 0.0);
+            cc[s] = 0.0;
+            xn[s] = 0.0;
+            rv[s] = 0.0;
+            const bool pin = UNC || (mk & (1u << s)), pout = UNC || (mk & (1u << (16 + s)));
+            if (pin) in[s] = __ldg(min + s * n + j);
+            // symmetric A stores every undirected edge twice; read the negative-offset slots from
+            // the partner's positive slot (A_{j-d,j} = A_{j,j-d} = c[rev s][j-d]): same bits, and
+            // those lines were just fetched for node j-d, so the coefficient DRAM traffic halves
+            if (pout) {
+                const double v = __ldg(SYM && s < P.nneg ? P.c + P.rev[s] * n + max(j + P.off[s], 0) : P.c + s * n + j);
+                cc[s] = (mk & (1u << (16 + s))) ? v : 0.0;
+            }
+            if (!DEFER && res && pin) {
+                const int q = j + P.off[s];
+                xn[s] = xr[q < 0 ? 0 : (q >= n ? n - 1 : q)];
+                if (!SYM) rv[s] = __ldg(P.rowv + s * n + j);
+            }
+        }
+        if (!DEFER && res) xj = xr[j];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            if (s == P.nneg) sig = dadd(sig, dj);
+            if (mk & (1u << s)) {
+                acc = dadd(acc, in[s].y);
+                if (mk & (1u << (16 + s))) sig = dadd(sig, dmul(in[s].x, cc[s]));
+            }
+        }
+        if (P.nneg == S) sig = dadd(sig, dj);
+        if (t >= 2) {  // x-stage of sweep t-1
+            xw[j] = ddiv(acc, sig);
+            if (fabs(sig) < kPivotFloor) atomicMin(&ctrl->npiv[(t - 1) & 3], (unsigned long long)j);
+        }
+        if (!DEFER && res) {  // residual of x(t-2) in CSR order (sparse.cpp:108-114)
+            double r = bj;
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                if (s == P.nneg) r = dsub(r, dmul(dj, xj));
+                if (mk & (1u << s)) r = dsub(r, dmul(SYM ? cc[s] : rv[s], xn[s]));
+            }
+            if (P.nneg == S) r = dsub(r, dmul(dj, xj));
+            rabs = nan_skip_abs(r);
+        }
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            if (!(mk & (1u << (16 + s)))) continue;
+            const double den = dsub(sig, dmul(in[s].x, cc[s]));
+            const int k = j + P.off[s];
+            if (fabs(den) < kPivotFloor)
+                atomicMin(&ctrl->epiv[t & 3], ((unsigned long long)j << 32) | (unsigned)k);
+            const double nl = ddiv(-cc[s], den);
+            const double nm = dmul(nl, dsub(acc, in[s].y));
+            double2* dst = mout + P.rev[s] * n + k;
+            if (DELTA) {
+                const double2 o = min[P.rev[s] * n + k];
+                dmax = fmax(dmax, fmax(nan_skip_abs(dsub(nl, o.x)), nan_skip_abs(dsub(nm, o.y))));
+            }
+            *dst = make_double2(nl, nm);
+        }
+        if (ASYNC && res) {
+            cp_async_wait_all();  // own copies only: each thread reads back what it staged
+            double r = bj;
+            const double xjj = xs[S * 256 + threadIdx.x];
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                if (s == P.nneg) r = dsub(r, dmul(dj, xjj));
+                if (mk & (1u << s))
+                    r = dsub(r, dmul(SYM ? cc[s] : __ldg(P.rowv + s * n + j), xs[s * 256 + threadIdx.x]));
+            }
+            if (P.nneg == S) r = dsub(r, dmul(dj, xjj));
+            rabs = nan_skip_abs(r);
+        } else if (DEFER && res) {
+            double r = bj;
+            const double xjj = xr[j];
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                if (mk & (1u << s)) {
+                    xn[s] = xr[j + P.off[s]];
+                    if (!SYM) rv[s] = __ldg(P.rowv + s * n + j);
+                }
+            }
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                if (s == P.nneg) r = dsub(r, dmul(dj, xjj));
+                if (mk & (1u << s)) r = dsub(r, dmul(SYM ? cc[s] : rv[s], xn[s]));
+            }
+            if (P.nneg == S) r = dsub(r, dmul(dj, xjj));
+            rabs = nan_skip_abs(r);
+        }
+    }
+    if (res) warp_max_spread(spread + (size_t)((t - 2) & 3) * kSpread, rabs);
+    if (DELTA) warp_max_spread(spread + (size_t)(4 + (t & 3)) * kSpread, dmax);
+}
+
+template <int S, bool DELTA, bool SYM, int MINB = 4, bool DEFER = true, bool RES = true, bool ASYNC = false,
+          bool UNC = true>
+static __global__ void __launch_bounds__(256, MINB) k_old_nosm(DiaP P, const double* __restrict__ b, double2* m0,
+                                                              double2* m1, double* x0, double* x1, Ctrl* ctrl,
+                                                              unsigned long long* spread) {
+    if (ld_ctrl(&ctrl->done)) return;
+    const int t = ld_ctrl(&ctrl->step);
+    const double2* __restrict__ min = (t & 1) ? m0 : m1;
+    double2* __restrict__ mout = (t & 1) ? m1 : m0;
+    double* __restrict__ xw = ((t - 1) & 1) ? x1 : x0;        // x(t-1)
+    const double* __restrict__ xr = ((t - 2) & 1) ? x1 : x0;  // x(t-2)
+    const int n = P.n;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool res = RES && t >= 3;
+    double dmax = 0.0, rabs = 0.0;
+    // ASYNC: stage x(t-2) at j and j+off_s for the whole block into shared memory with LDGSTS
+    // before the sweep, so the residual's loads are in flight during the message work without
+    // holding registers.  Requires blockDim.x == 256.
+    double* xs = nullptr;
+    if (ASYNC && res) {
+#pragma unroll
+        for (int s = 0; s <= S; ++s) {
+            const int o = s < S ? P.off[s] : 0;
+            const long long q = (long long)j + o;
+            cp_async8(&xs[s * 256 + threadIdx.x], xr + (q >= 0 && q < n ? q : 0), q >= 0 && q < n);
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    }
+    if (j < n) {
+        const uint32_t mk = P.mask[j];
+        const double dj = P.diag[j];
+        const double bj = b[j];
+        double sig = 0.0, acc = bj;
+        double2 in[S];
+        double cc[S], xn[S], rv[S];
+        double xj = 0.0;
+        // UNC: issue every load at once, independent of the mask (slot-major arrays are full
+        // size, indices are clamped; the mask still selects every term below).  Predicating the
+        // loads on the mask serialises a second DRAM round trip behind the mask load (ncu: the
+        // mask test and the first message use were the two hottest stall sites).
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            in[s] = make_double2(0.0, 0.0);
+            cc[s] = 0.0;
+            xn[s] = 0.0;
+            rv[s] = 0.0;
+            const bool pin = UNC || (mk & (1u << s)), pout = UNC || (mk & (1u << (16 + s)));
+            if (pin) in[s] = __ldg(min + s * n + j);
+            // symmetric A stores every undirected edge twice; read the negative-offset slots from
+            // the partner's positive slot (A_{j-d,j} = A_{j,j-d} = c[rev s][j-d]): same bits, and
+            // those lines were just fetched for node j-d, so the coefficient DRAM traffic halves
+            if (pout) {
+                const double v = __ldg(SYM && s < P.nneg ? P.c + P.rev[s] * n + max(j + P.off[s], 0) : P.c + s * n + j);
+                cc[s] = (mk & (1u << (16 + s))) ? v : 0.0;
+            }
+            if (!DEFER && res && pin) {
+                const int q = j + P.off[s];
+                xn[s] = xr[q < 0 ? 0 : (q >= n ? n - 1 : q)];
+                if (!SYM) rv[s] = __ldg(P.rowv + s * n + j);
+            }
+        }
+        if (!DEFER && res) xj = xr[j];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            if (s == P.nneg) sig = dadd(sig, dj);
+            if (mk & (1u << s)) {
+                acc = dadd(acc, in[s].y);
+                if (mk & (1u << (16 + s))) sig = dadd(sig, dmul(in[s].x, cc[s]));
+            }
+        }
+        if (P.nneg == S) sig = dadd(sig, dj);
+        if (t >= 2) {  // x-stage of sweep t-1
+            xw[j] = ddiv(acc, sig);
+            if (fabs(sig) < kPivotFloor) atomicMin(&ctrl->npiv[(t - 1) & 3], (unsigned long long)j);
+        }
+        if (!DEFER && res) {  // residual of x(t-2) in CSR order (sparse.cpp:108-114)
+            double r = bj;
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                if (s == P.nneg) r = dsub(r, dmul(dj, xj));
+                if (mk & (1u << s)) r = dsub(r, dmul(SYM ? cc[s] : rv[s], xn[s]));
+            }
+            if (P.nneg == S) r = dsub(r, dmul(dj, xj));
+            rabs = nan_skip_abs(r);
+        }
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            if (!(mk & (1u << (16 + s)))) continue;
+            const double den = dsub(sig, dmul(in[s].x, cc[s]));
+            const int k = j + P.off[s];
+            if (fabs(den) < kPivotFloor)
+                atomicMin(&ctrl->epiv[t & 3], ((unsigned long long)j << 32) | (unsigned)k);
+            const double nl = ddiv(-cc[s], den);
+            const double nm = dmul(nl, dsub(acc, in[s].y));
+            double2* dst = mout + P.rev[s] * n + k;
+            if (DELTA) {
+                const double2 o = min[P.rev[s] * n + k];
+                dmax = fmax(dmax, fmax(nan_skip_abs(dsub(nl, o.x)), nan_skip_abs(dsub(nm, o.y))));
+            }
+            *dst = make_double2(nl, nm);
+        }
+        if (ASYNC && res) {
+            cp_async_wait_all();  // own copies only: each thread reads back what it staged
+            double r = bj;
+            const double xjj = xs[S * 256 + threadIdx.x];
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                if (s == P.nneg) r = dsub(r, dmul(dj, xjj));
+                if (mk & (1u << s))
+                    r = dsub(r, dmul(SYM ? cc[s] : __ldg(P.rowv + s * n + j), xs[s * 256 + threadIdx.x]));
+            }
+            if (P.nneg == S) r = dsub(r, dmul(dj, xjj));
+            rabs = nan_skip_abs(r);
+        } else if (DEFER && res) {
+            double r = bj;
+            const double xjj = xr[j];
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                if (mk & (1u << s)) {
+                    xn[s] = xr[j + P.off[s]];
+                    if (!SYM) rv[s] = __ldg(P.rowv + s * n + j);
+                }
+            }
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                if (s == P.nneg) r = dsub(r, dmul(dj, xjj));
+                if (mk & (1u << s)) r = dsub(r, dmul(SYM ? cc[s] : rv[s], xn[s]));
+            }
+            if (P.nneg == S) r = dsub(r, dmul(dj, xjj));
+            rabs = nan_skip_abs(r);
+        }
+    }
+    if (res) warp_max_spread(spread + (size_t)((t - 2) & 3) * kSpread, rabs);
+    if (DELTA) warp_max_spread(spread + (size_t)(4 + (t & 3)) * kSpread, dmax);
+}
+
+
+// the current node body, launched with x(t-1) / x(t-2) as two separately passed buffers
+template <int S, bool SYM, int MINB, bool DEFER>
+static __global__ void __launch_bounds__(256, MINB) k_new_x01(DiaP P, const double* __restrict__ b, double2* m0,
+                                                              double2* m1, double* x0, double* x1, Ctrl* ctrl,
+                                                              unsigned long long* spread) {
+    if (ld_ctrl(&ctrl->done)) return;
+    const int t = ld_ctrl(&ctrl->step);
+    const double2* __restrict__ min = (t & 1) ? m0 : m1;
+    double2* __restrict__ mout = (t & 1) ? m1 : m0;
+    double* __restrict__ xw = ((t - 1) & 1) ? x1 : x0;
+    const double* __restrict__ xr = ((t - 2) & 1) ? x1 : x0;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool res = t >= 3;
+    double dmax = 0.0, rabs = 0.0;
+    if (j < P.n) flood_solve_node<S, false, SYM, DEFER, true, false, false>(P, b, min, mout, xw, xr, ctrl, t, res, j, rabs, dmax);
+    if (res) warp_max_spread(spread + (size_t)((t - 2) & 3) * kSpread, rabs);
+}
+}  // namespace bgabp
+
 template <class T>
 T* up(const std::vector<T>& v) {
     T* d;
@@ -76,7 +370,7 @@ void run(int N) {
     }
     P.mask = up(mask);
     P.c = up(c);
-    P.rowv = P.c;
+    P.rowv = getenv("EXP_SHARED_ROWV") ? P.c : up(c);  // nonsymmetric variants read their own row copy
     P.diag = up(diag);
     double* db = up(b);
     double2 *m0, *m1;
@@ -128,18 +422,19 @@ void run(int N) {
     };
 #define W(NAME, MINB, DEFER, UNC)                                                                             \
     timeit(NAME, [&] {                                                                                        \
-        k_flood_solve_dia<S, false, true, MINB, DEFER, UNC><<<g, 256>>>(P, db, m0, m1, xr, ctrl, spread); \
+        k_flood_solve_dia<S, false, true, MINB, DEFER, UNC><<<g, 256>>>(P, db, m0, m1, xr, xr + n, ctrl, spread); \
         k_solve_decide_lag2<<<1, 64>>>(ctrl, hist, spread);                                                   \
     });
 #define U(NAME, MINB, DEFER)                                                                                 \
     timeit(NAME, [&] {                                                                                        \
         P.uniform = 1;                                                                                        \
-        k_flood_solve_dia<S, false, true, MINB, DEFER, true, true><<<g, 256>>>(P, db, m0, m1, xr, ctrl, spread); \
+        k_flood_solve_dia<S, false, true, MINB, DEFER, true, true><<<g, 256>>>(P, db, m0, m1, xr, xr + n, ctrl, spread); \
         k_solve_decide_lag2<<<1, 64>>>(ctrl, hist, spread);                                                   \
         P.uniform = 0;                                                                                        \
     });
     for (int s = 0; s < S; ++s) P.cu[s] = -1.0;
     P.du = 2.0 * dims + 0.01;
+    if (!getenv("EXP_ONLY_NONSYM")) {
     U("UNIF MINB=4 DEFER", 4, true)
     U("UNIF MINB=3 DEFER", 3, true)
     U("UNIF MINB=4 early-x", 4, false)
@@ -149,10 +444,32 @@ void run(int N) {
     U("UNIF MINB=5 DEFER", 5, true)
     U("UNIF MINB=6 early-x", 6, false)
     U("UNIF MINB=6 DEFER", 6, true)
-    timeit("NONSYM MINB=3 early-x", [&] {
-        k_flood_solve_dia<S, false, false, 3, false, true><<<g, 256>>>(P, db, m0, m1, xr, ctrl, spread);
+    }
+#define NS(NAME, MINB, DEFER, UNC)                                                                            \
+    timeit(NAME, [&] {                                                                                        \
+        k_flood_solve_dia<S, false, false, MINB, DEFER, UNC><<<g, 256>>>(P, db, m0, m1, xr, xr + n, ctrl, spread);   \
+        k_solve_decide_lag2<<<1, 64>>>(ctrl, hist, spread);                                                   \
+    });
+    timeit("OLDK NONSYM MINB=3 early-x", [&] {
+        k_old_solve<S, false, false, 3, false><<<g, 256>>>(P, db, m0, m1, xr, xr + n, ctrl, spread);
         k_solve_decide_lag2<<<1, 64>>>(ctrl, hist, spread);
     });
+    timeit("OLDK no-smem NONSYM MINB=3 early-x", [&] {
+        k_old_nosm<S, false, false, 3, false><<<g, 256>>>(P, db, m0, m1, xr, xr + n, ctrl, spread);
+        k_solve_decide_lag2<<<1, 64>>>(ctrl, hist, spread);
+    });
+    timeit("NEW x0/x1 NONSYM MINB=3 early-x", [&] {
+        k_new_x01<S, false, 3, false><<<g, 256>>>(P, db, m0, m1, xr, xr + n, ctrl, spread);
+        k_solve_decide_lag2<<<1, 64>>>(ctrl, hist, spread);
+    });
+    NS("NONSYM MINB=3 early-x", 3, false, true)
+    NS("NONSYM MINB=2 early-x", 2, false, true)
+    NS("NONSYM MINB=4 early-x", 4, false, true)
+    NS("NONSYM MINB=3 DEFER", 3, true, true)
+    NS("NONSYM MINB=2 DEFER", 2, true, true)
+    NS("NONSYM MINB=4 DEFER", 4, true, true)
+    NS("NONSYM MINB=3 early-x predicated", 3, false, false)
+    if (getenv("EXP_ONLY_NONSYM")) return;
     W("MINB=4 DEFER predicated", 4, true, false)
     W("MINB=4 DEFER unconditional", 4, true, true)
     W("MINB=3 DEFER unconditional", 3, true, true)
@@ -160,7 +477,7 @@ void run(int N) {
     W("MINB=3 early-x unconditional", 3, false, true)
     W("MINB=2 early-x unconditional", 2, false, true)
     timeit("MINB=3 early-x unconditional DELTA", [&] {
-        k_flood_solve_dia<S, true, true, 3, false, true><<<g, 256>>>(P, db, m0, m1, xr, ctrl, spread);
+        k_flood_solve_dia<S, true, true, 3, false, true><<<g, 256>>>(P, db, m0, m1, xr, xr + n, ctrl, spread);
         k_solve_decide_lag2<<<1, 64>>>(ctrl, hist, spread);
     });
     cudaFree(m0);
