@@ -295,6 +295,10 @@ struct bgmg {
                     c.reuse == reuse)
                     g = &c;
             if (!g) {
+                if (graphs.size() >= 8) {  // bounded: callers cycling through many buffers
+                    if (graphs.front().exec) cudaGraphExecDestroy(graphs.front().exec);
+                    graphs.erase(graphs.begin());
+                }
                 CycleGraph c;
                 c.pre = spec.pre;
                 c.post = spec.post;

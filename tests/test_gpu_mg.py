@@ -105,6 +105,45 @@ def test_repeated_runs_bit_identical():
     assert a.iterations == b.iterations and a.residual_history.tobytes() == b.residual_history.tobytes()
 
 
+@pytest.mark.parametrize("sm,pre,post", [(S.GabpRedBlack, 2, 2), (S.GabpSequential, 1, 1), (S.GabpFlood, 2, 2),
+                                         (S.GabpLine, 1, 1), (S.GsRedBlack, 2, 2), (S.Jacobi, 1, 1)])
+def test_captured_cycles_match_plain_launches(monkeypatch, sm, pre, post):
+    """From the second cycle on a V-cycle replays a captured CUDA graph (BGABP_MG_GRAPH=0: plain
+    launches); both must give the same residual history bit for bit, for solves on host and on
+    device buffers, and for a second solve on the same hierarchy."""
+    import torch
+
+    def run():
+        h = g.Hierarchy("poisson", 6, 4, {}, sm)
+        spec, opt = g.CycleSpec(pre, post, sm), g.MgSolveOptions(tol=1e-10, max_cycles=12)
+        r1 = g.mg_solve(h, spec, h.fine_rhs(), opt)
+        b = torch.tensor(h.fine_rhs(), device="cuda")
+        x = torch.zeros_like(b)
+        r2 = g.mg_solve_device(h, spec, b.data_ptr(), x.data_ptr(), opt)
+        r3 = g.mg_solve(h, spec, 2.0 * h.fine_rhs(), opt)
+        return [r1, r2, r3], x.cpu().numpy()
+
+    monkeypatch.setenv("BGABP_MG_GRAPH", "0")
+    plain, xp = run()
+    monkeypatch.setenv("BGABP_MG_GRAPH", "1")
+    graph, xg = run()
+    for a, b in zip(plain, graph):
+        assert a.status == b.status and a.iterations == b.iterations
+        assert a.residual_history.tobytes() == b.residual_history.tobytes()
+    assert xp.tobytes() == xg.tobytes()
+
+
+def test_captured_cycles_report_smoother_breakdown(monkeypatch):
+    """A breakdown inside a replayed cycle is still reported with the reference's message."""
+    out = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("BGABP_MG_GRAPH", flag)
+        h = g.Hierarchy("boundary-layer", 6, 6, {"eps": 0.01}, S.GabpFlood)
+        r = g.mg_solve(h, g.CycleSpec(2, 2, S.GabpFlood), h.fine_rhs(), g.MgSolveOptions(tol=1e-12, max_cycles=30))
+        out.append((r.status, r.iterations, r.residual_history.tobytes(), r.detail))
+    assert out[0] == out[1]
+
+
 def _oracle_for(ref, orc):
     return ref if ref is not None else orc
 
