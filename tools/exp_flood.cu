@@ -10,6 +10,8 @@
 
 #include "../paper_1904_04093_b200/csrc/kernels.cuh"
 
+#define SYM_ROWS 1
+
 using namespace bgabp;
 
 #define CK(x)                                                                              \
@@ -313,6 +315,117 @@ static __global__ void __launch_bounds__(256, MINB) k_new_x01(DiaP P, const doub
     if (j < P.n) flood_solve_node<S, false, SYM, DEFER, true, false, false>(P, b, min, mout, xw, xr, ctrl, t, res, j, rabs, dmax);
     if (res) warp_max_spread(spread + (size_t)((t - 2) & 3) * kSpread, rabs);
 }
+
+// residual variants: UNC = loads independent of the mask; RED = 0 none, 1 block + one atomic
+// (warp_max_commit), 2 spread slots
+template <int S, bool SYM, bool UNC, int RED>
+static __global__ void __launch_bounds__(256) k_res_var(DiaP P, const double* __restrict__ b,
+                                                        const double* __restrict__ x, double* __restrict__ r,
+                                                        unsigned long long* rmax) {
+    const int n = P.n;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    double a = 0.0;
+    if (j < n) {
+        const uint32_t mk = P.mask[j];
+        const double dj = P.diag[j], xj = x[j];
+        double acc = b[j];
+        double cv[S], xv[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const bool p = UNC || (mk & (1u << s));
+            cv[s] = 0.0;
+            xv[s] = 0.0;
+            if (p) {
+                const int q = j + P.off[s];
+                const int qc = q < 0 ? 0 : (q >= n ? n - 1 : q);
+                cv[s] = __ldg(SYM && s < P.nneg ? P.rowv + (size_t)P.rev[s] * n + qc : P.rowv + (size_t)s * n + j);
+                xv[s] = __ldg(x + qc);
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            if (s == P.nneg) acc = dsub(acc, dmul(dj, xj));
+            if (mk & (1u << s)) acc = dsub(acc, dmul(cv[s], xv[s]));
+        }
+        if (P.nneg == S) acc = dsub(acc, dmul(dj, xj));
+        if (r) r[j] = acc;
+        a = nan_skip_abs(acc);
+    }
+    if (RED == 1) warp_max_commit(rmax, a);
+    if (RED == 2) warp_max_spread(rmax, a);
+    if (RED == 5) {  // warp max to a per-warp partial, folded by k_fold_partials
+        unsigned long long bits = __double_as_longlong(a);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long ot = __shfl_xor_sync(0xffffffffu, bits, o);
+            bits = ot > bits ? ot : bits;
+        }
+        if ((threadIdx.x & 31) == 0) rmax[(blockIdx.x * blockDim.x + threadIdx.x) >> 5] = bits;
+    }
+    if (RED >= 3 && RED <= 4) {  // block max, then one fire-and-forget atomic (3: one word, 4: 64 block-indexed slots)
+        __shared__ unsigned long long part[8];
+        unsigned long long bits = __double_as_longlong(a);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long ot = __shfl_xor_sync(0xffffffffu, bits, o);
+            bits = ot > bits ? ot : bits;
+        }
+        if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = bits;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int k = 1; k < 8; ++k) bits = part[k] > bits ? part[k] : bits;
+            if (bits) atomicMax(RED == 3 ? rmax : rmax + (blockIdx.x & 63), bits);
+        }
+    }
+}
+
+// grid-stride residual: a fixed number of blocks, one block-level max and one atomic per block
+template <int S, bool SYM, bool UNC>
+static __global__ void __launch_bounds__(256) k_res_gs(DiaP P, const double* __restrict__ b,
+                                                       const double* __restrict__ x, double* __restrict__ r,
+                                                       unsigned long long* rmax) {
+    const int n = P.n;
+    double a = 0.0;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const uint32_t mk = P.mask[j];
+        const double dj = P.diag[j], xj = x[j];
+        double acc = b[j];
+        double cv[S], xv[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const bool p = UNC || (mk & (1u << s));
+            cv[s] = 0.0;
+            xv[s] = 0.0;
+            if (p) {
+                const int q = j + P.off[s];
+                const int qc = q < 0 ? 0 : (q >= n ? n - 1 : q);
+                cv[s] = __ldg(SYM && s < P.nneg ? P.rowv + (size_t)P.rev[s] * n + qc : P.rowv + (size_t)s * n + j);
+                xv[s] = __ldg(x + qc);
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            if (s == P.nneg) acc = dsub(acc, dmul(dj, xj));
+            if (mk & (1u << s)) acc = dsub(acc, dmul(cv[s], xv[s]));
+        }
+        if (P.nneg == S) acc = dsub(acc, dmul(dj, xj));
+        if (r) r[j] = acc;
+        a = fmax(a, nan_skip_abs(acc));
+    }
+    warp_max_commit(rmax, a);
+}
+
+static __global__ void __launch_bounds__(1024) k_fold_partials(const unsigned long long* __restrict__ part, int np,
+                                                              unsigned long long* out) {
+    unsigned long long m = 0ull;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) m = part[i] > m ? part[i] : m;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long ot = __shfl_xor_sync(0xffffffffu, m, o);
+        m = ot > m ? ot : m;
+    }
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
 }  // namespace bgabp
 
 template <class T>
@@ -432,6 +545,44 @@ void run(int N) {
         k_solve_decide_lag2<<<1, 64>>>(ctrl, hist, spread);                                                   \
         P.uniform = 0;                                                                                        \
     });
+    if (getenv("EXP_RESIDUAL")) {
+        double* rr;
+        CK(cudaMalloc(&rr, sizeof(double) * n));
+        const double rbytes = 8.0 * n * 4 + 4.0 * n + 8.0 * E / 2 * (SYM_ROWS ? 1 : 2);
+        auto rt = [&](const char* name, auto&& launch) {
+            for (int k = 0; k < 5; ++k) launch();
+            CK(cudaDeviceSynchronize());
+            cudaEventRecord(e0);
+            for (int k = 0; k < steps; ++k) launch();
+            cudaEventRecord(e1);
+            CK(cudaEventSynchronize(e1));
+            CK(cudaGetLastError());
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            const double us = ms * 1e3 / steps;
+            std::printf("S=%d %-44s %8.2f us  %7.1f GB/s\n", S, name, us, rbytes / us / 1e3);
+        };
+        rt("residual (product k_residual_dia, r + rmax)", [&] { k_residual_dia<S, true><<<g, 256>>>(P, db, xr, rr, spread, ctrl, MODE_PLAIN); });
+        rt("residual (product, rmax only)", [&] { k_residual_dia<S, true><<<g, 256>>>(P, db, xr, nullptr, spread, ctrl, MODE_PLAIN); });
+        rt("var predicated, block atomic", [&] { k_res_var<S, true, false, 1><<<g, 256>>>(P, db, xr, rr, spread); });
+        rt("var UNC, block atomic", [&] { k_res_var<S, true, true, 1><<<g, 256>>>(P, db, xr, rr, spread); });
+        rt("var UNC, spread", [&] { k_res_var<S, true, true, 2><<<g, 256>>>(P, db, xr, rr, spread); });
+        rt("var UNC, block RED no precheck", [&] { k_res_var<S, true, true, 3><<<g, 256>>>(P, db, xr, rr, spread); });
+        rt("var UNC, block RED 64 slots", [&] { k_res_var<S, true, true, 4><<<g, 256>>>(P, db, xr, rr, spread); });
+        unsigned long long* parts;
+        const int np = (int)((size_t)g * 256 / 32);
+        CK(cudaMalloc(&parts, sizeof(unsigned long long) * np));
+        rt("var UNC, warp partials + fold kernel", [&] {
+            k_res_var<S, true, true, 5><<<g, 256>>>(P, db, xr, rr, parts);
+            k_fold_partials<<<148, 1024>>>(parts, np, spread);
+        });
+        rt("var UNC, no reduction", [&] { k_res_var<S, true, true, 0><<<g, 256>>>(P, db, xr, rr, spread); });
+        for (int gb : {148 * 4, 148 * 8, 148 * 16, 148 * 32})
+            rt(gb == 592 ? "grid-stride UNC 592 blocks" : gb == 1184 ? "grid-stride UNC 1184 blocks" : gb == 2368 ? "grid-stride UNC 2368 blocks" : "grid-stride UNC 4736 blocks",
+               [&] { k_res_gs<S, true, true><<<gb, 256>>>(P, db, xr, rr, spread); });
+        rt("var predicated, no reduction", [&] { k_res_var<S, true, false, 0><<<g, 256>>>(P, db, xr, rr, spread); });
+        return;
+    }
     for (int s = 0; s < S; ++s) P.cu[s] = -1.0;
     P.du = 2.0 * dims + 0.01;
     if (!getenv("EXP_ONLY_NONSYM")) {
