@@ -123,7 +123,8 @@ struct Engine {
     RbP rb{};
     double2* d_rbmsg = nullptr;
     bool rb_applicable(const bgabp_schedule& s) const;
-    void rb_build(int nx);
+    void rb_build(int nx, bool msgs = true);  // msgs: also the colour-compact message buffers
+    void launch_gs_rb(const double* b, double* x);
     void launch_rb_sweep(const double* b, double* x, bool cold, bool delta, unsigned long long* dslot, int mode);
     void rb_state(bool to_compact, double2* natural);
     // cold smoothing with recorded lambda / sigma per sweep (multigrid smoother fast path)

@@ -191,6 +191,9 @@ struct bgmg {
                 L.launch_jacobi(b, x, L.d_e);
                 ck(cudaMemcpyAsync(x, L.d_e, sizeof(double) * L.n, cudaMemcpyDeviceToDevice, st), "copy");
             }
+        } else if (smoother == GsRB && L.rb_applicable(levels[k].sched)) {  // colour-compact coefficients
+            L.rb_build(levels[k].sched.nx, false);
+            for (int s = 0; s < sweeps; ++s) L.launch_gs_rb(b, x);
         } else {
             const Levels& lv = L.levels_for(levels[k].sched);
             for (int s = 0; s < sweeps; ++s) L.launch_gs_levels(lv, b, x);

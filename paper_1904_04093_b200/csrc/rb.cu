@@ -14,8 +14,11 @@ bool Engine::rb_applicable(const bgabp_schedule& s) const {
     return dia.off[0] == -s.nx && dia.off[1] == -1 && dia.off[2] == 1 && dia.off[3] == s.nx && dia.nneg == 2;
 }
 
-void Engine::rb_build(int nx) {
-    if (rb_ready && rb_nx == nx) return;
+void Engine::rb_build(int nx, bool msgs) {
+    if (rb_ready && rb_nx == nx) {
+        if (msgs && !d_rbmsg) d_rbmsg = static_cast<double2*>(dalloc(sizeof(double2) * 4 * (size_t)std::max(n, 2)));
+        return;
+    }
     const int nR = (n + 1) / 2, nB = n / 2;
     rb.nx = nx;
     rb.nR = nR;
@@ -42,9 +45,17 @@ void Engine::rb_build(int nx) {
     rb.rowv[1] = symmetric ? cB : rB;
     rb.diag[0] = dR;
     rb.diag[1] = dB;
-    if (!d_rbmsg) d_rbmsg = static_cast<double2*>(dalloc(sizeof(double2) * 4 * (size_t)std::max(n, 2)));
+    if (msgs && !d_rbmsg) d_rbmsg = static_cast<double2*>(dalloc(sizeof(double2) * 4 * (size_t)std::max(n, 2)));
     rb_nx = nx;
     rb_ready = true;
+}
+
+// one red-black Gauss-Seidel pass (classic.cpp:16-30 in red_black_grid order) on the
+// colour-compact coefficients: reds, then blacks, x in natural order, in place
+void Engine::launch_gs_rb(const double* b, double* x) {
+    if (n == 0) return;
+    k_gs_rb_half<0><<<nblk_host(rb.nR), 256, 0, st>>>(rb, b, x, d_ctrl);
+    if (rb.nB > 0) k_gs_rb_half<1><<<nblk_host(rb.nB), 256, 0, st>>>(rb, b, x, d_ctrl);
 }
 
 void Engine::launch_rb_sweep(const double* b, double* x, bool cold, bool delta, unsigned long long* dslot, int mode) {

@@ -94,6 +94,38 @@ static __global__ void __launch_bounds__(256) k_rb_half(RbP P, const double* __r
     if (DELTA) warp_max_commit(dslot, dmax);
 }
 
+// One colour of a red-black Gauss-Seidel pass (classic.cpp:16-30, gs_pass in red_black_grid
+// order): x_g = (b_g - sum_{k != g} A_gk x_k) / A_gg with the row in CSR column order.  Row
+// coefficients and the diagonal come from the colour-compact copies (coalesced); x stays in
+// natural order, where a warp's 32 nodes and their 64 horizontal neighbours share the same
+// 512 bytes.  Zero diagonal: the visit position (reds first, ascending) into opiv, like the level
+// kernel.
+template <int COLOUR>
+static __global__ void __launch_bounds__(256) k_gs_rb_half(RbP P, const double* __restrict__ b, double* x,
+                                                          Ctrl* ctrl) {
+    if (ctrl->opiv != kNone) return;
+    const int nc = COLOUR == 0 ? P.nR : P.nB, n = P.nR + P.nB;
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nc) return;
+    const int g = rb_nat(P, q, COLOUR);
+    const uint32_t mk = P.mask[COLOUR][q];
+    const int off[4] = {-P.nx, -1, 1, P.nx};
+    double cv[4], xv[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {  // every load up front; the mask selects the terms
+        const int k = g + off[s];
+        cv[s] = __ldg(P.rowv[COLOUR] + s * nc + q);
+        xv[s] = x[k < 0 ? 0 : (k >= n ? n - 1 : k)];
+    }
+    const double d = __ldg(P.diag[COLOUR] + q);
+    double acc = b[g];
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+        if (mk & (1u << s)) acc = dsub(acc, dmul(cv[s], xv[s]));
+    if (d == 0.0) atomicMin(&ctrl->opiv, (unsigned long long)(COLOUR == 0 ? q : P.nR + q) << 32);
+    x[g] = ddiv(acc, d);
+}
+
 // colour-split copies of the DIA arrays (natural slots -nx, -1, +1, +nx)
 static __global__ void k_rb_split(int n, int nR, int nx, const uint32_t* __restrict__ mask, const double* __restrict__ c,
                                   const double* __restrict__ rowv, const double* __restrict__ diag, uint32_t* mR,
@@ -171,17 +203,25 @@ static __global__ void __launch_bounds__(256) k_rb_mean_half(RbP P, const double
     if (q >= nc) return;
     const int g = rb_nat(P, q, COLOUR);
     const uint32_t mk = P.mask[COLOUR][q];
-    double acc = r[g], in[4];
+    // all loads issued before the mask is known (slot arrays are full size; the mask still
+    // selects every term): predicated loads wait for the mask's DRAM round trip first
+    double acc = r[g], in[4], lam[4];
 #pragma unroll
-    for (int s = 0; s < 4; ++s) in[s] = (!FIRST && (mk & (1u << s))) ? m_mine[s * nc + q] : 0.0;
+    for (int s = 0; s < 4; ++s) {
+        in[s] = FIRST ? 0.0 : m_mine[s * nc + q];
+        lam[s] = __ldg(lam_rec + s * nc + q);
+    }
+    const double sg = LAST ? __ldg(sig_rec + q) : 1.0;
+    const double xg = LAST ? x[g] : 0.0;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        if (!(mk & (1u << s))) in[s] = 0.0;
+        else acc = dadd(acc, in[s]);  // (adding a zero would turn acc = -0 into +0)
+    }
+    if (LAST) x[g] = dadd(xg, ddiv(acc, sg));
 #pragma unroll
     for (int s = 0; s < 4; ++s)
-        if (mk & (1u << s)) acc = dadd(acc, in[s]);
-    if (LAST) x[g] = dadd(x[g], ddiv(acc, sig_rec[q]));
-#pragma unroll
-    for (int s = 0; s < 4; ++s)
-        if (mk & (1u << (16 + s)))
-            m_other[(3 - s) * no + rb_other(g, s, P.nx)] = dmul(__ldg(lam_rec + s * nc + q), dsub(acc, in[s]));
+        if (mk & (1u << (16 + s))) m_other[(3 - s) * no + rb_other(g, s, P.nx)] = dmul(lam[s], dsub(acc, in[s]));
 }
 
 // message state natural DIA [4][n] <-> colour-compact ([4][nR] reds, then [4][nB] blacks)
