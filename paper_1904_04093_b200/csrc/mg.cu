@@ -217,7 +217,7 @@ struct bgmg {
         k_restrict<<<nblk_host(C.E->n), 256, 0, st>>>(L.d_r, levels[k].nx, C.d_b);
         ck(cudaMemsetAsync(C.d_x, 0, sizeof(double) * std::max(C.E->n, 1), st), "memset");
         cycle(k + 1, spec, C.d_b, C.d_x);
-        k_prolong_add<<<nblk_host(L.n), 256, 0, st>>>(C.d_x, C.nx, x, 0);
+        k_prolong_add<<<dim3(nblk_host(C.nx + 1), levels[k].nx), 256, 0, st>>>(C.d_x, C.nx, x, 0);
         smooth(k, b, x, spec.post, spec.frozen != 0);
     }
 
@@ -651,7 +651,7 @@ int bgmg_prolong(const double* coarse, int mc, double* out) {
         ck(cudaMalloc(&df, sizeof(double) * mf * mf), "malloc");
         ck(cudaMalloc(&dc, sizeof(double) * std::max(mc * mc, 1)), "malloc");
         if (mc > 0) ck(cudaMemcpy(dc, coarse, sizeof(double) * mc * mc, cudaMemcpyHostToDevice), "H2D");
-        k_prolong_add<<<nblk_host((long long)mf * mf), 256>>>(dc, mc, df, 1);
+        k_prolong_add<<<dim3(nblk_host(mc + 1), mf), 256>>>(dc, mc, df, 1);
         ck(cudaMemcpy(out, df, sizeof(double) * mf * mf, cudaMemcpyDeviceToHost), "D2H");
         cudaFree(df);
         cudaFree(dc);

@@ -362,6 +362,22 @@ static __global__ void __launch_bounds__(256) k_res_var(DiaP P, const double* __
         }
         if ((threadIdx.x & 31) == 0) rmax[(blockIdx.x * blockDim.x + threadIdx.x) >> 5] = bits;
     }
+    if (RED >= 6 && RED <= 7) {  // 6: block max to a per-block partial (plain store); 7: atomic into 1024 slots
+        __shared__ unsigned long long part2[8];
+        unsigned long long bits = __double_as_longlong(a);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long ot = __shfl_xor_sync(0xffffffffu, bits, o);
+            bits = ot > bits ? ot : bits;
+        }
+        if ((threadIdx.x & 31) == 0) part2[threadIdx.x >> 5] = bits;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int k = 1; k < 8; ++k) bits = part2[k] > bits ? part2[k] : bits;
+            if (RED == 6) rmax[blockIdx.x] = bits;
+            else if (bits) atomicMax(rmax + (blockIdx.x & 1023), bits);
+        }
+    }
     if (RED >= 3 && RED <= 4) {  // block max, then one fire-and-forget atomic (3: one word, 4: 64 block-indexed slots)
         __shared__ unsigned long long part[8];
         unsigned long long bits = __double_as_longlong(a);
@@ -425,6 +441,48 @@ static __global__ void __launch_bounds__(1024) k_fold_partials(const unsigned lo
         m = ot > m ? ot : m;
     }
     if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+// residual with PPT nodes per thread (block-strided), one block max + atomic at the end
+template <int S, int PPT>
+static __global__ void __launch_bounds__(256) k_res_ppt(DiaP P, const double* __restrict__ b,
+                                                        const double* __restrict__ x, double* __restrict__ r,
+                                                        unsigned long long* rmax) {
+    const int n = P.n;
+    const int j0 = blockIdx.x * blockDim.x * PPT + threadIdx.x;
+    double a = 0.0;
+    uint32_t mk[PPT];
+    double cv[PPT][S], xv[PPT][S], dj[PPT], xj[PPT], bj[PPT];
+#pragma unroll
+    for (int u = 0; u < PPT; ++u) {
+        const int j = min(j0 + u * (int)blockDim.x, n - 1);
+        mk[u] = P.mask[j];
+        dj[u] = P.diag[j];
+        xj[u] = x[j];
+        bj[u] = b[j];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const int q = j + P.off[s];
+            const int qc = q < 0 ? 0 : (q >= n ? n - 1 : q);
+            cv[u][s] = __ldg(s < P.nneg ? P.rowv + (size_t)P.rev[s] * n + qc : P.rowv + (size_t)s * n + j);
+            xv[u][s] = __ldg(x + qc);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < PPT; ++u) {
+        const int j = j0 + u * (int)blockDim.x;
+        if (j >= n) continue;
+        double acc = bj[u];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            if (s == P.nneg) acc = dsub(acc, dmul(dj[u], xj[u]));
+            if (mk[u] & (1u << s)) acc = dsub(acc, dmul(cv[u][s], xv[u][s]));
+        }
+        if (P.nneg == S) acc = dsub(acc, dmul(dj[u], xj[u]));
+        if (r) r[j] = acc;
+        a = fmax(a, nan_skip_abs(acc));
+    }
+    block_max_red(rmax, a);
 }
 }  // namespace bgabp
 
@@ -576,6 +634,16 @@ void run(int N) {
             k_res_var<S, true, true, 5><<<g, 256>>>(P, db, xr, rr, parts);
             k_fold_partials<<<148, 1024>>>(parts, np, spread);
         });
+        unsigned long long* bparts;
+        CK(cudaMalloc(&bparts, sizeof(unsigned long long) * (g + 1024)));
+        rt("var UNC, block partial store (no atomic)", [&] { k_res_var<S, true, true, 6><<<g, 256>>>(P, db, xr, rr, bparts); });
+        rt("var UNC, block atomic 1024 slots", [&] { k_res_var<S, true, true, 7><<<g, 256>>>(P, db, xr, rr, bparts); });
+        rt("var UNC, no reduction + k_inf_norm over r", [&] {
+            k_res_var<S, true, true, 0><<<g, 256>>>(P, db, xr, rr, spread);
+            k_inf_norm<<<1184, 256>>>(rr, n, spread);
+        });
+        rt("PPT=2 block RED", [&] { k_res_ppt<S, 2><<<(n + 511) / 512, 256>>>(P, db, xr, rr, spread); });
+        rt("PPT=4 block RED", [&] { k_res_ppt<S, 4><<<(n + 1023) / 1024, 256>>>(P, db, xr, rr, spread); });
         rt("var UNC, no reduction", [&] { k_res_var<S, true, true, 0><<<g, 256>>>(P, db, xr, rr, spread); });
         for (int gb : {148 * 4, 148 * 8, 148 * 16, 148 * 32})
             rt(gb == 592 ? "grid-stride UNC 592 blocks" : gb == 1184 ? "grid-stride UNC 1184 blocks" : gb == 2368 ? "grid-stride UNC 2368 blocks" : "grid-stride UNC 4736 blocks",
