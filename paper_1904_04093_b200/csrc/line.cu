@@ -150,10 +150,11 @@ void LineEngine::clear_fail() {
 void LineEngine::sweep(const double* b, int mode, double* x, const int* done) {
     if (n == 0) return;
     const int c = cur, o = mode == 1 ? cur ^ 1 : cur;  // flood writes the other buffer
-    k_line_phase<true><<<lblk(ny, 32), 32, 0, st>>>(P, b, lc[c], mc[c], lr[o], mr[o], nullptr, d_fd, d_fy, d_fail,
-                                                    done);
-    k_line_phase<false><<<lblk(nx, 32), 32, 0, st>>>(P, b, mode == 1 ? lr[c] : lr[o], mode == 1 ? mr[c] : mr[o],
-                                                     lc[o], mc[o], x, d_fd, d_fy, d_fail, done);
+    k_line_full_rows<false><<<lblk(ny, 4), 128, 0, st>>>(P, b, lc[c], mc[c], lr[o], mr[o], d_fd, d_fy, d_fail, done,
+                                                         LineRec{});
+    k_line_full_cols<false><<<lblk(nx, kFCW), kFCT, 0, st>>>(P, b, mode == 1 ? lr[c] : lr[o],
+                                                             mode == 1 ? mr[c] : mr[o], lc[o], mc[o], x, d_fd, d_fy,
+                                                             d_fail, done, LineRec{});
     cur = o;
     ck(cudaGetLastError(), "line sweep");
 }
@@ -177,10 +178,10 @@ bool LineEngine::record(int sweeps) {
     reset_state();
     clear_fail();
     for (int s = 0; s < sweeps; ++s) {  // sequential mode: rows then columns, in place
-        k_line_phase<true, true><<<lblk(ny, 32), 32, 0, st>>>(P, d_b, lc[0], mc[0], lr[0], mr[0], nullptr, d_fd, d_fy,
-                                                             d_fail, nullptr, rec_rows[s]);
-        k_line_phase<false, true><<<lblk(nx, 32), 32, 0, st>>>(P, d_b, lr[0], mr[0], lc[0], mc[0], nullptr, d_fd,
-                                                              d_fy, d_fail, nullptr, rec_cols[s]);
+        k_line_full_rows<true><<<lblk(ny, 4), 128, 0, st>>>(P, d_b, lc[0], mc[0], lr[0], mr[0], d_fd, d_fy, d_fail,
+                                                            nullptr, rec_rows[s]);
+        k_line_full_cols<true><<<lblk(nx, kFCW), kFCT, 0, st>>>(P, d_b, lr[0], mr[0], lc[0], mc[0], nullptr, d_fd,
+                                                               d_fy, d_fail, nullptr, rec_cols[s]);
     }
     ck(cudaGetLastError(), "line record");
     if (read_fail() != kNone) {
