@@ -542,7 +542,9 @@ void Engine::launch_residual(const double* b, const double* x, double* r, unsign
     if (n == 0) return;
     const unsigned g = nblk(n);
     if (layout == BGABP_LAYOUT_DIA) {
-        if (symmetric) {
+        if (dia.uniform) {
+            DIA_SWITCH(S, k_residual_dia<SS, true, true><<<g, 256, 0, st>>>(dia, b, x, r, rmax, d_ctrl, mode));
+        } else if (symmetric) {
             DIA_SWITCH(S, k_residual_dia<SS, true><<<g, 256, 0, st>>>(dia, b, x, r, rmax, d_ctrl, mode));
         } else {
             DIA_SWITCH(S, k_residual_dia<SS><<<g, 256, 0, st>>>(dia, b, x, r, rmax, d_ctrl, mode));

@@ -45,6 +45,9 @@ void Engine::rb_build(int nx, bool msgs) {
     rb.rowv[1] = symmetric ? cB : rB;
     rb.diag[0] = dR;
     rb.diag[1] = dB;
+    rb.uniform = dia.uniform;
+    for (int s = 0; s < 4; ++s) rb.cu[s] = dia.cu[s];
+    rb.du = dia.du;
     if (msgs && !d_rbmsg) d_rbmsg = static_cast<double2*>(dalloc(sizeof(double2) * 4 * (size_t)std::max(n, 2)));
     rb_nx = nx;
     rb_ready = true;
@@ -63,6 +66,14 @@ void Engine::launch_rb_sweep(const double* b, double* x, bool cold, bool delta, 
     double2* mR = d_rbmsg;
     double2* mB = d_rbmsg + 4 * (size_t)rb.nR;
     const unsigned gr = nblk_host(rb.nR), gb = nblk_host(std::max(rb.nB, 1));
+    if (rb.uniform && !delta) {  // constant stencil: no coefficient / diagonal loads
+        if (cold)
+            k_rb_half<0, true, false, true><<<gr, 256, 0, st>>>(rb, b, mR, mB, x, d_ctrl, dslot, mode);
+        else
+            k_rb_half<0, false, false, true><<<gr, 256, 0, st>>>(rb, b, mR, mB, x, d_ctrl, dslot, mode);
+        if (rb.nB > 0) k_rb_half<1, false, false, true><<<gb, 256, 0, st>>>(rb, b, mB, mR, x, d_ctrl, dslot, mode);
+        return;
+    }
     if (delta) {
         if (cold)
             k_rb_half<0, true, true><<<gr, 256, 0, st>>>(rb, b, mR, mB, x, d_ctrl, dslot, mode);

@@ -23,6 +23,8 @@ struct RbP {
     const double* c[2];       // [colour][4][n_c] A_{k,j} of the node's outgoing message per slot
     const double* rowv[2];    // [colour][4][n_c] A_{j,k} (residual / GS), == c if symmetric
     const double* diag[2];    // [colour][n_c]
+    int uniform;              // constant stencil (DiaP::uniform): cu / du replace c / diag
+    double cu[4], du;
 };
 
 // Even nx: natural pair (2q, 2q+1) lies in one row and holds one red and one black node, so the
@@ -41,7 +43,7 @@ __device__ __forceinline__ int rb_other(int g, int s, int nx) {
 
 // One colour phase of a red-black sweep.  COLD: first sweep of a cold start on the red phase
 // (every in-message is still zero, so none is read and no buffer has to be cleared).
-template <int COLOUR, bool COLD, bool DELTA>
+template <int COLOUR, bool COLD, bool DELTA, bool UNIF = false>
 static __global__ void __launch_bounds__(256) k_rb_half(RbP P, const double* __restrict__ b, double2* mine,
                                                        double2* other, double* __restrict__ x, Ctrl* ctrl,
                                                        unsigned long long* dslot, int mode) {
@@ -53,7 +55,7 @@ static __global__ void __launch_bounds__(256) k_rb_half(RbP P, const double* __r
     if (q < nc) {
         const int g = rb_nat(P, q, COLOUR);
         const uint32_t mk = P.mask[COLOUR][q];
-        const double dj = P.diag[COLOUR][q];
+        const double dj = UNIF ? P.du : P.diag[COLOUR][q];
         double sig = 0.0, acc = b[g];
         double2 in[4];
         double cc[4];
@@ -62,7 +64,7 @@ static __global__ void __launch_bounds__(256) k_rb_half(RbP P, const double* __r
             in[s] = make_double2(0.0, 0.0);
             cc[s] = 0.0;
             if (!COLD && (mk & (1u << s))) in[s] = mine[s * nc + q];
-            if (mk & (1u << (16 + s))) cc[s] = __ldg(P.c[COLOUR] + s * nc + q);
+            if (mk & (1u << (16 + s))) cc[s] = UNIF ? P.cu[s] : __ldg(P.c[COLOUR] + s * nc + q);
         }
 #pragma unroll
         for (int s = 0; s < 4; ++s) {
