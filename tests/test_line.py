@@ -230,6 +230,27 @@ def test_gpu_line_sweep_from_the_same_state(orc, nx, ny, seed, mode):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("mode", [0, 1])
+def test_gpu_line_sweep_long_lines(orc, mode):
+    """Rows longer than one 128-node warp tile and columns cut into many segments, so the scan
+    carries between tiles and between segments are exercised (nonsymmetric, from the same state)."""
+    nx, ny, seed = 160, 140, 7
+    A = _scaled_grid(orc, nx, ny, seed)
+    b = np.random.RandomState(seed).uniform(-1, 1, A.n)
+    R = orc.region(A, orc.grid_lines(nx, ny))
+    D = g.LineGabpEngine(g.SparseMatrix.of(A), nx, ny)
+    lr, mr = R.make_state()
+    xr = np.zeros(A.n)
+    for k in range(3):
+        ld, md, xd = lr.copy(), mr.copy(), xr.copy()
+        assert R.sweep(b, lr, mr, xr, mode)[0]
+        assert D.sweep(b, ld, md, xd, mode)[0]
+        _close(ld, lr, f"Lambda of sweep {k + 1}", RTOL_SWEEP)
+        _close(md, mr, f"m of sweep {k + 1}", RTOL_SWEEP)
+        _close(xd, xr, f"x of sweep {k + 1}", RTOL_SWEEP)
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("nx,ny", [(6, 6), (31, 17), (64, 64)])
 @pytest.mark.parametrize("mode", [0, 1])
 def test_gpu_line_sweeps_free_running(orc, nx, ny, mode):
