@@ -92,6 +92,11 @@ int bgabp_create(int n, const int* row_offsets, const int* col_indices, const do
                  int layout, bgabp_engine** out, char* err, size_t errlen);
 void bgabp_destroy(bgabp_engine* e);
 int bgabp_get_info(const bgabp_engine* e, bgabp_info* info);
+/* diagnostic: FNV-1a digest of the device layout (DIA mask/coefficients/diagonal, the CSR-position
+ * slot map) and of the facts derived from it.  The layout is built by kernels from the uploaded
+ * CSR; with the environment variable BGABP_HOST_BUILD set it is built on the host instead, and
+ * the two digests of one matrix must be equal. */
+int bgabp_layout_digest(bgabp_engine* e, unsigned long long* out);
 /* the handle's CUDA stream (cudaStream_t), for callers that time or order work around it */
 void* bgabp_stream(bgabp_engine* e);
 

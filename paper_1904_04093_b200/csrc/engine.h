@@ -63,9 +63,14 @@ struct Engine {
     Ctrl* d_ctrl = nullptr;
     Ctrl* h_ctrl = nullptr;
     long long* d_csr2slot = nullptr;
-    void ensure_csr2slot() {
-        if (!d_csr2slot && nnz > 0) d_csr2slot = upload(csr2slot);
-    }
+    void ensure_csr2slot();
+    // the matrix in HBM (canonical CSR); the host copies above exist once host_ready is set
+    int* d_ro = nullptr;
+    int* d_ci = nullptr;
+    double* d_val = nullptr;
+    bool host_ready = false;
+    void ensure_host();  // ro/ci/val/tpos/uptr/unbr from the device CSR, on first use
+
     double2* d_msg[2] = {nullptr, nullptr};
     int cur = 0;
     double *d_b = nullptr, *d_x = nullptr, *d_r = nullptr, *d_e = nullptr, *d_aux = nullptr;
@@ -97,12 +102,19 @@ struct Engine {
 
     ~Engine();
     void* dalloc(size_t bytes);
+    void dfree(void* p);
     template <class T>
     T* upload(const std::vector<T>& v);
 
     void build(int n, const int* ro, const int* ci, const double* v, int layout,
                cudaStream_t shared_stream = nullptr);
-    std::vector<int> schedule_order(const bgabp_schedule& s) const;
+    void build_dia_device(const int* ro, const int* ci, const double* v);
+    void build_dia_host();
+    void build_ucsr_host();
+    void host_graph(const int* ro, const int* ci, const double* v);
+    void upload_host(void* dst, const void* src, size_t bytes);
+    long long find_pos(int r, int c) const;
+    std::vector<int> schedule_order(const bgabp_schedule& s);
     // validates the schedule (reference exceptions) and caches its levels
     void schedule_order_check(const bgabp_schedule& s) {
         if (s.kind != BGABP_SCHED_FLOOD) (void)levels_for(s);

@@ -6,6 +6,8 @@
 // precomputed inverse (host partial-pivot LU at setup, device GEMV per cycle) in place of the
 // reference's Eigen PartialPivLU; only that solve's rounding differs from the reference.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -36,7 +38,8 @@ struct MgLevel {
 };
 
 // dense partial-pivot LU + explicit inverse of the coarsest operator (host, setup only)
-std::vector<double> dense_inverse(const Engine& E) {
+std::vector<double> dense_inverse(Engine& E) {
+    E.ensure_host();
     const int n = E.n;
     std::vector<double> a((size_t)n * n, 0.0), inv((size_t)n * n, 0.0);
     for (int i = 0; i < n; ++i)
@@ -51,6 +54,8 @@ std::vector<double> dense_inverse(const Engine& E) {
             for (int c = 0; c < n; ++c) std::swap(a[(size_t)k * n + c], a[(size_t)best * n + c]);
         const double d = a[(size_t)k * n + k];
         if (d == 0.0) continue;
+        // rows are independent: the same operations per element as the serial loop
+#pragma omp parallel for schedule(static) if (n - k > 64)
         for (int i = k + 1; i < n; ++i) {
             double& l = a[(size_t)i * n + k];
             l /= d;
@@ -58,9 +63,9 @@ std::vector<double> dense_inverse(const Engine& E) {
                 for (int c = k + 1; c < n; ++c) a[(size_t)i * n + c] -= l * a[(size_t)k * n + c];
         }
     }
-    std::vector<double> y(n);
+#pragma omp parallel for schedule(dynamic, 8)
     for (int col = 0; col < n; ++col) {
-        std::fill(y.begin(), y.end(), 0.0);
+        std::vector<double> y(n, 0.0);
         y[col] = 1.0;
         for (int k = 0; k < n; ++k)
             if (piv[k] != k) std::swap(y[k], y[piv[k]]);
@@ -451,6 +456,16 @@ static bgabp_schedule schedule_for(int sm, int nx) {  // multigrid.cpp:25-32
 // Hierarchy ctor (multigrid.cpp:74-109) over caller-supplied levels
 static void build_hierarchy(bgmg* h, int nlevels, const int* n, const int* const* ro, const int* const* ci,
                             const double* const* v, const int* nx, int smoother) {
+    const bool timing = std::getenv("BGABP_TIMING") != nullptr;
+    auto t_last = std::chrono::steady_clock::now();
+    auto phase = [&](const char* what, int k) {
+        if (!timing) return;
+        ck(cudaStreamSynchronize(h->st), "sync");
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[mg] %-22s level %d %8.1f ms\n", what, k,
+                     std::chrono::duration<double, std::milli>(now - t_last).count());
+        t_last = now;
+    };
     if (nlevels < 1) throw InvalidArg("Hierarchy: need 1 <= J2 and a coarsest exponent >= 1");
     if (!supported(smoother)) throw InvalidArg("Hierarchy: unsupported smoother " + std::to_string(smoother));
     h->smoother = smoother;
@@ -474,6 +489,7 @@ static void build_hierarchy(bgmg* h, int nlevels, const int* n, const int* const
             L.d_x = static_cast<double*>(L.E->dalloc(sizeof(double) * std::max(n[k], 1)));
         }
         h->levels.push_back(std::move(L));
+        phase("engine build", k);
     }
     if (is_gabp(smoother)) {
         for (int k = 0; k < (int)h->levels.size(); ++k) {
@@ -482,6 +498,7 @@ static void build_hierarchy(bgmg* h, int nlevels, const int* n, const int* const
                 h->levels.resize(k + 1);
                 break;
             }
+            phase("sweeps_expand probe", k);
             // multigrid.cpp:94-95 computes the frozen precisions here for every level it keeps
             // before a truncation; they are only read by frozen cycles and level_frozen_ok, so
             // they are computed on first use (bgmg::ensure_frozen) with the same values
@@ -497,6 +514,7 @@ static void build_hierarchy(bgmg* h, int nlevels, const int* n, const int* const
     if (const char* e = std::getenv("BGABP_MG_GRAPH")) h->use_graphs = std::atoi(e) != 0;
     Engine& C = *h->levels.back().E;
     std::vector<double> inv = dense_inverse(C);
+    phase("coarse inverse", (int)h->levels.size() - 1);
     ck(cudaMalloc(&h->d_inv, sizeof(double) * std::max<size_t>(inv.size(), 1)), "malloc");
     if (!inv.empty())
         ck(cudaMemcpyAsync(h->d_inv, inv.data(), sizeof(double) * inv.size(), cudaMemcpyHostToDevice, h->st), "H2D");

@@ -76,6 +76,7 @@ def lib():
             "bgabp_destroy": (None, [_vp]),
             "bgabp_get_info": (C.c_int, [_vp, C.POINTER(_Info)]),
             "bgabp_stream": (_vp, [_vp]),
+            "bgabp_layout_digest": (C.c_int, [_vp, C.POINTER(C.c_ulonglong)]),
             "bgabp_reset_state": (C.c_int, [_vp]),
             "bgabp_set_state": (C.c_int, [_vp, _dp, _dp]),
             "bgabp_get_state": (C.c_int, [_vp, _dp, _dp]),
@@ -355,6 +356,12 @@ class GabpEngine:
 
     def stream(self):
         return lib().bgabp_stream(self._h)
+
+    def layout_digest(self) -> int:
+        """FNV-1a digest of the device layout (diagnostic; see bgabp_layout_digest)."""
+        out = C.c_ulonglong(0)
+        _raise(lib().bgabp_layout_digest(self._h, C.byref(out)), "layout digest")
+        return int(out.value)
 
     def make_state(self) -> MessageState:
         return MessageState(np.zeros(self.A.nnz), np.zeros(self.A.nnz))
