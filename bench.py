@@ -332,6 +332,10 @@ def run_gpu(args, world, rank, local):
             "gpu_launches": 2 * args.steps, "clocks": clk.summary()}
     if tts is not None:
         line["solve"] = tts
+    if args.config == 2 and not args.no_tts and rank == 0:
+        del eng
+        torch.cuda.synchronize()
+        line["time_to_solution"] = time_to_solution(g, torch, args)
     if schedules:
         line["schedules"] = schedules  # same system, sweep + residual + stop test per iteration
     if args.config != 2:
@@ -346,6 +350,49 @@ def run_gpu(args, world, rank, local):
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "unavailable", "sample": str(ex)}
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def time_to_solution(g, torch, args):
+    """The metric's 'time to residual 1e-8' on the configs that reach it, through the public API
+    with host buffers, setup (engine / hierarchy build from host CSR) included:
+    config 3 (nonsymmetric GaBP, bgabp_solve) and config 5 (V(2,2) red-black GaBP, bgmg_solve).
+    Config 2's flood solve needs ~6.7M sweeps and stops at the 20000 cap."""
+    out = {}
+    P3 = g.config_problem(3)
+    tol3 = 1e-8 * float(np.abs(P3.b).max())
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e3 = g.GabpEngine(P3.A)
+    torch.cuda.synchronize()
+    setup = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    rep = e3.solve(P3.b, g.Schedule.parallel_flood(), g.GabpOptions(tol=tol3, max_iter=20000))
+    dt = time.perf_counter() - t0
+    out["config3_nonsymmetric_gabp"] = {
+        "status": rep.status.name, "iterations": rep.iterations, "setup_seconds": setup, "solve_seconds": dt,
+        "time_to_solution_seconds": setup + dt,
+        "final_rel_residual": float(rep.residual_history[-1] / np.abs(P3.b).max())}
+    del e3
+    for sigma in (1.0, 2.0):
+        levels, b = _mg_levels(g, args.mg_J, sigma)
+        tol = 1e-8 * float(np.abs(b).max())
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        h = g.Hierarchy.from_levels([p.A for p in levels], [p.nx for p in levels], g.MgSmoother.GabpRedBlack)
+        torch.cuda.synchronize()
+        setup = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        rep = g.mg_solve(h, g.CycleSpec(2, 2, g.MgSmoother.GabpRedBlack), b,
+                         g.MgSolveOptions(tol=tol, max_cycles=args.mg_cycles))
+        dt = time.perf_counter() - t0
+        out[f"config5_mg_v22_gabp_red_black_sigma{sigma:g}"] = {
+            "status": rep.status.name, "cycles": rep.iterations, "levels": h.num_levels(), "setup_seconds": setup,
+            "solve_seconds": dt, "time_to_solution_seconds": setup + dt,
+            "final_rel_residual": float(rep.residual_history[-1] / np.abs(b).max()),
+            "note": ("as specified (sigma 2): diverges, as the reference's own V-cycle does (DESIGN.md 6)"
+                     if sigma == 2.0 else "sigma 1: same recipe with milder contrast, converges")}
+        del h, levels
+    return out
 
 
 # ------------------------------------------------------------------------------------------------
@@ -458,6 +505,7 @@ def main():
     ap.add_argument("--ref-iters", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-schedules", action="store_true", help="skip the red-black / sequential timings")
+    ap.add_argument("--no-tts", action="store_true", help="skip the time-to-1e-8 runs (configs 3 and 5)")
     ap.add_argument("--mg-J", type=int, default=12)
     ap.add_argument("--mg-cycles", type=int, default=100)
     ap.add_argument("--mg-cpu-J", type=int, default=9)

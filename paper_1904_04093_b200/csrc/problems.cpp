@@ -329,7 +329,7 @@ Config5Field& config5_field(int J, unsigned seed, double sigma, int levels) {
 }
 
 bgabp_problem* varcoef2d_problem(int Jf, int k, unsigned seed, double sigma) {
-    Config5Field& F = config5_field(Jf, seed, sigma, k + 1);
+    Config5Field& F = config5_field(Jf, seed, sigma, Jf);  // every level at once: later calls hit the cache
     if ((int)F.logK.size() <= k) throw std::invalid_argument("config 5: level below the coarsest grid");
     const int J = Jf - k, m = (1 << J) - 1;
     const double h = 1.0 / (1 << J), inv_h2 = 1.0 / (h * h);
