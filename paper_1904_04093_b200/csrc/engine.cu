@@ -853,6 +853,18 @@ void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bga
                          const double* r0_override) {
     solve_flood = s.kind == BGABP_SCHED_FLOOD;
     solve_fused = solve_flood && layout == BGABP_LAYOUT_DIA;
+    {
+        const char* e = std::getenv("BGABP_FLOOD2");
+        const bool sharded = dia.j0 != 0 || dia.j1 != n || dia.gofs != 0;
+        // opt-in (BGABP_FLOOD2=1): bit-identical and half the DRAM traffic per iteration, but
+        // latency-bound at 168 registers / 12 warps per SM -- on par with the one-iteration step
+        // on the B200, so the one-iteration step stays the default
+        solve_double = solve_fused && grid5 && !sharded && o.stop == BGABP_STOP_RESIDUAL && e && std::atoi(e) != 0;
+        if (const char* hh = std::getenv("BGABP_FLOOD2_H")) flood2_h = std::max(1, std::atoi(hh));
+        if (const char* e2 = std::getenv("BGABP_FLOOD2_ST")) flood2_st = std::atoi(e2) == 3 ? 3 : 4;
+        if (const char* e3 = std::getenv("BGABP_FLOOD2_MINB")) flood2_minb = std::atoi(e3);
+        if (solve_double) enqueue_double_kernel(true);
+    }
     solve_levels = solve_flood ? nullptr : &levels_for(s);
     solve_rb = !solve_flood && rb_applicable(s);
     solve_seq = !solve_flood && !solve_rb && seq_applicable(s);
@@ -875,8 +887,9 @@ void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bga
         ck(cudaMemsetAsync(d_msg[k], 0, sizeof(double2) * (size_t)std::max<long long>(nslots, 1), st), "memset");
     ck(cudaMemsetAsync(d_x, 0, sizeof(double) * std::max(n, 1), st), "memset x");
     if (solve_fused) {
-        if (!d_xf) d_xf = static_cast<double*>(dalloc(sizeof(double) * kXRing * (size_t)std::max(n, 1)));
-        ck(cudaMemsetAsync(d_xf, 0, sizeof(double) * kXRing * (size_t)std::max(n, 1), st), "memset x ring");
+        // kXRing2 slots: the two-iteration launch keeps x(k) in slot k % 4 (single steps use 0, 1)
+        if (!d_xf) d_xf = static_cast<double*>(dalloc(sizeof(double) * kXRing2 * (size_t)std::max(n, 1)));
+        ck(cudaMemsetAsync(d_xf, 0, sizeof(double) * kXRing2 * (size_t)std::max(n, 1), st), "memset x ring");
     }
     ck(cudaMemsetAsync(d_spread, 0, sizeof(unsigned long long) * 8 * kSpread, st), "memset");
     if (solve_rb) ck(cudaMemsetAsync(d_rbmsg, 0, sizeof(double2) * 4 * (size_t)std::max(n, 2), st), "memset");
@@ -902,6 +915,12 @@ void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bga
 }
 
 void Engine::enqueue_step() {
+    if (solve_double) {  // iterations t and t+1, then their decisions in order
+        enqueue_double_kernel();
+        k_solve_decide_lag2<<<1, kSpread, 0, st>>>(d_ctrl, d_hist, d_spread);
+        k_solve_decide_lag2<<<1, kSpread, 0, st>>>(d_ctrl, d_hist, d_spread);
+        return;
+    }
     if (solve_fused) {
         enqueue_fused_kernel();
         k_solve_decide_lag2<<<1, kSpread, 0, st>>>(d_ctrl, d_hist, d_spread);
@@ -952,6 +971,40 @@ void Engine::enqueue_fused_kernel() {
     }
 }
 
+template <bool UNIF, bool SYM, int TPB, int MINB, int ST>
+static void launch_flood2(const DiaP& dia, int nx, int ny, int H, const double* b, double2* m0, double2* m1, double* xf,
+                          Ctrl* ctrl, unsigned long long* spread, cudaStream_t st) {
+    const size_t smem = sizeof(Stage5<UNIF, SYM, TPB, ST>);
+    if (!b) {  // attribute pass (solve_begin, outside any stream capture)
+        ck(cudaFuncSetAttribute(k_flood2_grid5<UNIF, SYM, TPB, MINB, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem),
+           "flood2 smem");
+        return;
+    }
+    const dim3 grid((unsigned)((nx + TPB - 5) / (TPB - 4)), (unsigned)((ny + H - 1) / H));
+    k_flood2_grid5<UNIF, SYM, TPB, MINB, ST><<<grid, TPB, smem, st>>>(dia, nx, ny, H, b, m0, m1, xf, ctrl, spread);
+}
+
+void Engine::enqueue_double_kernel(bool attr_only) {
+    constexpr int TPB = 128;
+    const int nx = grid5_nx, ny = n / std::max(grid5_nx, 1);
+    const double* bb = attr_only ? nullptr : solve_b;
+    if (timed_events) ck(cudaEventRecord((*timed_events)[2 * timed_index], st), "event");
+    if (dia.uniform && flood2_st == 3 && flood2_minb == 3)
+        launch_flood2<true, true, TPB, 3, 3>(dia, nx, ny, flood2_h, bb, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread, st);
+    else if (dia.uniform && flood2_st == 3)
+        launch_flood2<true, true, TPB, 4, 3>(dia, nx, ny, flood2_h, bb, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread, st);
+    else if (dia.uniform)
+        launch_flood2<true, true, TPB, 3, 4>(dia, nx, ny, flood2_h, bb, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread, st);
+    else if (symmetric)
+        launch_flood2<false, true, TPB, 3, 4>(dia, nx, ny, flood2_h, bb, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread, st);
+    else
+        launch_flood2<false, false, TPB, 2, 4>(dia, nx, ny, flood2_h, bb, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread,
+                                               st);
+    ck(cudaGetLastError(), "flood2");
+    if (timed_events) ck(cudaEventRecord((*timed_events)[2 * timed_index + 1], st), "event");
+}
+
 void Engine::enqueue_step_other() {
     if (solve_flood) {
         if (timed_events) ck(cudaEventRecord((*timed_events)[2 * timed_index], st), "event");
@@ -989,13 +1042,16 @@ void Engine::solve_steps(int nsteps) {
     }
     // graph-replay chunks of iterations: the kernels read their step index from the device,
     // so one captured chunk is valid for any position in the loop
-    const size_t per_step = solve_fused ? 2 : solve_flood ? 3 : solve_levels->ptr.size() + 1;
+    const int per_call = solve_double ? 2 : 1;  // iterations per enqueue_step
+    if (solve_double) nsteps = (nsteps + 1) / 2;  // enqueue_step calls
+    const size_t per_step = solve_double ? 3 : solve_fused ? 2 : solve_flood ? 3 : solve_levels->ptr.size() + 1;
     const bool use_graph = per_step * 16 <= 4096 && n > 0 && !solve_seq;  // cooperative launches stay out of graphs
     int left = nsteps;
     while (left > 0) {
         const int chunk = use_graph ? std::min(left, 16) : left;
         if (use_graph && chunk == 16) {
-            const std::string key = std::string(solve_fused ? "F" : solve_flood ? "f" : "o") + std::to_string(solve_stop) + ":" +
+            const std::string key = std::string(solve_double ? "D" : solve_fused ? "F" : solve_flood ? "f" : "o") +
+                                    std::to_string(solve_stop) + ":" + std::to_string(flood2_h) + ":" +
                                     std::to_string((long long)(uintptr_t)solve_b) + ":" +
                                     std::to_string((long long)(uintptr_t)solve_levels);
             auto it = graphs.find(key);
@@ -1014,7 +1070,7 @@ void Engine::solve_steps(int nsteps) {
             for (int k = 0; k < chunk; ++k) enqueue_step();
         }
         left -= chunk;
-        steps_enqueued += chunk;
+        steps_enqueued += (long long)chunk * per_call;
     }
     ck(cudaGetLastError(), "solve steps");
 }
@@ -1034,7 +1090,7 @@ void Engine::solve_run_to_end() {
     }
     read_ctrl();
     if (h_ctrl->done) return;
-    const long long total = (long long)solve_max_iter + (solve_fused ? 2 : 1);
+    const long long total = (long long)solve_max_iter + (solve_double ? 3 : solve_fused ? 2 : 1);
     int chunk = 16, inflight = 0, oldest = 0;
     while (true) {
         while (inflight < 2 && steps_enqueued < total) {
@@ -1101,10 +1157,11 @@ const double* Engine::solve_x() {
     }
     if (!solve_fused) return d_x;
     const Ctrl& c = *h_ctrl;  // read by solve_report
-    const double* xs = xslot(d_xf, n, c.solx);
+    const int ring = solve_double ? kXRing2 : kXRing;
+    const double* xs = d_xf + (size_t)(c.solx & (ring - 1)) * n;
     if (c.status == BGABP_DIVERGED && c.detail_kind == 1 && n > 0) {
         // the reference stops its x-stage at the pivot node: x(k) below it, x(k-1) from it on
-        const double* xo = xslot(d_xf, n, c.solx - 1);
+        const double* xo = d_xf + (size_t)((c.solx - 1) & (ring - 1)) * n;
         k_compose_pivot_x<<<nblk(n), 256, 0, st>>>(xs, xo, d_aux, n, (long long)c.detail_key - dia.gofs);
         ck(cudaGetLastError(), "compose x");
         return d_aux;
@@ -1577,11 +1634,12 @@ int bgabp_solve_device_end(bgabp_engine* h, bgabp_report* rep, double* x_dev, do
 int bgabp_solve_device_steps_timed(bgabp_engine* h, int nsteps, double* hot_ms) {
     ABI_GUARD(nullptr, 0, {
         Engine& E = h->E;
-        std::vector<cudaEvent_t> ev(2 * (size_t)std::max(nsteps, 0));
+        // one event pair per launch; a two-iteration launch covers two of the nsteps iterations
+        const int launches = E.solve_double ? (nsteps + 1) / 2 : nsteps;
+        std::vector<cudaEvent_t> ev(2 * (size_t)std::max(launches, 0));
         for (auto& e : ev) ck(cudaEventCreate(&e), "event");
         E.timed_events = &ev;
-        const int launches = nsteps;
-        for (int k = 0; k < nsteps; ++k) {
+        for (int k = 0; k < launches; ++k) {
             E.timed_index = k;
             E.enqueue_step();
         }
@@ -1595,7 +1653,7 @@ int bgabp_solve_device_steps_timed(bgabp_engine* h, int nsteps, double* hot_ms) 
             total += ms;
         }
         for (auto& e : ev) cudaEventDestroy(e);
-        E.steps_enqueued += nsteps;
+        E.steps_enqueued += (long long)launches * (E.solve_double ? 2 : 1);
         *hot_ms = total;
         return BGABP_OK;
     })

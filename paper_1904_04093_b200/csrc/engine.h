@@ -12,6 +12,7 @@
 
 #include "../../include/gabp_b200.h"
 #include "kernels.cuh"
+#include "flood2_kernels.cuh"
 #include "rb_kernels.cuh"
 #include "seq_kernels.cuh"
 #include "seqpipe_kernels.cuh"
@@ -89,6 +90,11 @@ struct Engine {
     // device-resident solve loop
     bool solve_flood = true;
     bool solve_fused = false;
+    bool solve_double = false;  // fused flood solve, two iterations per launch (flood2_kernels.cuh)
+    int flood2_h = 80;          // tile rows of k_flood2_grid5 (2048^2: 17 x 26 tiles = one wave at 3 per SM)
+    int flood2_st = 3;          // staged rows (cp.async pipeline depth + 1)
+    int flood2_minb = 3;        // resident blocks the uniform variant is compiled for
+    void enqueue_double_kernel(bool attr_only = false);
     const Levels* solve_levels = nullptr;
     bool solve_rb = false;
     bool solve_seq = false;
