@@ -1875,7 +1875,7 @@ int bgabp_shard_step_decide(bgabp_engine* h) {
 void* bgabp_shard_msg(bgabp_engine* h, int which) { return (void*)h->E.d_msg[which & 1]; }
 void* bgabp_shard_x(bgabp_engine* h, int which) {  // the slot holding x(which)
     Engine& E = h->E;
-    if (!E.d_xf) E.d_xf = static_cast<double*>(E.dalloc(sizeof(double) * kXRing * (size_t)std::max(E.n, 1)));
+    if (!E.d_xf) E.d_xf = static_cast<double*>(E.dalloc(sizeof(double) * kXRing2 * (size_t)std::max(E.n, 1)));
     return (void*)xslot(E.d_xf, E.n, which);
 }
 
