@@ -861,8 +861,10 @@ void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bga
         // on the B200, so the one-iteration step stays the default
         solve_double = solve_fused && grid5 && !sharded && o.stop == BGABP_STOP_RESIDUAL && e && std::atoi(e) != 0;
         if (const char* hh = std::getenv("BGABP_FLOOD2_H")) flood2_h = std::max(1, std::atoi(hh));
-        if (const char* e2 = std::getenv("BGABP_FLOOD2_ST")) flood2_st = std::atoi(e2) == 3 ? 3 : 4;
+        if (const char* e2 = std::getenv("BGABP_FLOOD2_ST")) flood2_st = std::min(5, std::max(3, std::atoi(e2)));
         if (const char* e3 = std::getenv("BGABP_FLOOD2_MINB")) flood2_minb = std::atoi(e3);
+        if (const char* e4 = std::getenv("BGABP_FLOOD2_KIND")) flood2_band = std::string(e4) == "band";
+        if (const char* e5 = std::getenv("BGABP_FLOOD2_R")) flood2_r = std::atoi(e5);
         if (solve_double) enqueue_double_kernel(true);
     }
     solve_levels = solve_flood ? nullptr : &levels_for(s);
@@ -985,15 +987,49 @@ static void launch_flood2(const DiaP& dia, int nx, int ny, int H, const double* 
     k_flood2_grid5<UNIF, SYM, TPB, MINB, ST><<<grid, TPB, smem, st>>>(dia, nx, ny, H, b, m0, m1, xf, ctrl, spread);
 }
 
+template <bool UNIF, bool SYM, int R, int MINB>
+static void launch_flood2b(const DiaP& dia, int nx, int ny, int H, const double* b, double2* m0, double2* m1,
+                           double* xf, Ctrl* ctrl, unsigned long long* spread, cudaStream_t st) {
+    const size_t smem = sizeof(Band5Smem<UNIF, SYM, R>);
+    if (!b) {  // attribute pass (solve_begin, outside any stream capture)
+        ck(cudaFuncSetAttribute(k_flood2b_grid5<UNIF, SYM, R, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem),
+           "flood2b smem");
+        return;
+    }
+    const dim3 grid((unsigned)((nx + 123) / 124), (unsigned)((ny + H - 1) / H));
+    k_flood2b_grid5<UNIF, SYM, R, MINB><<<grid, dim3(128, R), smem, st>>>(dia, nx, ny, H, b, m0, m1, xf, ctrl, spread);
+}
+
 void Engine::enqueue_double_kernel(bool attr_only) {
+    if (flood2_band) {
+        const int nx = grid5_nx, ny = n / std::max(grid5_nx, 1);
+        const double* bb = attr_only ? nullptr : solve_b;
+        if (timed_events) ck(cudaEventRecord((*timed_events)[2 * timed_index], st), "event");
+        if (dia.uniform && flood2_r == 41)
+            launch_flood2b<true, true, 4, 1>(dia, nx, ny, flood2_h, bb, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread, st);
+        else if (dia.uniform && flood2_r == 22)
+            launch_flood2b<true, true, 2, 2>(dia, nx, ny, flood2_h, bb, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread, st);
+        else if (dia.uniform && flood2_r == 12)
+            launch_flood2b<true, true, 1, 2>(dia, nx, ny, flood2_h, bb, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread, st);
+        else if (dia.uniform)
+            launch_flood2b<true, true, 4, 2>(dia, nx, ny, flood2_h, bb, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread, st);
+        else if (symmetric)
+            launch_flood2b<false, true, 4, 1>(dia, nx, ny, flood2_h, bb, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread, st);
+        else
+            launch_flood2b<false, false, 4, 1>(dia, nx, ny, flood2_h, bb, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread, st);
+        ck(cudaGetLastError(), "flood2b");
+        if (timed_events) ck(cudaEventRecord((*timed_events)[2 * timed_index + 1], st), "event");
+        return;
+    }
     constexpr int TPB = 128;
     const int nx = grid5_nx, ny = n / std::max(grid5_nx, 1);
     const double* bb = attr_only ? nullptr : solve_b;
     if (timed_events) ck(cudaEventRecord((*timed_events)[2 * timed_index], st), "event");
-    if (dia.uniform && flood2_st == 3 && flood2_minb == 3)
+    if (dia.uniform && flood2_st == 3)
         launch_flood2<true, true, TPB, 3, 3>(dia, nx, ny, flood2_h, bb, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread, st);
-    else if (dia.uniform && flood2_st == 3)
-        launch_flood2<true, true, TPB, 4, 3>(dia, nx, ny, flood2_h, bb, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread, st);
+    else if (dia.uniform && flood2_st == 5)
+        launch_flood2<true, true, TPB, 3, 5>(dia, nx, ny, flood2_h, bb, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread, st);
     else if (dia.uniform)
         launch_flood2<true, true, TPB, 3, 4>(dia, nx, ny, flood2_h, bb, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread, st);
     else if (symmetric)

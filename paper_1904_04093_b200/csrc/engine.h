@@ -94,6 +94,8 @@ struct Engine {
     int flood2_h = 80;          // tile rows of k_flood2_grid5 (2048^2: 17 x 26 tiles = one wave at 3 per SM)
     int flood2_st = 3;          // staged rows (cp.async pipeline depth + 1)
     int flood2_minb = 3;        // resident blocks the uniform variant is compiled for
+    bool flood2_band = false;   // banded variant (k_flood2b_grid5)
+    int flood2_r = 42;          // banded variant: rows per band * 10 + resident blocks
     void enqueue_double_kernel(bool attr_only = false);
     const Levels* solve_levels = nullptr;
     bool solve_rb = false;

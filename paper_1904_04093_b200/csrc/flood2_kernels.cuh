@@ -569,3 +569,214 @@ static __global__ void __launch_bounds__(TPB, MINB)
 }
 
 }  // namespace bgabp
+
+namespace bgabp {
+
+// ---------------------------------------------------------------------------------------------
+// Banded variant: the block (128 columns x R rows of threads) walks its tile R rows at a time in
+// three fully parallel passes per band -- A (sweep t, rows ya), B (sweep t+1, rows ya - 2) and the
+// x(t) residual (rows ya - 4) -- with the sweep-t messages and both x rings in shared memory
+// (8-row rings, two barriers per band).  Each thread owns one node per pass: no per-thread row
+// queues, so the register budget stays small and many more warps are resident than in the
+// column-walking kernel above.  Same arithmetic, same ownership rules, bit-identical.
+// ---------------------------------------------------------------------------------------------
+template <bool UNIF, bool SYM, int R>
+struct Band5Smem {
+    double2 msg[8][4][128];  // outgoing sweep-t messages (S, W, E, N) of each ring row
+    double xa[8][128];       // x(t-1)
+    double xb[8][128];       // x(t)
+};
+
+template <bool UNIF, bool SYM, int R, int MINB>
+static __global__ void __launch_bounds__(128 * R, MINB)
+    k_flood2b_grid5(DiaP P, int nx, int ny, int H, const double* __restrict__ b, double2* m0, double2* m1,
+                    double* xring, Ctrl* ctrl, unsigned long long* spread) {
+    constexpr int TX = 128, W = TX - 4;
+    if (ld_ctrl(&ctrl->done)) return;
+    extern __shared__ __align__(16) unsigned char dsm[];
+    Band5Smem<UNIF, SYM, R>& S = *reinterpret_cast<Band5Smem<UNIF, SYM, R>*>(dsm);
+    const int t = ld_ctrl(&ctrl->step);
+    const int n = P.n;
+    const double2* __restrict__ mi = (((t - 1) >> 1) & 1) ? m1 : m0;  // sweep t-1
+    double2* __restrict__ mout = (((t + 1) >> 1) & 1) ? m1 : m0;       // sweep t+1
+    double* __restrict__ xa_out = xring + (size_t)((t - 1) & (kXRing2 - 1)) * n;
+    double* __restrict__ xb_out = xring + (size_t)(t & (kXRing2 - 1)) * n;
+    const bool have_xa = t >= 2;
+    const int c = threadIdx.x, r = threadIdx.y;
+    const int x0 = blockIdx.x * W, y0 = blockIdx.y * H;
+    const int x = x0 - 2 + c;
+    const bool colv = x >= 0 && x < nx;
+    const bool col1 = colv && c >= 1 && c <= W + 2;
+    const bool coli = colv && c >= 2 && c < W + 2;
+    const int ylo = y0, yhi = min(y0 + H, ny);
+    const int yfirst = y0 - 2;  // ring slot of row y: (y - yfirst) & 7
+    double cu[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) cu[s] = UNIF ? P.cu[s] : 0.0;
+    const double2 z2 = make_double2(0.0, 0.0);
+    double ra = 0.0, rb = 0.0;
+
+    // A-pass operands of the next band, prefetched into registers one band ahead
+    auto load_a = [&](int ya, Node5<UNIF, SYM>& d, double2 (&in)[4]) {
+        if (colv && ya >= 0 && ya < ny && ya <= y0 + H + 1) {
+            const int j = ya * nx + x;
+            load_node5<UNIF, SYM>(P, b, n, j, d);
+#pragma unroll
+            for (int s = 0; s < 4; ++s) in[s] = __ldg(mi + (size_t)s * n + j);
+        } else {
+            d.mk = 0u;
+        }
+    };
+    Node5<UNIF, SYM> dn;
+    double2 inn[4];
+    load_a(yfirst + r, dn, inn);
+    for (int ybase = yfirst; ybase <= y0 + H + 3; ybase += R) {
+        const int ya = ybase + r;
+        Node5<UNIF, SYM> da = dn;
+        double2 ina[4];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) ina[s] = inn[s];
+        load_a(ya + R, dn, inn);  // in flight during this band's three passes
+        const int sa = (ya - yfirst) & 7;
+        // ---- A: sweep t on node (x, ya) ------------------------------------------------------
+        {
+            double2 g[4] = {z2, z2, z2, z2};
+            double xA = 0.0;
+            const bool va = colv && ya >= 0 && ya < ny && ya <= y0 + H + 1;
+            if (va) {
+                const int j = ya * nx + x;
+                const bool own = coli && ya >= ylo && ya < yhi;
+                double sig, acc, den[4];
+                if (da.mk == kFull5) {
+                    double cf[4], rv[4];
+                    coef_full5<UNIF, SYM>(da, cu, cf, rv);
+                    node_full5(cf, da.dj, da.bj, ina, have_xa, sig, acc, xA, den, g);
+                    if (own) {
+#pragma unroll
+                        for (int s = 0; s < 4; ++s)
+                            if (fabs(den[s]) < kPivotFloor)
+                                atomicMin(&ctrl->epiv[t & 3], ((unsigned long long)j << 32) | (unsigned)(j + P.off[s]));
+                    }
+                } else {
+#pragma unroll
+                    for (int s = 0; s < 4; ++s)
+                        if (!(da.mk & (1u << s))) ina[s] = z2;
+                    aggregate5<UNIF, SYM>(P, da, ina, sig, acc);
+                    if (have_xa) xA = ddiv(acc, sig);
+#pragma unroll
+                    for (int s = 0; s < 4; ++s) {
+                        if (!(da.mk & (1u << (16 + s)))) continue;
+                        const double cs = cc5<UNIF, SYM>(P, da, s);
+                        den[s] = dsub(sig, dmul(ina[s].x, cs));
+                        if (own && fabs(den[s]) < kPivotFloor)
+                            atomicMin(&ctrl->epiv[t & 3], ((unsigned long long)j << 32) | (unsigned)(j + P.off[s]));
+                        const double q = ddiv(-cs, den[s]);
+                        g[s] = make_double2(q, dmul(q, dsub(acc, ina[s].y)));
+                    }
+                }
+                if (!have_xa) xA = 0.0;
+                if (have_xa && own) {
+                    xa_out[j] = xA;
+                    if (fabs(sig) < kPivotFloor) atomicMin(&ctrl->npiv[(t - 1) & 3], (unsigned long long)j);
+                }
+            }
+#pragma unroll
+            for (int s = 0; s < 4; ++s) S.msg[sa][s][c] = g[s];
+            S.xa[sa][c] = xA;
+        }
+        __syncthreads();
+        // ---- B: sweep t+1 on node (x, yb), yb = ya - 2; x(t-1) residual there ----------------------
+        const int yb = ya - 2;
+        {
+            const bool vb = col1 && yb >= 0 && yb < ny && yb >= y0 - 1 && yb <= y0 + H;
+            const int sb = (yb - yfirst) & 7, sbm = (yb - 1 - yfirst) & 7, sbp = (yb + 1 - yfirst) & 7;
+            double xB = 0.0;
+            if (vb) {
+                const int j = yb * nx + x;
+                const bool own = coli && yb >= ylo && yb < yhi;
+                Node5<UNIF, SYM> d;
+                load_node5<UNIF, SYM>(P, b, n, j, d);
+                double2 in[4];
+                in[0] = S.msg[sbm][3][c];      // north-going from (x, yb - 1)
+                in[1] = S.msg[sb][2][c - 1];   // east-going from (x - 1, yb)
+                in[2] = S.msg[sb][1][c + 1];   // west-going from (x + 1, yb)
+                in[3] = S.msg[sbp][0][c];      // south-going from (x, yb + 1)
+                double sig, acc, den[4];
+                double2 g[4];
+                double cf[4], rv[4];
+                const bool full = d.mk == kFull5;
+                if (full) {
+                    coef_full5<UNIF, SYM>(d, cu, cf, rv);
+                    node_full5(cf, d.dj, d.bj, in, true, sig, acc, xB, den, g);
+                } else {
+#pragma unroll
+                    for (int s = 0; s < 4; ++s)
+                        if (!(d.mk & (1u << s))) in[s] = z2;
+                    aggregate5<UNIF, SYM>(P, d, in, sig, acc);
+                    xB = ddiv(acc, sig);
+                }
+                if (own) {
+                    xb_out[j] = xB;
+                    if (fabs(sig) < kPivotFloor) atomicMin(&ctrl->npiv[t & 3], (unsigned long long)j);
+                    if (full) {
+                        mout[(size_t)3 * n + j - nx] = g[0];
+                        mout[(size_t)2 * n + j - 1] = g[1];
+                        mout[(size_t)1 * n + j + 1] = g[2];
+                        mout[j + nx] = g[3];
+#pragma unroll
+                        for (int s = 0; s < 4; ++s)
+                            if (fabs(den[s]) < kPivotFloor)
+                                atomicMin(&ctrl->epiv[(t + 1) & 3],
+                                          ((unsigned long long)j << 32) | (unsigned)(j + P.off[s]));
+                    } else {
+#pragma unroll
+                        for (int s = 0; s < 4; ++s) {
+                            if (!(d.mk & (1u << (16 + s)))) continue;
+                            const double cs = cc5<UNIF, SYM>(P, d, s);
+                            const double dn2 = dsub(sig, dmul(in[s].x, cs));
+                            const int k = j + P.off[s];
+                            if (fabs(dn2) < kPivotFloor)
+                                atomicMin(&ctrl->epiv[(t + 1) & 3], ((unsigned long long)j << 32) | (unsigned)k);
+                            const double q = ddiv(-cs, dn2);
+                            mout[(size_t)P.rev[s] * n + k] = make_double2(q, dmul(q, dsub(acc, in[s].y)));
+                        }
+                    }
+                    if (have_xa) {  // residual of x(t-1) at (x, yb)
+                        const double rr =
+                            full ? residual_full5(rv, d.dj, d.bj, S.xa[sb][c], S.xa[sbm][c], S.xa[sb][c - 1],
+                                                  S.xa[sb][c + 1], S.xa[sbp][c])
+                                 : residual5<UNIF, SYM>(P, d, S.xa[sb][c], S.xa[sbm][c], S.xa[sb][c - 1],
+                                                        S.xa[sb][c + 1], S.xa[sbp][c]);
+                        ra = fmax(ra, nan_skip_abs(rr));
+                    }
+                }
+            }
+            S.xb[sb][c] = xB;
+        }
+        __syncthreads();
+        // ---- C: residual of x(t) at (x, yc), yc = ya - 4 ------------------------------------------
+        const int yc = ya - 4;
+        if (coli && yc >= ylo && yc < yhi) {
+            const int sc = (yc - yfirst) & 7, scm = (yc - 1 - yfirst) & 7, scp = (yc + 1 - yfirst) & 7;
+            Node5<UNIF, SYM> d;
+            load_node5<UNIF, SYM>(P, b, n, yc * nx + x, d);
+            double rr;
+            if (d.mk == kFull5) {
+                double cf[4], rv[4];
+                coef_full5<UNIF, SYM>(d, cu, cf, rv);
+                rr = residual_full5(rv, d.dj, d.bj, S.xb[sc][c], S.xb[scm][c], S.xb[sc][c - 1], S.xb[sc][c + 1],
+                                    S.xb[scp][c]);
+            } else {
+                rr = residual5<UNIF, SYM>(P, d, S.xb[sc][c], S.xb[scm][c], S.xb[sc][c - 1], S.xb[sc][c + 1],
+                                          S.xb[scp][c]);
+            }
+            rb = fmax(rb, nan_skip_abs(rr));
+        }
+    }
+    const unsigned tid = threadIdx.y * 128 + threadIdx.x;
+    const unsigned wid = ((blockIdx.y * gridDim.x + blockIdx.x) * (128 * R) + tid) >> 5;
+    if (have_xa) warp_max_spread2(spread + (size_t)((t - 1) & 3) * kSpread, ra, wid);
+    warp_max_spread2(spread + (size_t)(t & 3) * kSpread, rb, wid);
+}
+
+}  // namespace bgabp

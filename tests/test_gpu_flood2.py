@@ -1,5 +1,5 @@
-"""The two-iteration flood solve launch (flood2_kernels.cuh, k_flood2_grid5) against the CPU
-oracle and against the one-iteration fused step (BGABP_FLOOD2=0): GabpEngine::solve
+"""The two-iteration flood solve launches (flood2_kernels.cuh: the column-walking k_flood2_grid5
+and the banded k_flood2b_grid5) against the CPU oracle and against the one-iteration fused step: GabpEngine::solve
 (gabp.cpp:174-219) statuses, iteration counts, details, residual histories and x, bit for bit, on
 5-point grids of every tile-boundary shape, uniform / variable / nonsymmetric coefficients,
 convergence at odd and even iterations, max_iter caps, pivot breakdowns and residual blowups."""
@@ -28,20 +28,23 @@ def _triplets(A):
     return rows, cols, vals
 
 
-def _solve(A, b, tol, max_iter, double):
-    os.environ["BGABP_FLOOD2"] = "1" if double else "0"
+def _solve(A, b, tol, max_iter, kind):
+    """kind: "single" (one iteration per launch), "col" (k_flood2_grid5), "band" (k_flood2b_grid5)"""
+    os.environ["BGABP_FLOOD2"] = "0" if kind == "single" else "1"
+    os.environ["BGABP_FLOOD2_KIND"] = kind
     try:
         eng = g.GabpEngine(A)
         return eng.solve(b, g.Schedule.parallel_flood(), g.GabpOptions(tol=tol, max_iter=max_iter))
     finally:
         os.environ.pop("BGABP_FLOOD2", None)
+        os.environ.pop("BGABP_FLOOD2_KIND", None)
 
 
 def _check(orc, A, b, tol, max_iter):
-    d = _solve(A, b, tol, max_iter, True)
-    s = _solve(A, b, tol, max_iter, False)
+    reps = [_solve(A, b, tol, max_iter, k) for k in ("col", "band", "single")]
     want = orc.engine(_csr_to_orc(A)).solve(b, OSched.parallel_flood(), tol=tol, max_iter=max_iter)
-    for got in (d, s):
+    d = reps[0]
+    for got in reps:
         assert (int(got.status), got.iterations, got.detail) == (want.status, want.iterations, want.detail)
         assert np.array_equal(got.residual_history, want.residual_history)
         assert np.array_equal(got.solution, want.solution)
