@@ -100,3 +100,15 @@ def test_device_built_engine_solves_like_host_built(orc):
             st = eng.get_state()
             reps.append((int(rep.status), rep.iterations, rep.solution.tobytes(), st.m.tobytes()))
     assert reps[:5] == reps[5:]
+
+
+@pytest.mark.parametrize("cfg", [2, 4])
+def test_device_build_equals_host_build_full_size(cfg):
+    """BASELINE.json configs 2 (4.2M nodes, 21M entries) and 4 (16.8M nodes, 117M entries, 7-point,
+    variable coefficients): the device-built layout equals the host-built one bit for bit."""
+    A = g.config_problem(cfg).A
+    dd, info_d = _digest(A, False)
+    dh, info_h = _digest(A, True)
+    info_d.pop("device_bytes"), info_h.pop("device_bytes")
+    assert info_d == info_h
+    assert dd == dh
