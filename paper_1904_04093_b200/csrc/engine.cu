@@ -283,28 +283,51 @@ struct Stager {
     void* buf[2] = {nullptr, nullptr};
     cudaEvent_t ev[2] = {nullptr, nullptr};
     static constexpr size_t kChunk = size_t(32) << 20;
+    void init() {
+        if (buf[0]) return;
+        for (int k = 0; k < 2; ++k) {
+            ck(cudaMallocHost(&buf[k], kChunk), "cudaMallocHost");
+            ck(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming), "event");
+        }
+    }
 };
+void par_copy(char* dst, const char* src, size_t len) {
+    const int T = std::max(1, std::min(omp_get_max_threads(), 16));
+    const size_t piece = (len + T - 1) / T;
+#pragma omp parallel for num_threads(T) schedule(static)
+    for (int t = 0; t < T; ++t) {
+        const size_t a = std::min(len, (size_t)t * piece), b = std::min(len, a + piece);
+        if (b > a) std::memcpy(dst + a, src + a, b - a);
+    }
+}
 Stager& stager() {
     static Stager* s = new Stager();  // leaked on purpose: no teardown-order issues at exit
     return *s;
 }
 }  // namespace
 
-void Engine::upload_host(void* dst, const void* src, size_t bytes) {
+static bool is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+// Host -> device on `st`.  Pinned sources and small copies go straight to the DMA engine; large
+// pageable ones through the stager: parallel host copies into one pinned chunk overlapped with
+// the DMA of the other.  On return the source may be reused.
+void host_to_device(void* dst, const void* src, size_t bytes, cudaStream_t st) {
     if (bytes == 0) return;
     constexpr size_t kChunk = Stager::kChunk;
-    if (bytes <= (size_t(1) << 20)) {
+    if (bytes <= (size_t(1) << 20) || is_pinned(src)) {
         ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st), "H2D");
         return;
     }
     Stager& S = stager();
     std::lock_guard<std::mutex> lock(S.mu);
-    if (!S.buf[0]) {
-        for (int k = 0; k < 2; ++k) {
-            ck(cudaMallocHost(&S.buf[k], kChunk), "cudaMallocHost");
-            ck(cudaEventCreateWithFlags(&S.ev[k], cudaEventDisableTiming), "event");
-        }
-    }
+    S.init();
     const char* s = static_cast<const char*>(src);
     char* d = static_cast<char*>(dst);
     int k = 0;
@@ -312,21 +335,47 @@ void Engine::upload_host(void* dst, const void* src, size_t bytes) {
     for (size_t off = 0; off < bytes; off += kChunk, k ^= 1) {
         const size_t len = std::min(kChunk, bytes - off);
         if (used[k]) ck(cudaEventSynchronize(S.ev[k]), "stage wait");
-        char* h = static_cast<char*>(S.buf[k]);
-        const int T = std::max(1, std::min(omp_get_max_threads(), 16));
-        const size_t piece = (len + T - 1) / T;
-#pragma omp parallel for num_threads(T) schedule(static)
-        for (int t = 0; t < T; ++t) {
-            const size_t a = std::min(len, (size_t)t * piece), b = std::min(len, a + piece);
-            if (b > a) std::memcpy(h + a, s + off + a, b - a);
-        }
-        ck(cudaMemcpyAsync(d + off, h, len, cudaMemcpyHostToDevice, st), "H2D");
+        par_copy(static_cast<char*>(S.buf[k]), s + off, len);
+        ck(cudaMemcpyAsync(d + off, S.buf[k], len, cudaMemcpyHostToDevice, st), "H2D");
         ck(cudaEventRecord(S.ev[k], st), "event");
         used[k] = true;
     }
     for (int q = 0; q < 2; ++q)  // the buffers are reused by the next caller (any stream)
         if (used[q]) ck(cudaEventSynchronize(S.ev[q]), "stage wait");
 }
+
+// Device -> host on `st`, ordered after the work already on `st`.  Pinned destinations (and small
+// copies) are enqueued and complete with the caller's next synchronisation; large pageable ones
+// go through the stager and have landed in `dst` on return.
+void device_to_host(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    if (bytes == 0) return;
+    constexpr size_t kChunk = Stager::kChunk;
+    if (bytes <= (size_t(1) << 20) || is_pinned(dst)) {
+        ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st), "D2H");
+        return;
+    }
+    Stager& S = stager();
+    std::lock_guard<std::mutex> lock(S.mu);
+    S.init();
+    const char* s = static_cast<const char*>(src);
+    char* d = static_cast<char*>(dst);
+    // chunk i lands in buffer i & 1; the host copy-out of chunk i overlaps the DMA of chunk i+1
+    const size_t nch = (bytes + kChunk - 1) / kChunk;
+    auto enqueue = [&](size_t i) {
+        const size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
+        ck(cudaMemcpyAsync(S.buf[i & 1], s + off, len, cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaEventRecord(S.ev[i & 1], st), "event");
+    };
+    enqueue(0);
+    for (size_t i = 0; i < nch; ++i) {
+        if (i + 1 < nch) enqueue(i + 1);
+        ck(cudaEventSynchronize(S.ev[i & 1]), "stage wait");
+        const size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
+        par_copy(d + off, static_cast<const char*>(S.buf[i & 1]), len);
+    }
+}
+
+void Engine::upload_host(void* dst, const void* src, size_t bytes) { host_to_device(dst, src, bytes, st); }
 
 // host copies of the matrix and its message-graph structure: canonical CSR, transpose positions
 // (sparse.cpp:70-74), bit-symmetry, union neighbour lists (row j and column j, sorted)
@@ -1618,13 +1667,12 @@ int bgabp_solve(bgabp_engine* h, const double* b, const bgabp_schedule* s, const
     ABI_GUARD(detail, dl, {
         Engine& E = h->E;
         E.schedule_order_check(*s);
-        if (E.n > 0) ck(cudaMemcpyAsync(E.d_b, b, sizeof(double) * E.n, cudaMemcpyHostToDevice, E.st), "H2D b");
+        host_to_device(E.d_b, b, sizeof(double) * E.n, E.st);
         E.solve_begin(E.d_b, *s, *opt);
         E.solve_run_to_end();
         std::string d;
         E.solve_report(*rep, d);
-        if (x_out && E.n > 0)
-            ck(cudaMemcpyAsync(x_out, E.solve_x(), sizeof(double) * E.n, cudaMemcpyDeviceToHost, E.st), "D2H x");
+        if (x_out && E.n > 0) device_to_host(x_out, E.solve_x(), sizeof(double) * E.n, E.st);
         if (history)
             ck(cudaMemcpyAsync(history, E.d_hist, sizeof(double) * (rep->iterations + 1), cudaMemcpyDeviceToHost, E.st),
                "D2H hist");

@@ -27,6 +27,9 @@ struct CudaError : std::runtime_error {
 };
 
 void put_err(char* err, size_t len, const std::string& s);
+// host <-> device copies of caller buffers: direct when pinned, staged (parallel) when pageable
+void host_to_device(void* dst, const void* src, size_t bytes, cudaStream_t st);
+void device_to_host(void* dst, const void* src, size_t bytes, cudaStream_t st);
 void ck(cudaError_t e, const char* what);
 
 inline double bits2d(unsigned long long b) {

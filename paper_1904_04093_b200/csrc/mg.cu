@@ -63,19 +63,35 @@ std::vector<double> dense_inverse(Engine& E) {
                 for (int c = k + 1; c < n; ++c) a[(size_t)i * n + c] -= l * a[(size_t)k * n + c];
         }
     }
-#pragma omp parallel for schedule(dynamic, 8)
-    for (int col = 0; col < n; ++col) {
-        std::vector<double> y(n, 0.0);
-        y[col] = 1.0;
+    // columns of the inverse, four at a time per thread: each column's operations and their
+    // order are those of the one-column substitution (independent accumulations, more ILP)
+    constexpr int B = 4;
+#pragma omp parallel for schedule(dynamic, 2)
+    for (int c0 = 0; c0 < n; c0 += B) {
+        const int nb = std::min(B, n - c0);
+        std::vector<double> y((size_t)n * B, 0.0);  // y[i * B + q]: column c0 + q
+        for (int q = 0; q < nb; ++q) y[(size_t)(c0 + q) * B + q] = 1.0;
         for (int k = 0; k < n; ++k)
-            if (piv[k] != k) std::swap(y[k], y[piv[k]]);
-        for (int i = 0; i < n; ++i)
-            for (int c = 0; c < i; ++c) y[i] -= a[(size_t)i * n + c] * y[c];
-        for (int i = n - 1; i >= 0; --i) {
-            for (int c = i + 1; c < n; ++c) y[i] -= a[(size_t)i * n + c] * y[c];
-            y[i] /= a[(size_t)i * n + i];
+            if (piv[k] != k)
+                for (int q = 0; q < B; ++q) std::swap(y[(size_t)k * B + q], y[(size_t)piv[k] * B + q]);
+        for (int i = 0; i < n; ++i) {
+            double acc[B];
+            for (int q = 0; q < B; ++q) acc[q] = y[(size_t)i * B + q];
+            const double* ai = a.data() + (size_t)i * n;
+            for (int c = 0; c < i; ++c)
+                for (int q = 0; q < B; ++q) acc[q] -= ai[c] * y[(size_t)c * B + q];
+            for (int q = 0; q < B; ++q) y[(size_t)i * B + q] = acc[q];
         }
-        for (int i = 0; i < n; ++i) inv[(size_t)i * n + col] = y[i];
+        for (int i = n - 1; i >= 0; --i) {
+            double acc[B];
+            for (int q = 0; q < B; ++q) acc[q] = y[(size_t)i * B + q];
+            const double* ai = a.data() + (size_t)i * n;
+            for (int c = i + 1; c < n; ++c)
+                for (int q = 0; q < B; ++q) acc[q] -= ai[c] * y[(size_t)c * B + q];
+            for (int q = 0; q < B; ++q) y[(size_t)i * B + q] = acc[q] / ai[i];
+        }
+        for (int i = 0; i < n; ++i)
+            for (int q = 0; q < nb; ++q) inv[(size_t)i * n + c0 + q] = y[(size_t)i * B + q];
     }
     return inv;
 }
@@ -599,11 +615,11 @@ int bgmg_vcycle(bgmg* h, const bgmg_cycle* spec, const double* b, double* x, cha
     MG_GUARD(err, errlen, {
         const int n = h->E(0).n;
         h->ensure_fine_scratch();
-        ck(cudaMemcpyAsync(h->d_fine_b, b, sizeof(double) * n, cudaMemcpyHostToDevice, h->st), "H2D");
-        ck(cudaMemcpyAsync(h->d_fine_x, x, sizeof(double) * n, cudaMemcpyHostToDevice, h->st), "H2D");
+        host_to_device(h->d_fine_b, b, sizeof(double) * n, h->st);
+        host_to_device(h->d_fine_x, x, sizeof(double) * n, h->st);
         h->fine_r_b = h->fine_r_x = nullptr;
         h->v_cycle_dev(*spec, h->d_fine_b, h->d_fine_x);
-        ck(cudaMemcpyAsync(x, h->d_fine_x, sizeof(double) * n, cudaMemcpyDeviceToHost, h->st), "D2H");
+        device_to_host(x, h->d_fine_x, sizeof(double) * n, h->st);
         ck(cudaStreamSynchronize(h->st), "sync");
         std::string f = h->failure();
         if (!f.empty()) {
@@ -619,11 +635,11 @@ int bgmg_solve(bgmg* h, const bgmg_cycle* spec, const double* b, const bgmg_opti
     MG_GUARD(detail, dl, {
         const int n = h->E(0).n;
         h->ensure_fine_scratch();
-        ck(cudaMemcpyAsync(h->d_fine_b, b, sizeof(double) * n, cudaMemcpyHostToDevice, h->st), "H2D");
+        host_to_device(h->d_fine_b, b, sizeof(double) * n, h->st);
         std::vector<double> hist;
         std::string d;
         h->solve_dev(*spec, h->d_fine_b, h->d_fine_x, *opt, *rep, hist, d);
-        if (x_out) ck(cudaMemcpyAsync(x_out, h->d_fine_x, sizeof(double) * n, cudaMemcpyDeviceToHost, h->st), "D2H");
+        if (x_out) device_to_host(x_out, h->d_fine_x, sizeof(double) * n, h->st);
         ck(cudaStreamSynchronize(h->st), "sync");
         if (history) std::memcpy(history, hist.data(), sizeof(double) * hist.size());
         put_err(detail, dl, d);
