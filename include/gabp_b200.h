@@ -167,6 +167,23 @@ int bgabp_shard_pack(bgabp_engine* e, int which, int lo, int len, void* out_dev)
 int bgabp_shard_unpack(bgabp_engine* e, int which, const void* recv_dev, int lo, int len, int sender_lo,
                        int sender_hi);
 int bgabp_shard_state(bgabp_engine* e, int* done, int* step);
+/* Peer-memory variant (direct peer stores instead of pack / collective / unpack).
+ * The fused step stores the messages it computes for a neighbour's owned nodes straight into that
+ * neighbour's message buffer (and x(t-1) of the neighbour's ghost nodes into its x slot), and the
+ * fold writes the four reduction words into slot [rank][t & 1] of every shard; each shard then
+ * waits for every other shard's step (bgabp_shard_p2p_wait) and decides on the MAX of the slots.
+ * lower / upper = {msg buffer 0, msg buffer 1, x slot 0, x slot 1} device pointers of the
+ * neighbour (bgabp_shard_msg / bgabp_shard_x; peer-mapped between GPUs), or NULL at the ends;
+ * *_n = the neighbour's local node count, *_delta = its local index minus ours for the same
+ * global node; own local nodes j < xlo_end are the lower neighbour's ghosts, j >= xhi_begin the
+ * upper's; slots[q] = shard q's bgabp_shard_peer_slots array.  1 <= nranks <= 8. */
+int bgabp_shard_peer_slots(bgabp_engine* e, void** slots);
+int bgabp_shard_set_peers(bgabp_engine* e, int nranks, int rank, void* const* lower, int lower_n, int lower_delta,
+                          void* const* upper, int upper_n, int upper_delta, int xlo_end, int xhi_begin,
+                          void* const* slots);
+int bgabp_shard_p2p_compute(bgabp_engine* e);
+int bgabp_shard_p2p_wait(bgabp_engine* e, bgabp_engine* other);
+int bgabp_shard_p2p_decide(bgabp_engine* e);
 
 /* residual_inf_norm(A, x, b) (sparse.cpp:104-115) on the handle's matrix */
 int bgabp_residual_inf_norm(bgabp_engine* e, const double* x, const double* b, double* out);

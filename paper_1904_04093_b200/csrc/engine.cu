@@ -68,6 +68,7 @@ Engine::~Engine() {
     for (void* p : allocs) cudaFree(p);
     if (h_ctrl) cudaFreeHost(h_ctrl);
     if (h_poll) cudaFreeHost(h_poll);
+    if (step_ev) cudaEventDestroy(step_ev);
     for (auto& e : poll_ev)
         if (e) cudaEventDestroy(e);
     if (st && own_stream) cudaStreamDestroy(st);
@@ -980,6 +981,29 @@ void Engine::enqueue_step() {
     enqueue_step_other();
 }
 
+// the sharded fused step (runtime node range / global pivot keys), with or without peer halos
+template <int SS, int MB, bool DF>
+static void launch_sharded_step(Engine& E, unsigned g, bool dl) {
+    double *x0 = E.d_xf, *x1 = E.d_xf + E.n;
+#define SHARDED_STEP(DL_, SYM_, PEER_)                                                                          \
+    k_flood_solve_dia<SS, DL_, SYM_, MB, DF, true, false, true, PEER_><<<g, 256, 0, E.st>>>(                   \
+        E.dia, E.solve_b, E.d_msg[0], E.d_msg[1], x0, x1, E.d_ctrl, E.d_spread, E.peer)
+    if (E.peer_on) {
+        if (E.symmetric) {
+            if (dl) SHARDED_STEP(true, true, true); else SHARDED_STEP(false, true, true);
+        } else {
+            if (dl) SHARDED_STEP(true, false, true); else SHARDED_STEP(false, false, true);
+        }
+    } else {
+        if (E.symmetric) {
+            if (dl) SHARDED_STEP(true, true, false); else SHARDED_STEP(false, true, false);
+        } else {
+            if (dl) SHARDED_STEP(true, false, false); else SHARDED_STEP(false, false, false);
+        }
+    }
+#undef SHARDED_STEP
+}
+
 void Engine::enqueue_fused_kernel() {
     {
         const bool dl = solve_stop == BGABP_STOP_MESSAGE_DELTA;
@@ -988,13 +1012,7 @@ void Engine::enqueue_fused_kernel() {
         // register cap per slot count: 4 resident blocks for 2-4 slots, fewer for 6-8 (no spills)
 #define FUSED(SS_, MB_, DF_, MBU_, DFU_)                                                                            \
     if (sharded) {                                                                                                 \
-        if (symmetric) {                                                                                           \
-            if (dl) k_flood_solve_dia<SS_, true, true, MB_, DF_, true, false, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
-            else k_flood_solve_dia<SS_, false, true, MB_, DF_, true, false, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
-        } else {                                                                                                   \
-            if (dl) k_flood_solve_dia<SS_, true, false, MB_, DF_, true, false, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
-            else k_flood_solve_dia<SS_, false, false, MB_, DF_, true, false, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
-        }                                                                                                          \
+        launch_sharded_step<SS_, MB_, DF_>(*this, g, dl);                                                          \
     } else if (dia.uniform) {                                                                                      \
         if (dl) k_flood_solve_dia<SS_, true, true, MBU_, DFU_, true, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
         else k_flood_solve_dia<SS_, false, true, MBU_, DFU_, true, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
@@ -1952,6 +1970,84 @@ int bgabp_shard_step_decide(bgabp_engine* h) {
         Engine& E = h->E;
         k_shard_decide<<<1, 1, 0, E.st>>>(E.d_ctrl, E.d_hist, E.d_red4);
         ck(cudaGetLastError(), "shard decide");
+        return BGABP_OK;
+    })
+}
+
+// ---- sharded solve with peer-memory halos and reduction (no pack/unpack, no collective) ----------
+int bgabp_shard_peer_slots(bgabp_engine* h, void** slots) {
+    ABI_GUARD(nullptr, 0, {
+        Engine& E = h->E;
+        if (!E.d_slots) {
+            const size_t bytes = sizeof(unsigned long long) * kMaxShards * 2 * 4;
+            E.d_slots = static_cast<unsigned long long*>(E.dalloc(bytes));
+            ck(cudaMemsetAsync(E.d_slots, 0, bytes, E.st), "memset");
+        }
+        if (!E.d_xf) E.d_xf = static_cast<double*>(E.dalloc(sizeof(double) * kXRing2 * (size_t)std::max(E.n, 1)));
+        *slots = E.d_slots;
+        return BGABP_OK;
+    })
+}
+
+int bgabp_shard_set_peers(bgabp_engine* h, int nranks, int rank, void* const* lower, int lower_n, int lower_delta,
+                          void* const* upper, int upper_n, int upper_delta, int xlo_end, int xhi_begin,
+                          void* const* slots) {
+    ABI_GUARD(nullptr, 0, {
+        Engine& E = h->E;
+        if (nranks < 1 || nranks > kMaxShards || rank < 0 || rank >= nranks)
+            throw InvalidArg("shard: 1 <= nranks <= 8 and 0 <= rank < nranks");
+        if (E.dia.j0 == 0 && E.dia.j1 == E.n && nranks > 1 && !E.d_red4)
+            throw InvalidArg("shard: call set_range first");
+        PeerP& Q = E.peer;
+        std::memset(&Q, 0, sizeof Q);
+        for (int b2 = 0; b2 < 2; ++b2) {  // lower/upper = {msg0, msg1, x0, x1} of the neighbour (or null)
+            Q.m[0][b2] = lower ? static_cast<double2*>(lower[b2]) : nullptr;
+            Q.x[0][b2] = lower ? static_cast<double*>(lower[2 + b2]) : nullptr;
+            Q.m[1][b2] = upper ? static_cast<double2*>(upper[b2]) : nullptr;
+            Q.x[1][b2] = upper ? static_cast<double*>(upper[2 + b2]) : nullptr;
+        }
+        Q.nq[0] = lower_n;
+        Q.nq[1] = upper_n;
+        Q.delta[0] = lower_delta;
+        Q.delta[1] = upper_delta;
+        Q.xlo_end = xlo_end;
+        Q.xhi_begin = xhi_begin;
+        for (int q = 0; q < nranks; ++q) Q.red[q] = static_cast<unsigned long long*>(slots[q]);
+        Q.nranks = nranks;
+        Q.rank = rank;
+        E.peer_on = true;
+        if (!E.d_red4) E.d_red4 = static_cast<unsigned long long*>(E.dalloc(sizeof(unsigned long long) * 4));
+        if (!E.step_ev) ck(cudaEventCreateWithFlags(&E.step_ev, cudaEventDisableTiming), "event");
+        return BGABP_OK;
+    })
+}
+
+// the fused step with peer stores, the fold into every shard's slots, and this shard's event
+int bgabp_shard_p2p_compute(bgabp_engine* h) {
+    ABI_GUARD(nullptr, 0, {
+        Engine& E = h->E;
+        if (!E.solve_fused || !E.peer_on) throw InvalidArg("shard: call set_peers and shard_solve_begin first");
+        E.enqueue_fused_kernel();
+        k_shard_fold_p2p<<<1, kSpread, 0, E.st>>>(E.d_ctrl, E.d_spread, E.d_red4, E.peer);
+        ck(cudaEventRecord(E.step_ev, E.st), "event");
+        ck(cudaGetLastError(), "shard p2p compute");
+        return BGABP_OK;
+    })
+}
+
+// order this shard's stream after another shard's last p2p_compute (its peer stores and words)
+int bgabp_shard_p2p_wait(bgabp_engine* h, bgabp_engine* other) {
+    ABI_GUARD(nullptr, 0, {
+        ck(cudaStreamWaitEvent(h->E.st, other->E.step_ev, 0), "wait");
+        return BGABP_OK;
+    })
+}
+
+int bgabp_shard_p2p_decide(bgabp_engine* h) {
+    ABI_GUARD(nullptr, 0, {
+        Engine& E = h->E;
+        k_shard_decide_p2p<<<1, 1, 0, E.st>>>(E.d_ctrl, E.d_hist, E.d_slots, E.peer.nranks, E.d_red4);
+        ck(cudaGetLastError(), "shard p2p decide");
         return BGABP_OK;
     })
 }

@@ -93,7 +93,11 @@ struct Engine {
     // device-resident solve loop
     bool solve_flood = true;
     bool solve_fused = false;
-    bool solve_double = false;  // fused flood solve, two iterations per launch (flood2_kernels.cuh)
+    bool solve_double = false;
+    PeerP peer{};               // sharded solve: peer-memory halos and reduction slots
+    bool peer_on = false;
+    unsigned long long* d_slots = nullptr;  // [kMaxShards][2][4] reduction words of every shard
+    cudaEvent_t step_ev = nullptr;          // recorded after each p2p step  // fused flood solve, two iterations per launch (flood2_kernels.cuh)
     int flood2_h = 80;          // tile rows of k_flood2_grid5 (2048^2: 17 x 26 tiles = one wave at 3 per SM)
     int flood2_st = 3;          // staged rows (cp.async pipeline depth + 1)
     int flood2_minb = 3;        // resident blocks the uniform variant is compiled for

@@ -153,6 +153,12 @@ def lib():
             "bgabp_shard_pack": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _vp]),
             "bgabp_shard_unpack": (C.c_int, [_vp, C.c_int, _vp, C.c_int, C.c_int, C.c_int, C.c_int]),
             "bgabp_shard_state": (C.c_int, [_vp, _ip, _ip]),
+            "bgabp_shard_peer_slots": (C.c_int, [_vp, C.POINTER(_vp)]),
+            "bgabp_shard_set_peers": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(_vp), C.c_int, C.c_int,
+                                                 C.POINTER(_vp), C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)]),
+            "bgabp_shard_p2p_compute": (C.c_int, [_vp]),
+            "bgabp_shard_p2p_wait": (C.c_int, [_vp, _vp]),
+            "bgabp_shard_p2p_decide": (C.c_int, [_vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)

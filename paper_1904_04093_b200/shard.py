@@ -258,3 +258,70 @@ def sharded_solve(shards: dict, layouts, owner, world, b_inf, opt: GabpOptions, 
             out[k] = x
             res = (status, its, detail, hist)
     return res[0], res[1], res[2], out, res[3]
+
+
+def connect_peers(shards: dict, layouts):
+    """Wire every GpuShard of this process to its neighbours for the peer-memory step: each
+    shard stores the halo messages / x it computes straight into the neighbour's buffers and its
+    reduction words into every shard's slot array (bgabp_shard_set_peers).  Shards may live on
+    different GPUs of one process (peer access enabled) or share one GPU."""
+    L = lib()
+    P = len(layouts)
+    if sorted(shards) != list(range(P)):
+        raise ValueError("connect_peers: every shard must live in this process")
+    slots = []
+    for k in range(P):
+        p = C.c_void_p()
+        _raise(L.bgabp_shard_peer_slots(shards[k].eng.handle, C.byref(p)), "peer slots")
+        slots.append(p.value)
+    slot_arr = (C.c_void_p * P)(*slots)
+
+    def bufs(k):
+        h = shards[k].eng.handle
+        return (C.c_void_p * 4)(L.bgabp_shard_msg(h, 0), L.bgabp_shard_msg(h, 1), L.bgabp_shard_x(h, 0),
+                                L.bgabp_shard_x(h, 1))
+
+    for k in range(P):
+        Lk = layouts[k]
+        lower = bufs(k - 1) if k > 0 else None
+        upper = bufs(k + 1) if k + 1 < P else None
+        lo_n = layouts[k - 1].n_local if k > 0 else 0
+        up_n = layouts[k + 1].n_local if k + 1 < P else 0
+        lo_d = Lk.glo - layouts[k - 1].glo if k > 0 else 0
+        up_d = Lk.glo - layouts[k + 1].glo if k + 1 < P else 0
+        xlo_end = layouts[k - 1].ghi - Lk.glo if k > 0 else 0          # own nodes in the lower one's halo
+        xhi_begin = layouts[k + 1].glo - Lk.glo if k + 1 < P else Lk.n_local  # ... in the upper one's
+        _raise(L.bgabp_shard_set_peers(shards[k].eng.handle, P, k, lower, lo_n, lo_d, upper, up_n, up_d,
+                                       xlo_end, xhi_begin, slot_arr), "set peers")
+
+
+def sharded_solve_p2p(shards: dict, layouts, b_inf, opt: GabpOptions, poll_every=16):
+    """The sharded flood solve with the halo exchange and the stop-word reduction done by the
+    step kernels themselves through peer memory (no pack / unpack kernels, no collective, no host
+    synchronisation inside the loop): per iteration every shard enqueues its fused step (+ peer
+    stores) and fold, then waits on every other shard's step event and decides.  Bit-identical to
+    the single-engine solve.  Returns (status, iterations, detail, {shard: owned x}, history)."""
+    connect_peers(shards, layouts)
+    L = lib()
+    order = sorted(shards)
+    for k in order:
+        shards[k].begin(opt, b_inf)
+    t, cap = 1, opt.max_iter + 2
+    done = shards[order[0]].done()
+    while not done and t <= cap:
+        for k in order:
+            _raise(L.bgabp_shard_p2p_compute(shards[k].eng.handle), "p2p compute")
+        for k in order:
+            for q in order:
+                if q != k:
+                    _raise(L.bgabp_shard_p2p_wait(shards[k].eng.handle, shards[q].eng.handle), "p2p wait")
+            _raise(L.bgabp_shard_p2p_decide(shards[k].eng.handle), "p2p decide")
+        t += 1
+        if t % poll_every == 0 or t > cap:
+            done = shards[order[0]].done()
+    out, res = {}, None
+    for k in order:
+        status, its, detail, x, hist = shards[k].end(opt.max_iter)
+        out[k] = x
+        res = (status, its, detail, hist)
+    return res[0], res[1], res[2], out, res[3]

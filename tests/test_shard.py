@@ -206,3 +206,37 @@ def test_gpu_shards_match_single_engine(name):
     status, its, detail, xs, hist = sharded_solve(shards, layouts, [0] * count, 1, _r0(b), opt)
     rep = GabpEngine(A, Layout.Dia).solve(b, GSchedule.parallel_flood(), opt)
     _assert_same(rep, status, its, detail, _gather(layouts, xs), hist)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", sorted(PROBLEMS))
+def test_gpu_peer_shards_match_single_engine(name):
+    """The peer-memory step (halo messages and x stored by the step kernel into the neighbour's
+    buffers, stop words into every shard's slots; bgabp_shard_p2p_*) against the single engine."""
+    from paper_1904_04093_b200.gabp import GabpEngine, Layout
+    from paper_1904_04093_b200.gabp import Schedule as GSchedule
+    from paper_1904_04093_b200.shard import GpuShard, sharded_solve_p2p
+    build, align, count, opt = PROBLEMS[name]
+    A = build()
+    b = _rhs(A.n)
+    layouts = ShardLayout.partition(A.n, dia_halo(A), count, align=align)
+    shards = _shards(A, b, layouts, range(count), GpuShard)
+    status, its, detail, xs, hist = sharded_solve_p2p(shards, layouts, _r0(b), opt)
+    rep = GabpEngine(A, Layout.Dia).solve(b, GSchedule.parallel_flood(), opt)
+    _assert_same(rep, status, its, detail, _gather(layouts, xs), hist)
+
+
+@pytest.mark.gpu
+def test_gpu_peer_shards_config2_slab():
+    """Eight peer-connected shards of a 512 x 512 Poisson system (the config-2 operator), 300
+    iterations: bit-identical to the single engine."""
+    import paper_1904_04093_b200 as g
+    from paper_1904_04093_b200.shard import GpuShard, sharded_solve_p2p
+    A = g.poisson5(512, 512)
+    b = _rhs(A.n, 11)
+    opt = GabpOptions(tol=0.0, max_iter=300)
+    layouts = ShardLayout.partition(A.n, dia_halo(A), 8, align=512)
+    shards = _shards(A, b, layouts, range(8), GpuShard)
+    status, its, detail, xs, hist = sharded_solve_p2p(shards, layouts, _r0(b), opt)
+    rep = g.GabpEngine(A).solve(b, g.Schedule.parallel_flood(), opt)
+    _assert_same(rep, status, its, detail, _gather(layouts, xs), hist)
