@@ -183,7 +183,15 @@ int bgabp_shard_set_peers(bgabp_engine* e, int nranks, int rank, void* const* lo
                           void* const* slots);
 int bgabp_shard_p2p_compute(bgabp_engine* e);
 int bgabp_shard_p2p_wait(bgabp_engine* e, bgabp_engine* other);
-int bgabp_shard_p2p_decide(bgabp_engine* e);
+/* spin = 0: the caller ordered this stream after every other shard's step (bgabp_shard_p2p_wait,
+ * shards of one process); spin = 1: wait on the device for the other shards' step flags (shards
+ * in other processes, slot arrays mapped with bgabp_ipc_*; ~20 s timeout -> Diverged "peer shard
+ * timeout") */
+int bgabp_shard_p2p_decide(bgabp_engine* e, int spin);
+/* CUDA IPC of device allocations (64-byte handles) for shards in different processes */
+int bgabp_ipc_get(const void* dev_ptr, void* handle_out);
+int bgabp_ipc_open(const void* handle, void** dev_ptr);
+int bgabp_ipc_close(void* dev_ptr);
 
 /* residual_inf_norm(A, x, b) (sparse.cpp:104-115) on the handle's matrix */
 int bgabp_residual_inf_norm(bgabp_engine* e, const double* x, const double* b, double* out);

@@ -944,6 +944,8 @@ void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bga
         ck(cudaMemsetAsync(d_xf, 0, sizeof(double) * kXRing2 * (size_t)std::max(n, 1), st), "memset x ring");
     }
     ck(cudaMemsetAsync(d_spread, 0, sizeof(unsigned long long) * 8 * kSpread, st), "memset");
+    if (d_slots)  // peer-memory shards: words and step flags of the previous solve
+        ck(cudaMemsetAsync(d_slots, 0, sizeof(unsigned long long) * (kSlotWords + kMaxShards), st), "memset");
     if (solve_rb) ck(cudaMemsetAsync(d_rbmsg, 0, sizeof(double2) * 4 * (size_t)std::max(n, 2), st), "memset");
     solve_pipe = solve_seq && pipe_fits();
     if (solve_pipe) {  // pipelined lexicographic sweeps: x(0) = 0 in ring slot 0
@@ -1235,6 +1237,7 @@ void Engine::solve_report(bgabp_report& rep, std::string& detail) {
                 pivot = true;
                 break;
             case 3: detail = "residual blowup"; break;
+            case 5: detail = "peer shard timeout"; break;
             case 4: detail = ordered_detail(solve_levels->order, c.detail_key); pivot = true; break;
         }
     }
@@ -1979,7 +1982,7 @@ int bgabp_shard_peer_slots(bgabp_engine* h, void** slots) {
     ABI_GUARD(nullptr, 0, {
         Engine& E = h->E;
         if (!E.d_slots) {
-            const size_t bytes = sizeof(unsigned long long) * kMaxShards * 2 * 4;
+            const size_t bytes = sizeof(unsigned long long) * (kSlotWords + kMaxShards);
             E.d_slots = static_cast<unsigned long long*>(E.dalloc(bytes));
             ck(cudaMemsetAsync(E.d_slots, 0, bytes, E.st), "memset");
         }
@@ -2043,11 +2046,37 @@ int bgabp_shard_p2p_wait(bgabp_engine* h, bgabp_engine* other) {
     })
 }
 
-int bgabp_shard_p2p_decide(bgabp_engine* h) {
+int bgabp_shard_p2p_decide(bgabp_engine* h, int spin) {
     ABI_GUARD(nullptr, 0, {
         Engine& E = h->E;
-        k_shard_decide_p2p<<<1, 1, 0, E.st>>>(E.d_ctrl, E.d_hist, E.d_slots, E.peer.nranks, E.d_red4);
+        k_shard_decide_p2p<<<1, 1, 0, E.st>>>(E.d_ctrl, E.d_hist, E.d_slots, E.peer.nranks, E.d_red4, E.peer.rank,
+                                              spin);
         ck(cudaGetLastError(), "shard p2p decide");
+        return BGABP_OK;
+    })
+}
+
+// CUDA IPC for shards in different processes (one process per GPU): export / open the device
+// allocations a neighbour stores into (message buffers, x ring base, slot array)
+int bgabp_ipc_get(const void* dev_ptr, void* handle_out) {
+    ABI_GUARD(nullptr, 0, {
+        cudaIpcMemHandle_t hd;
+        ck(cudaIpcGetMemHandle(&hd, const_cast<void*>(dev_ptr)), "cudaIpcGetMemHandle");
+        std::memcpy(handle_out, &hd, sizeof hd);
+        return BGABP_OK;
+    })
+}
+int bgabp_ipc_open(const void* handle, void** dev_ptr) {
+    ABI_GUARD(nullptr, 0, {
+        cudaIpcMemHandle_t hd;
+        std::memcpy(&hd, handle, sizeof hd);
+        ck(cudaIpcOpenMemHandle(dev_ptr, hd, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+        return BGABP_OK;
+    })
+}
+int bgabp_ipc_close(void* dev_ptr) {
+    ABI_GUARD(nullptr, 0, {
+        ck(cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle");
         return BGABP_OK;
     })
 }

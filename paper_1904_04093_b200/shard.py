@@ -295,7 +295,7 @@ def connect_peers(shards: dict, layouts):
                                        xlo_end, xhi_begin, slot_arr), "set peers")
 
 
-def sharded_solve_p2p(shards: dict, layouts, b_inf, opt: GabpOptions, poll_every=16):
+def sharded_solve_p2p(shards: dict, layouts, b_inf, opt: GabpOptions, poll_every=16, spin=False):
     """The sharded flood solve with the halo exchange and the stop-word reduction done by the
     step kernels themselves through peer memory (no pack / unpack kernels, no collective, no host
     synchronisation inside the loop): per iteration every shard enqueues its fused step (+ peer
@@ -306,16 +306,19 @@ def sharded_solve_p2p(shards: dict, layouts, b_inf, opt: GabpOptions, poll_every
     order = sorted(shards)
     for k in order:
         shards[k].begin(opt, b_inf)
+    shards[order[0]].torch.cuda.synchronize()  # every shard reset before any peer stores into it
     t, cap = 1, opt.max_iter + 2
     done = shards[order[0]].done()
     while not done and t <= cap:
         for k in order:
             _raise(L.bgabp_shard_p2p_compute(shards[k].eng.handle), "p2p compute")
+        if spin:  # the device-flag wait of the multi-process path, exercised with every flag already set
+            shards[order[0]].torch.cuda.synchronize()
         for k in order:
             for q in order:
-                if q != k:
+                if q != k and not spin:
                     _raise(L.bgabp_shard_p2p_wait(shards[k].eng.handle, shards[q].eng.handle), "p2p wait")
-            _raise(L.bgabp_shard_p2p_decide(shards[k].eng.handle), "p2p decide")
+            _raise(L.bgabp_shard_p2p_decide(shards[k].eng.handle, 1 if spin else 0), "p2p decide")
         t += 1
         if t % poll_every == 0 or t > cap:
             done = shards[order[0]].done()
@@ -325,3 +328,79 @@ def sharded_solve_p2p(shards: dict, layouts, b_inf, opt: GabpOptions, poll_every
         out[k] = x
         res = (status, its, detail, hist)
     return res[0], res[1], res[2], out, res[3]
+
+
+def sharded_solve_ipc(shard, layouts, b_inf, opt: GabpOptions, poll_every=16, host_barrier=False):
+    """One shard per process (one process per GPU, torch.distributed initialised): the neighbours'
+    message buffers / x ring and every rank's slot array are mapped with CUDA IPC once, then each
+    iteration is the peer-memory step (halos and stop words stored by the kernels into the
+    peers' memory) followed by a device-side wait on the peers' step flags -- no host
+    synchronisation and no collective inside the loop.  host_barrier=True puts a host barrier
+    between the steps and the decisions (every peer flag is already set when a decision runs):
+    the mode for ranks sharing one GPU, where device-side waits between processes must not be
+    used.  Returns (status, iterations, detail, owned x, history)."""
+    import torch
+    import torch.distributed as dist
+    L = lib()
+    rank, P = dist.get_rank(), dist.get_world_size()
+    if len(layouts) != P:
+        raise ValueError("sharded_solve_ipc: one shard per rank")
+    h = shard.eng.handle
+    slots = C.c_void_p()
+    _raise(L.bgabp_shard_peer_slots(h, C.byref(slots)), "peer slots")
+
+    def export(ptr):
+        buf = C.create_string_buffer(64)
+        _raise(L.bgabp_ipc_get(C.c_void_p(ptr), buf), "ipc get")
+        return buf.raw
+
+    mine = {"msg0": export(L.bgabp_shard_msg(h, 0)), "msg1": export(L.bgabp_shard_msg(h, 1)),
+            "x": export(L.bgabp_shard_x(h, 0)), "slots": export(slots.value)}
+    peers = [None] * P
+    dist.all_gather_object(peers, mine)
+    opened = []
+
+    def imp(handle):
+        p = C.c_void_p()
+        _raise(L.bgabp_ipc_open(handle, C.byref(p)), "ipc open")
+        opened.append(p.value)
+        return p.value
+
+    slot_ptrs = [slots.value if q == rank else imp(peers[q]["slots"]) for q in range(P)]
+
+    def nbr(q):
+        xb = imp(peers[q]["x"])
+        return (C.c_void_p * 4)(imp(peers[q]["msg0"]), imp(peers[q]["msg1"]), xb, xb + 8 * layouts[q].n_local)
+
+    Lk = layouts[rank]
+    lower = nbr(rank - 1) if rank > 0 else None
+    upper = nbr(rank + 1) if rank + 1 < P else None
+    _raise(L.bgabp_shard_set_peers(h, P, rank, lower, layouts[rank - 1].n_local if rank > 0 else 0,
+                                   Lk.glo - layouts[rank - 1].glo if rank > 0 else 0, upper,
+                                   layouts[rank + 1].n_local if rank + 1 < P else 0,
+                                   Lk.glo - layouts[rank + 1].glo if rank + 1 < P else 0,
+                                   layouts[rank - 1].ghi - Lk.glo if rank > 0 else 0,
+                                   layouts[rank + 1].glo - Lk.glo if rank + 1 < P else Lk.n_local,
+                                   (C.c_void_p * P)(*slot_ptrs)), "set peers")
+    shard.begin(opt, b_inf)  # zeroes this rank's buffers and slots
+    torch.cuda.synchronize()
+    dist.barrier()  # nobody stores into a peer before every peer has been reset
+    t, cap = 1, opt.max_iter + 2
+    done = shard.done()
+    try:
+        while not done and t <= cap:
+            _raise(L.bgabp_shard_p2p_compute(h), "p2p compute")
+            if host_barrier:
+                torch.cuda.synchronize()
+                dist.barrier()
+            _raise(L.bgabp_shard_p2p_decide(h, 1), "p2p decide")
+            t += 1
+            if t % poll_every == 0 or t > cap or host_barrier:
+                done = shard.done()
+        out = shard.end(opt.max_iter)
+    finally:
+        torch.cuda.synchronize()
+        dist.barrier()  # every peer is done storing before the mappings go
+        for p in opened:
+            L.bgabp_ipc_close(C.c_void_p(p))
+    return out

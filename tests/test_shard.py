@@ -210,7 +210,8 @@ def test_gpu_shards_match_single_engine(name):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", sorted(PROBLEMS))
-def test_gpu_peer_shards_match_single_engine(name):
+@pytest.mark.parametrize("spin", [False, True])
+def test_gpu_peer_shards_match_single_engine(name, spin):
     """The peer-memory step (halo messages and x stored by the step kernel into the neighbour's
     buffers, stop words into every shard's slots; bgabp_shard_p2p_*) against the single engine."""
     from paper_1904_04093_b200.gabp import GabpEngine, Layout
@@ -221,7 +222,7 @@ def test_gpu_peer_shards_match_single_engine(name):
     b = _rhs(A.n)
     layouts = ShardLayout.partition(A.n, dia_halo(A), count, align=align)
     shards = _shards(A, b, layouts, range(count), GpuShard)
-    status, its, detail, xs, hist = sharded_solve_p2p(shards, layouts, _r0(b), opt)
+    status, its, detail, xs, hist = sharded_solve_p2p(shards, layouts, _r0(b), opt, spin=spin)
     rep = GabpEngine(A, Layout.Dia).solve(b, GSchedule.parallel_flood(), opt)
     _assert_same(rep, status, its, detail, _gather(layouts, xs), hist)
 
@@ -240,3 +241,54 @@ def test_gpu_peer_shards_config2_slab():
     status, its, detail, xs, hist = sharded_solve_p2p(shards, layouts, _r0(b), opt)
     rep = g.GabpEngine(A).solve(b, g.Schedule.parallel_flood(), opt)
     _assert_same(rep, status, its, detail, _gather(layouts, xs), hist)
+
+
+def _ipc_worker(rank, world, port, name, q):
+    """One process per shard, CUDA IPC mappings, host barrier between steps and decisions (the
+    ranks share one GPU: device-side waits between processes are not used here)."""
+    import torch
+    import torch.distributed as dist
+    from paper_1904_04093_b200.shard import GpuShard, sharded_solve_ipc
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        build, align, count, opt = PROBLEMS[name]
+        A = build()
+        b = _rhs(A.n)
+        layouts = ShardLayout.partition(A.n, dia_halo(A), world, align=align)
+        L = layouts[rank]
+        shard = GpuShard(local_matrix(A, L), L, b[L.glo:L.ghi])
+        status, its, detail, x, hist = sharded_solve_ipc(shard, layouts, _r0(b), opt, host_barrier=True)
+        q.put((rank, status, its, detail, {rank: x}, hist))
+        torch.cuda.synchronize()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["grid5_sym", "grid5_nonsym", "grid7"])
+def test_gpu_ipc_ranks_match_single_engine(name):
+    """Two processes, one shard each, neighbour buffers and slot arrays mapped with CUDA IPC."""
+    import torch.multiprocessing as mp
+    from paper_1904_04093_b200.gabp import GabpEngine, Layout
+    from paper_1904_04093_b200.gabp import Schedule as GSchedule
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, name, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    build, align, count, opt = PROBLEMS[name]
+    A = build()
+    b = _rhs(A.n)
+    layouts = ShardLayout.partition(A.n, dia_halo(A), 2, align=align)
+    xs = {}
+    for rank, status, its, detail, x, hist in outs:
+        xs.update(x)
+    assert outs[0][1:4] == outs[1][1:4]
+    rep = GabpEngine(A, Layout.Dia).solve(b, GSchedule.parallel_flood(), opt)
+    _assert_same(rep, outs[0][1], outs[0][2], outs[0][3], _gather(layouts, xs), outs[0][5])
