@@ -188,6 +188,9 @@ int bgabp_shard_p2p_wait(bgabp_engine* e, bgabp_engine* other);
  * in other processes, slot arrays mapped with bgabp_ipc_*; ~20 s timeout -> Diverged "peer shard
  * timeout") */
 int bgabp_shard_p2p_decide(bgabp_engine* e, int spin);
+/* nsteps iterations of the peer-memory solve for the shards of one process (event-ordered);
+ * use_graph: replay 16-iteration chunks from a CUDA graph captured across the shards' streams */
+int bgabp_shard_p2p_steps(bgabp_engine* const* shards, int count, int nsteps, int use_graph);
 /* CUDA IPC of device allocations (64-byte handles) for shards in different processes */
 int bgabp_ipc_get(const void* dev_ptr, void* handle_out);
 int bgabp_ipc_open(const void* handle, void** dev_ptr);

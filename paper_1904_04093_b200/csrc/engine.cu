@@ -62,9 +62,15 @@ T* Engine::upload(const std::vector<T>& v) {
     return d;
 }
 
+void Engine::drop_graphs() {
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    graphs.clear();
+    p2p_forget(this);
+}
+
 Engine::~Engine() {
     if (st) cudaStreamSynchronize(st);
-    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    drop_graphs();
     for (void* p : allocs) cudaFree(p);
     if (h_ctrl) cudaFreeHost(h_ctrl);
     if (h_poll) cudaFreeHost(h_poll);
@@ -72,6 +78,34 @@ Engine::~Engine() {
     for (auto& e : poll_ev)
         if (e) cudaEventDestroy(e);
     if (st && own_stream) cudaStreamDestroy(st);
+}
+
+// captured multi-shard peer-memory iterations (bgabp_shard_p2p_steps), dropped with any of their
+// engines or when one of them reallocates a captured buffer
+struct P2PGraph {
+    std::vector<Engine*> engines;
+    std::vector<long long> gens;
+    cudaGraphExec_t exec = nullptr;
+    std::vector<cudaEvent_t> join;
+    cudaEvent_t fork = nullptr;
+};
+static std::vector<P2PGraph>& p2p_graphs() {
+    static std::vector<P2PGraph>* g = new std::vector<P2PGraph>();
+    return *g;
+}
+void p2p_forget(Engine* e) {
+    auto& all = p2p_graphs();
+    for (size_t i = 0; i < all.size();) {
+        if (std::find(all[i].engines.begin(), all[i].engines.end(), e) != all[i].engines.end()) {
+            if (all[i].exec) cudaGraphExecDestroy(all[i].exec);
+            for (auto ev : all[i].join)
+                if (ev) cudaEventDestroy(ev);
+            if (all[i].fork) cudaEventDestroy(all[i].fork);
+            all.erase(all.begin() + i);
+        } else {
+            ++i;
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -685,6 +719,7 @@ const Levels& Engine::levels_for(const bgabp_schedule& s) {
     if (it != level_cache.end()) {
         if (s.kind != BGABP_SCHED_CUSTOM || (s.order && std::equal(s.order, s.order + n, it->second->order.begin())))
             return *it->second;
+        drop_graphs();  // graphs captured with these levels (their key is the Levels address)
         level_cache.erase(it);
     }
     std::vector<int> order = schedule_order(s);
@@ -926,7 +961,12 @@ void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bga
     solve_max_iter = o.max_iter;
     if (hist_cap < (long long)std::max(o.max_iter, 0) + 2) {
         hist_cap = (long long)std::max(o.max_iter, 0) + 2;
+        // captured solve graphs hold the old history pointer: drop them with it
+        ck(cudaStreamSynchronize(st), "sync");
+        drop_graphs();
+        if (d_hist) dfree(d_hist);
         d_hist = static_cast<double*>(dalloc(sizeof(double) * hist_cap));
+        ++hist_gen;
     }
     Ctrl c;
     std::memset(&c, 0, sizeof(c));
@@ -2052,6 +2092,87 @@ int bgabp_shard_p2p_decide(bgabp_engine* h, int spin) {
         k_shard_decide_p2p<<<1, 1, 0, E.st>>>(E.d_ctrl, E.d_hist, E.d_slots, E.peer.nranks, E.d_red4, E.peer.rank,
                                               spin);
         ck(cudaGetLastError(), "shard p2p decide");
+        return BGABP_OK;
+    })
+}
+
+// nsteps iterations of the peer-memory solve for `count` shards of one process (event-ordered),
+// replayed from a CUDA graph of 16 iterations captured across all shards' streams (the kernels
+// read the iteration index from the device, so one graph serves every position in the loop)
+
+static void p2p_enqueue_iteration(bgabp_engine* const* sh, int count) {
+    for (int k = 0; k < count; ++k) {
+        Engine& E = sh[k]->E;
+        E.enqueue_fused_kernel();
+        k_shard_fold_p2p<<<1, kSpread, 0, E.st>>>(E.d_ctrl, E.d_spread, E.d_red4, E.peer);
+        ck(cudaEventRecord(E.step_ev, E.st), "event");
+    }
+    for (int k = 0; k < count; ++k) {
+        Engine& E = sh[k]->E;
+        for (int q = 0; q < count; ++q)
+            if (q != k) ck(cudaStreamWaitEvent(E.st, sh[q]->E.step_ev, 0), "wait");
+        k_shard_decide_p2p<<<1, 1, 0, E.st>>>(E.d_ctrl, E.d_hist, E.d_slots, E.peer.nranks, E.d_red4, E.peer.rank, 0);
+    }
+}
+
+int bgabp_shard_p2p_steps(bgabp_engine* const* shards, int count, int nsteps, int use_graph) {
+    ABI_GUARD(nullptr, 0, {
+        if (count < 1) throw InvalidArg("shard: no shards");
+        for (int k = 0; k < count; ++k)
+            if (!shards[k]->E.solve_fused || !shards[k]->E.peer_on)
+                throw InvalidArg("shard: call set_peers and shard_solve_begin first");
+        constexpr int kChunk = 16;
+        P2PGraph* g = nullptr;
+        if (use_graph && nsteps >= kChunk) {
+            auto& all = p2p_graphs();
+            for (auto& c : all) {
+                if (c.engines.size() != (size_t)count) continue;
+                bool same = true;
+                for (int k = 0; k < count && same; ++k)
+                    same = c.engines[k] == &shards[k]->E && c.gens[k] == shards[k]->E.hist_gen;
+                if (same) g = &c;
+            }
+            if (!g) {
+                P2PGraph c;
+                for (int k = 0; k < count; ++k) {
+                    c.engines.push_back(&shards[k]->E);
+                    c.gens.push_back(shards[k]->E.hist_gen);
+                }
+                ck(cudaEventCreateWithFlags(&c.fork, cudaEventDisableTiming), "event");
+                c.join.resize(count);
+                for (auto& e : c.join) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+                cudaStream_t s0 = shards[0]->E.st;
+                cudaGraph_t graph;
+                ck(cudaStreamBeginCapture(s0, cudaStreamCaptureModeThreadLocal), "capture");
+                ck(cudaEventRecord(c.fork, s0), "fork");
+                for (int k = 1; k < count; ++k) ck(cudaStreamWaitEvent(shards[k]->E.st, c.fork, 0), "fork wait");
+                for (int i = 0; i < kChunk; ++i) p2p_enqueue_iteration(shards, count);
+                for (int k = 1; k < count; ++k) {
+                    ck(cudaEventRecord(c.join[k], shards[k]->E.st), "join");
+                    ck(cudaStreamWaitEvent(s0, c.join[k], 0), "join wait");
+                }
+                ck(cudaStreamEndCapture(s0, &graph), "capture end");
+                ck(cudaGraphInstantiate(&c.exec, graph, 0), "graph instantiate");
+                cudaGraphDestroy(graph);
+                all.push_back(std::move(c));
+                g = &all.back();
+            }
+        }
+        int left = nsteps;
+        while (g && left >= kChunk) {
+            // order the graph after everything already on the other shards' streams, and them after it
+            cudaStream_t s0 = shards[0]->E.st;
+            for (int k = 1; k < count; ++k) {
+                ck(cudaEventRecord(g->join[k], shards[k]->E.st), "pre");
+                ck(cudaStreamWaitEvent(s0, g->join[k], 0), "pre wait");
+            }
+            ck(cudaGraphLaunch(g->exec, s0), "graph launch");
+            ck(cudaEventRecord(g->fork, s0), "post");
+            for (int k = 1; k < count; ++k) ck(cudaStreamWaitEvent(shards[k]->E.st, g->fork, 0), "post wait");
+            left -= kChunk;
+        }
+        for (; left > 0; --left) p2p_enqueue_iteration(shards, count);
+        ck(cudaGetLastError(), "p2p steps");
         return BGABP_OK;
     })
 }

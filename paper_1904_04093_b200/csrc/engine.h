@@ -27,6 +27,8 @@ struct CudaError : std::runtime_error {
 };
 
 void put_err(char* err, size_t len, const std::string& s);
+struct Engine;
+void p2p_forget(Engine* e);  // drop captured multi-shard graphs that use this engine
 // host <-> device copies of caller buffers: direct when pinned, staged (parallel) when pageable
 void host_to_device(void* dst, const void* src, size_t bytes, cudaStream_t st);
 void device_to_host(void* dst, const void* src, size_t bytes, cudaStream_t st);
@@ -83,6 +85,8 @@ struct Engine {
 
     unsigned long long* d_spread = nullptr;  // per-warp max slots of the fused solve step
     long long hist_cap = 0;
+    long long hist_gen = 0;  // bumped when d_hist is reallocated (captured graphs hold the pointer)
+    void drop_graphs();
     double *d_lam = nullptr, *d_lsrc = nullptr, *d_sigma = nullptr;
     bool has_frozen = false;
     std::vector<void*> allocs;

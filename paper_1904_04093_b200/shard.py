@@ -295,7 +295,7 @@ def connect_peers(shards: dict, layouts):
                                        xlo_end, xhi_begin, slot_arr), "set peers")
 
 
-def sharded_solve_p2p(shards: dict, layouts, b_inf, opt: GabpOptions, poll_every=16, spin=False):
+def sharded_solve_p2p(shards: dict, layouts, b_inf, opt: GabpOptions, poll_every=16, spin=False, graph=False):
     """The sharded flood solve with the halo exchange and the stop-word reduction done by the
     step kernels themselves through peer memory (no pack / unpack kernels, no collective, no host
     synchronisation inside the loop): per iteration every shard enqueues its fused step (+ peer
@@ -309,6 +309,13 @@ def sharded_solve_p2p(shards: dict, layouts, b_inf, opt: GabpOptions, poll_every
     shards[order[0]].torch.cuda.synchronize()  # every shard reset before any peer stores into it
     t, cap = 1, opt.max_iter + 2
     done = shards[order[0]].done()
+    if graph:  # whole chunks of iterations from a CUDA graph across the shards' streams
+        arr = (C.c_void_p * len(order))(*[shards[k].eng.handle.value for k in order])
+        chunk = 4 * 16
+        while not done and t <= cap:
+            _raise(L.bgabp_shard_p2p_steps(arr, len(order), chunk, 1), "p2p steps")
+            t += chunk
+            done = shards[order[0]].done()
     while not done and t <= cap:
         for k in order:
             _raise(L.bgabp_shard_p2p_compute(shards[k].eng.handle), "p2p compute")

@@ -380,3 +380,19 @@ def test_sequential_pipeline_pivot_stop_returns_the_partial_x(orc, ref):
     got = g.GabpEngine(A).solve(b, g.Schedule.sequential(), g.GabpOptions(tol=1e-10, max_iter=100))
     assert want.status == 1 and "pivot" in want.detail
     _same_report(got, want)
+
+
+@pytest.mark.parametrize("sched", ["flood", "rb", "seq"])
+def test_solve_history_after_growing_max_iter(orc, sched):
+    """A second solve with a larger max_iter on the same engine (the history buffer grows; solve
+    graphs captured by the first call must not keep writing into the old one) equals the oracle."""
+    A = orc.poisson5(40, 30)
+    b = orc.rng(21).vector(A.n)
+    s = {"flood": OSched.parallel_flood(), "rb": OSched.red_black_grid(40, 30), "seq": OSched.sequential()}[sched]
+    eng = g.GabpEngine(A)
+    eng.solve(b, gsched(s), g.GabpOptions(tol=0.0, max_iter=40))
+    rep = eng.solve(b, gsched(s), g.GabpOptions(tol=0.0, max_iter=600))
+    want = orc.engine(A).solve(b, s, tol=0.0, max_iter=600)
+    assert (int(rep.status), rep.iterations) == (want.status, want.iterations)
+    assert np.array_equal(rep.residual_history, want.residual_history)
+    assert np.array_equal(rep.solution, want.solution)

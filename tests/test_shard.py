@@ -210,8 +210,8 @@ def test_gpu_shards_match_single_engine(name):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", sorted(PROBLEMS))
-@pytest.mark.parametrize("spin", [False, True])
-def test_gpu_peer_shards_match_single_engine(name, spin):
+@pytest.mark.parametrize("mode", ["event", "spin", "graph"])
+def test_gpu_peer_shards_match_single_engine(name, mode):
     """The peer-memory step (halo messages and x stored by the step kernel into the neighbour's
     buffers, stop words into every shard's slots; bgabp_shard_p2p_*) against the single engine."""
     from paper_1904_04093_b200.gabp import GabpEngine, Layout
@@ -222,7 +222,8 @@ def test_gpu_peer_shards_match_single_engine(name, spin):
     b = _rhs(A.n)
     layouts = ShardLayout.partition(A.n, dia_halo(A), count, align=align)
     shards = _shards(A, b, layouts, range(count), GpuShard)
-    status, its, detail, xs, hist = sharded_solve_p2p(shards, layouts, _r0(b), opt, spin=spin)
+    status, its, detail, xs, hist = sharded_solve_p2p(shards, layouts, _r0(b), opt, spin=mode == "spin",
+                                                      graph=mode == "graph")
     rep = GabpEngine(A, Layout.Dia).solve(b, GSchedule.parallel_flood(), opt)
     _assert_same(rep, status, its, detail, _gather(layouts, xs), hist)
 
@@ -238,7 +239,7 @@ def test_gpu_peer_shards_config2_slab():
     opt = GabpOptions(tol=0.0, max_iter=300)
     layouts = ShardLayout.partition(A.n, dia_halo(A), 8, align=512)
     shards = _shards(A, b, layouts, range(8), GpuShard)
-    status, its, detail, xs, hist = sharded_solve_p2p(shards, layouts, _r0(b), opt)
+    status, its, detail, xs, hist = sharded_solve_p2p(shards, layouts, _r0(b), opt, graph=True)
     rep = g.GabpEngine(A).solve(b, g.Schedule.parallel_flood(), opt)
     _assert_same(rep, status, its, detail, _gather(layouts, xs), hist)
 
