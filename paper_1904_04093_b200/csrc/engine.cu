@@ -1027,20 +1027,22 @@ void Engine::enqueue_step() {
 template <int SS, int MB, bool DF>
 static void launch_sharded_step(Engine& E, unsigned g, bool dl) {
     double *x0 = E.d_xf, *x1 = E.d_xf + E.n;
-#define SHARDED_STEP(DL_, SYM_, PEER_)                                                                          \
-    k_flood_solve_dia<SS, DL_, SYM_, MB, DF, true, false, true, PEER_><<<g, 256, 0, E.st>>>(                   \
+#define SHARDED_STEP(DL_, SYM_, PEER_, UNIF_)                                                                   \
+    k_flood_solve_dia<SS, DL_, SYM_, MB, DF, true, UNIF_, true, PEER_><<<g, 256, 0, E.st>>>(                   \
         E.dia, E.solve_b, E.d_msg[0], E.d_msg[1], x0, x1, E.d_ctrl, E.d_spread, E.peer)
-    if (E.peer_on) {
+    if (E.peer_on && E.dia.uniform) {  // constant stencil: coefficients and diagonal as parameters
+        if (dl) SHARDED_STEP(true, true, true, true); else SHARDED_STEP(false, true, true, true);
+    } else if (E.peer_on) {
         if (E.symmetric) {
-            if (dl) SHARDED_STEP(true, true, true); else SHARDED_STEP(false, true, true);
+            if (dl) SHARDED_STEP(true, true, true, false); else SHARDED_STEP(false, true, true, false);
         } else {
-            if (dl) SHARDED_STEP(true, false, true); else SHARDED_STEP(false, false, true);
+            if (dl) SHARDED_STEP(true, false, true, false); else SHARDED_STEP(false, false, true, false);
         }
     } else {
         if (E.symmetric) {
-            if (dl) SHARDED_STEP(true, true, false); else SHARDED_STEP(false, true, false);
+            if (dl) SHARDED_STEP(true, true, false, false); else SHARDED_STEP(false, true, false, false);
         } else {
-            if (dl) SHARDED_STEP(true, false, false); else SHARDED_STEP(false, false, false);
+            if (dl) SHARDED_STEP(true, false, false, false); else SHARDED_STEP(false, false, false, false);
         }
     }
 #undef SHARDED_STEP
