@@ -317,17 +317,21 @@ struct Stager {
     std::mutex mu;
     void* buf[2] = {nullptr, nullptr};
     cudaEvent_t ev[2] = {nullptr, nullptr};
-    static constexpr size_t kChunk = size_t(32) << 20;
+    static constexpr size_t kMaxChunk = size_t(64) << 20;
+    size_t chunk = size_t(32) << 20;
+    int threads = 16;
     void init() {
         if (buf[0]) return;
+        if (const char* e = getenv("BGABP_STAGE_MB")) chunk = std::min(kMaxChunk, size_t(std::max(1, atoi(e))) << 20);
+        if (const char* e = getenv("BGABP_STAGE_THREADS")) threads = std::max(1, atoi(e));
         for (int k = 0; k < 2; ++k) {
-            ck(cudaMallocHost(&buf[k], kChunk), "cudaMallocHost");
+            ck(cudaMallocHost(&buf[k], chunk), "cudaMallocHost");
             ck(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming), "event");
         }
     }
 };
-void par_copy(char* dst, const char* src, size_t len) {
-    const int T = std::max(1, std::min(omp_get_max_threads(), 16));
+void par_copy(char* dst, const char* src, size_t len, int threads) {
+    const int T = std::max(1, std::min(omp_get_max_threads(), threads));
     const size_t piece = (len + T - 1) / T;
 #pragma omp parallel for num_threads(T) schedule(static)
     for (int t = 0; t < T; ++t) {
@@ -355,7 +359,6 @@ static bool is_pinned(const void* p) {
 // the DMA of the other.  On return the source may be reused.
 void host_to_device(void* dst, const void* src, size_t bytes, cudaStream_t st) {
     if (bytes == 0) return;
-    constexpr size_t kChunk = Stager::kChunk;
     if (bytes <= (size_t(1) << 20) || is_pinned(src)) {
         ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st), "H2D");
         return;
@@ -363,6 +366,7 @@ void host_to_device(void* dst, const void* src, size_t bytes, cudaStream_t st) {
     Stager& S = stager();
     std::lock_guard<std::mutex> lock(S.mu);
     S.init();
+    const size_t kChunk = S.chunk;
     const char* s = static_cast<const char*>(src);
     char* d = static_cast<char*>(dst);
     int k = 0;
@@ -370,7 +374,7 @@ void host_to_device(void* dst, const void* src, size_t bytes, cudaStream_t st) {
     for (size_t off = 0; off < bytes; off += kChunk, k ^= 1) {
         const size_t len = std::min(kChunk, bytes - off);
         if (used[k]) ck(cudaEventSynchronize(S.ev[k]), "stage wait");
-        par_copy(static_cast<char*>(S.buf[k]), s + off, len);
+        par_copy(static_cast<char*>(S.buf[k]), s + off, len, S.threads);
         ck(cudaMemcpyAsync(d + off, S.buf[k], len, cudaMemcpyHostToDevice, st), "H2D");
         ck(cudaEventRecord(S.ev[k], st), "event");
         used[k] = true;
@@ -384,7 +388,6 @@ void host_to_device(void* dst, const void* src, size_t bytes, cudaStream_t st) {
 // go through the stager and have landed in `dst` on return.
 void device_to_host(void* dst, const void* src, size_t bytes, cudaStream_t st) {
     if (bytes == 0) return;
-    constexpr size_t kChunk = Stager::kChunk;
     if (bytes <= (size_t(1) << 20) || is_pinned(dst)) {
         ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st), "D2H");
         return;
@@ -392,6 +395,7 @@ void device_to_host(void* dst, const void* src, size_t bytes, cudaStream_t st) {
     Stager& S = stager();
     std::lock_guard<std::mutex> lock(S.mu);
     S.init();
+    const size_t kChunk = S.chunk;
     const char* s = static_cast<const char*>(src);
     char* d = static_cast<char*>(dst);
     // chunk i lands in buffer i & 1; the host copy-out of chunk i overlaps the DMA of chunk i+1
@@ -406,7 +410,7 @@ void device_to_host(void* dst, const void* src, size_t bytes, cudaStream_t st) {
         if (i + 1 < nch) enqueue(i + 1);
         ck(cudaEventSynchronize(S.ev[i & 1]), "stage wait");
         const size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
-        par_copy(d + off, static_cast<const char*>(S.buf[i & 1]), len);
+        par_copy(d + off, static_cast<const char*>(S.buf[i & 1]), len, S.threads);
     }
 }
 
