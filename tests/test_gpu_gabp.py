@@ -396,3 +396,21 @@ def test_solve_history_after_growing_max_iter(orc, sched):
     assert (int(rep.status), rep.iterations) == (want.status, want.iterations)
     assert np.array_equal(rep.residual_history, want.residual_history)
     assert np.array_equal(rep.solution, want.solution)
+
+
+def test_solve_pinned_and_pageable_buffers_agree(orc):
+    """bgabp_solve copies caller buffers directly when they are pinned and through the staged
+    parallel path when pageable (large vectors): both give the oracle's x bit for bit."""
+    import torch
+    A = orc.poisson5(700, 600)  # 420k unknowns: 3.4 MB vectors take the staged path when pageable
+    b = orc.rng(3).vector(A.n)
+    opt = g.GabpOptions(tol=0.0, max_iter=60)
+    eng = g.GabpEngine(A)
+    rep_pageable = eng.solve(b, g.Schedule.parallel_flood(), opt)
+    b_pin = torch.from_numpy(b.copy()).pin_memory()
+    x_pin = torch.zeros(A.n, dtype=torch.float64).pin_memory()
+    rep_pinned = eng.solve(b_pin.numpy(), g.Schedule.parallel_flood(), opt, x_out=x_pin.numpy())
+    want = orc.engine(A).solve(b, OSched.parallel_flood(), tol=0.0, max_iter=60)
+    assert np.array_equal(rep_pageable.solution, want.solution)
+    assert np.array_equal(x_pin.numpy(), want.solution)
+    assert np.array_equal(rep_pinned.residual_history, want.residual_history)
