@@ -802,37 +802,38 @@ void Engine::launch_aggregate(const double* b, const double2* msg, double* x, do
     }
 }
 
-void Engine::launch_residual(const double* b, const double* x, double* r, unsigned long long* rmax, int mode) {
+void Engine::launch_residual(const double* b, const double* x, double* r, unsigned long long* rmax, int mode,
+                             long long xstride) {
     if (n == 0) return;
     const unsigned g = nblk(n);
     if (layout == BGABP_LAYOUT_DIA) {
         if (dia.uniform) {
-            DIA_SWITCH(S, k_residual_dia<SS, true, true><<<g, 256, 0, st>>>(dia, b, x, r, rmax, d_ctrl, mode));
+            DIA_SWITCH(S, k_residual_dia<SS, true, true><<<g, 256, 0, st>>>(dia, b, x, r, rmax, d_ctrl, mode, xstride));
         } else if (symmetric) {
-            DIA_SWITCH(S, k_residual_dia<SS, true><<<g, 256, 0, st>>>(dia, b, x, r, rmax, d_ctrl, mode));
+            DIA_SWITCH(S, k_residual_dia<SS, true><<<g, 256, 0, st>>>(dia, b, x, r, rmax, d_ctrl, mode, xstride));
         } else {
-            DIA_SWITCH(S, k_residual_dia<SS><<<g, 256, 0, st>>>(dia, b, x, r, rmax, d_ctrl, mode));
+            DIA_SWITCH(S, k_residual_dia<SS><<<g, 256, 0, st>>>(dia, b, x, r, rmax, d_ctrl, mode, xstride));
         }
     } else {
-        k_residual_csr<<<g, 256, 0, st>>>(csr, b, x, r, rmax, d_ctrl, mode);
+        k_residual_csr<<<g, 256, 0, st>>>(csr, b, x, r, rmax, d_ctrl, mode, xstride);
     }
 }
 
 void Engine::launch_levels(const Levels& L, const double* b, double2* msg, double* x, bool delta,
-                           unsigned long long* dslot, int mode) {
+                           unsigned long long* dslot, int mode, long long xstride) {
     for (size_t l = 0; l + 1 < L.ptr.size(); ++l) {
         const int cnt = L.ptr[l + 1] - L.ptr[l];
         const int* nodes = L.d_nodes + L.ptr[l];
         const int* npos = L.d_npos + L.ptr[l];
         const unsigned g = nblk(cnt);
         if (layout == BGABP_LAYOUT_DIA) {
-            DIA_SWITCH(S, if (delta) k_level_dia<SS, true><<<g, 256, 0, st>>>(dia, b, msg, x, nodes, npos, cnt, d_ctrl, dslot, mode);
-                       else k_level_dia<SS, false><<<g, 256, 0, st>>>(dia, b, msg, x, nodes, npos, cnt, d_ctrl, dslot, mode));
+            DIA_SWITCH(S, if (delta) k_level_dia<SS, true><<<g, 256, 0, st>>>(dia, b, msg, x, nodes, npos, cnt, d_ctrl, dslot, mode, xstride);
+                       else k_level_dia<SS, false><<<g, 256, 0, st>>>(dia, b, msg, x, nodes, npos, cnt, d_ctrl, dslot, mode, xstride));
         } else {
             if (delta)
-                k_level_csr<true><<<g, 256, 0, st>>>(csr, b, msg, x, nodes, npos, cnt, d_ctrl, dslot, mode);
+                k_level_csr<true><<<g, 256, 0, st>>>(csr, b, msg, x, nodes, npos, cnt, d_ctrl, dslot, mode, xstride);
             else
-                k_level_csr<false><<<g, 256, 0, st>>>(csr, b, msg, x, nodes, npos, cnt, d_ctrl, dslot, mode);
+                k_level_csr<false><<<g, 256, 0, st>>>(csr, b, msg, x, nodes, npos, cnt, d_ctrl, dslot, mode, xstride);
         }
     }
 }
@@ -982,6 +983,10 @@ void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bga
     for (int k = 0; k < 2; ++k)
         ck(cudaMemsetAsync(d_msg[k], 0, sizeof(double2) * (size_t)std::max<long long>(nslots, 1), st), "memset");
     ck(cudaMemsetAsync(d_x, 0, sizeof(double) * std::max(n, 1), st), "memset x");
+    if (!solve_flood && !solve_seq) {  // ordered solves on levels / red-black
+        if (!d_xord) d_xord = static_cast<double*>(dalloc(sizeof(double) * 2 * (size_t)std::max(n, 1)));
+        ck(cudaMemsetAsync(d_xord, 0, sizeof(double) * 2 * (size_t)std::max(n, 1), st), "memset x ring");
+    }
     if (solve_fused) {
         // kXRing2 slots: the two-iteration launch keeps x(k) in slot k % 4 (single steps use 0, 1)
         if (!d_xf) d_xf = static_cast<double*>(dalloc(sizeof(double) * kXRing2 * (size_t)std::max(n, 1)));
@@ -1169,15 +1174,21 @@ void Engine::enqueue_step_other() {
             ++pipe_next;
         }
     } else {
+        // x(t) goes to slot t & 1 of d_xord (the kernels pick the slot from the device's step), so a
+        // pivot stop still has x(t-1) for the reference's partly updated x (solve_x)
         if (solve_rb)
-            launch_rb_sweep(solve_b, d_x, false, solve_stop == BGABP_STOP_MESSAGE_DELTA, &d_ctrl->delta[0], MODE_SOLVE);
+            launch_rb_sweep(solve_b, d_xord, false, solve_stop == BGABP_STOP_MESSAGE_DELTA, &d_ctrl->delta[0], MODE_SOLVE,
+                            n);
         else if (solve_seq)  // grids too tall for the pipeline's x ring
             launch_seq_sweep(solve_b, d_msg[0], d_x, solve_stop == BGABP_STOP_MESSAGE_DELTA, &d_ctrl->delta[0],
                              MODE_SOLVE);
         else
-            launch_levels(*solve_levels, solve_b, d_msg[0], d_x, solve_stop == BGABP_STOP_MESSAGE_DELTA,
-                          &d_ctrl->delta[0], MODE_SOLVE);
-        launch_residual(solve_b, d_x, nullptr, nullptr, MODE_SOLVE_ORDERED);
+            launch_levels(*solve_levels, solve_b, d_msg[0], d_xord, solve_stop == BGABP_STOP_MESSAGE_DELTA,
+                          &d_ctrl->delta[0], MODE_SOLVE, n);
+        if (solve_seq)
+            launch_residual(solve_b, d_x, nullptr, nullptr, MODE_SOLVE_ORDERED);
+        else
+            launch_residual(solve_b, d_xord, nullptr, nullptr, MODE_SOLVE_ORDERED, n);
         k_solve_finalize_ordered<<<1, 1, 0, st>>>(d_ctrl, d_hist);
     }
 }
@@ -1307,7 +1318,28 @@ const double* Engine::solve_x() {
         }
         return xs;
     }
-    if (!solve_fused) return d_x;
+    if (!solve_fused && (solve_flood || solve_seq)) return d_x;
+    if (!solve_fused) {  // ordered (levels / red-black): x(k) in slot k & 1 of d_xord
+        const Ctrl& c = *h_ctrl;  // read by solve_report
+        const double* xs = d_xord + (size_t)(c.iterations & 1) * n;
+        if (c.status == BGABP_DIVERGED && c.detail_kind == 4 && n > 0 && solve_levels) {
+            // the reference's sweep stopped at visit position p (gabp.cpp:71-87): nodes visited
+            // before it (and the pivot node itself on an edge pivot, whose x-stage ran) hold x(k),
+            // the rest x(k-1)
+            const double* xo = d_xord + (size_t)((c.iterations + 1) & 1) * n;
+            std::vector<int> pos(n);
+            for (int q = 0; q < n; ++q) pos[solve_levels->order[q]] = q;
+            int* dpos = static_cast<int*>(dalloc(sizeof(int) * (size_t)n));
+            ck(cudaMemcpyAsync(dpos, pos.data(), sizeof(int) * (size_t)n, cudaMemcpyHostToDevice, st), "H2D");
+            const long long p = (long long)(c.detail_key >> 32) + ((c.detail_key & 0xffffffffu) ? 1 : 0);
+            k_compose_pos_x<<<nblk(n), 256, 0, st>>>(xs, xo, dpos, d_aux, n, p);
+            ck(cudaGetLastError(), "compose x");
+            ck(cudaStreamSynchronize(st), "sync");
+            dfree(dpos);
+            return d_aux;
+        }
+        return xs;
+    }
     const Ctrl& c = *h_ctrl;  // read by solve_report
     const int ring = solve_double ? kXRing2 : kXRing;
     const double* xs = d_xf + (size_t)(c.solx & (ring - 1)) * n;
@@ -1652,6 +1684,7 @@ int bgabp_layout_digest(bgabp_engine* h, unsigned long long* out) {
             mix_dev(E.dia.diag, sizeof(double) * (size_t)E.n);
         }
         E.ensure_csr2slot();
+        ck(cudaStreamSynchronize(E.st), "sync");  // built on the handle's (non-blocking) stream
         mix_dev(E.d_csr2slot, sizeof(long long) * (size_t)E.nnz);
         *out = f;
         return BGABP_OK;

@@ -82,6 +82,7 @@ struct Engine {
     double *d_b = nullptr, *d_x = nullptr, *d_r = nullptr, *d_e = nullptr, *d_aux = nullptr;
     double* d_hist = nullptr;
     double* d_xf = nullptr;          // fused flood solve: x(k) in ring slot k % kXRing ([kXRing][n])
+    double* d_xord = nullptr;        // ordered solves: x(k) in slot k & 1 ([2][n]); pivot stops compose
 
     unsigned long long* d_spread = nullptr;  // per-warp max slots of the fused solve step
     long long hist_cap = 0;
@@ -142,9 +143,10 @@ struct Engine {
 
     void launch_flood(const double* b, double2* m0, double2* m1, double* x, int mode, bool delta);
     void launch_aggregate(const double* b, const double2* msg, double* x, double* beta, unsigned long long* npiv);
-    void launch_residual(const double* b, const double* x, double* r, unsigned long long* rmax, int mode);
+    void launch_residual(const double* b, const double* x, double* r, unsigned long long* rmax, int mode,
+                         long long xstride = 0);
     void launch_levels(const Levels& L, const double* b, double2* msg, double* x, bool delta,
-                       unsigned long long* dslot, int mode);
+                       unsigned long long* dslot, int mode, long long xstride = 0);
     void launch_gs_levels(const Levels& L, const double* b, double* x);
     void launch_jacobi(const double* b, const double* x, double* xn);
 
@@ -156,7 +158,8 @@ struct Engine {
     bool rb_applicable(const bgabp_schedule& s) const;
     void rb_build(int nx, bool msgs = true);  // msgs: also the colour-compact message buffers
     void launch_gs_rb(const double* b, double* x);
-    void launch_rb_sweep(const double* b, double* x, bool cold, bool delta, unsigned long long* dslot, int mode);
+    void launch_rb_sweep(const double* b, double* x, bool cold, bool delta, unsigned long long* dslot, int mode,
+                         long long xstride = 0);
     void rb_state(bool to_compact, double2* natural);
     // cold smoothing with recorded lambda / sigma per sweep (multigrid smoother fast path)
     std::vector<double*> rb_lamrec, rb_sigrec;

@@ -61,31 +61,32 @@ void Engine::launch_gs_rb(const double* b, double* x) {
     if (rb.nB > 0) k_gs_rb_half<1><<<nblk_host(rb.nB), 256, 0, st>>>(rb, b, x, d_ctrl);
 }
 
-void Engine::launch_rb_sweep(const double* b, double* x, bool cold, bool delta, unsigned long long* dslot, int mode) {
+void Engine::launch_rb_sweep(const double* b, double* x, bool cold, bool delta, unsigned long long* dslot, int mode,
+                             long long xstride) {
     if (n == 0) return;
     double2* mR = d_rbmsg;
     double2* mB = d_rbmsg + 4 * (size_t)rb.nR;
     const unsigned gr = nblk_host(rb.nR), gb = nblk_host(std::max(rb.nB, 1));
     if (rb.uniform && !delta) {  // constant stencil: no coefficient / diagonal loads
         if (cold)
-            k_rb_half<0, true, false, true><<<gr, 256, 0, st>>>(rb, b, mR, mB, x, d_ctrl, dslot, mode);
+            k_rb_half<0, true, false, true><<<gr, 256, 0, st>>>(rb, b, mR, mB, x, d_ctrl, dslot, mode, xstride);
         else
-            k_rb_half<0, false, false, true><<<gr, 256, 0, st>>>(rb, b, mR, mB, x, d_ctrl, dslot, mode);
-        if (rb.nB > 0) k_rb_half<1, false, false, true><<<gb, 256, 0, st>>>(rb, b, mB, mR, x, d_ctrl, dslot, mode);
+            k_rb_half<0, false, false, true><<<gr, 256, 0, st>>>(rb, b, mR, mB, x, d_ctrl, dslot, mode, xstride);
+        if (rb.nB > 0) k_rb_half<1, false, false, true><<<gb, 256, 0, st>>>(rb, b, mB, mR, x, d_ctrl, dslot, mode, xstride);
         return;
     }
     if (delta) {
         if (cold)
-            k_rb_half<0, true, true><<<gr, 256, 0, st>>>(rb, b, mR, mB, x, d_ctrl, dslot, mode);
+            k_rb_half<0, true, true><<<gr, 256, 0, st>>>(rb, b, mR, mB, x, d_ctrl, dslot, mode, xstride);
         else
-            k_rb_half<0, false, true><<<gr, 256, 0, st>>>(rb, b, mR, mB, x, d_ctrl, dslot, mode);
-        if (rb.nB > 0) k_rb_half<1, false, true><<<gb, 256, 0, st>>>(rb, b, mB, mR, x, d_ctrl, dslot, mode);
+            k_rb_half<0, false, true><<<gr, 256, 0, st>>>(rb, b, mR, mB, x, d_ctrl, dslot, mode, xstride);
+        if (rb.nB > 0) k_rb_half<1, false, true><<<gb, 256, 0, st>>>(rb, b, mB, mR, x, d_ctrl, dslot, mode, xstride);
     } else {
         if (cold)
-            k_rb_half<0, true, false><<<gr, 256, 0, st>>>(rb, b, mR, mB, x, d_ctrl, dslot, mode);
+            k_rb_half<0, true, false><<<gr, 256, 0, st>>>(rb, b, mR, mB, x, d_ctrl, dslot, mode, xstride);
         else
-            k_rb_half<0, false, false><<<gr, 256, 0, st>>>(rb, b, mR, mB, x, d_ctrl, dslot, mode);
-        if (rb.nB > 0) k_rb_half<1, false, false><<<gb, 256, 0, st>>>(rb, b, mB, mR, x, d_ctrl, dslot, mode);
+            k_rb_half<0, false, false><<<gr, 256, 0, st>>>(rb, b, mR, mB, x, d_ctrl, dslot, mode, xstride);
+        if (rb.nB > 0) k_rb_half<1, false, false><<<gb, 256, 0, st>>>(rb, b, mB, mR, x, d_ctrl, dslot, mode, xstride);
     }
 }
 

@@ -46,9 +46,10 @@ __device__ __forceinline__ int rb_other(int g, int s, int nx) {
 template <int COLOUR, bool COLD, bool DELTA, bool UNIF = false>
 static __global__ void __launch_bounds__(256) k_rb_half(RbP P, const double* __restrict__ b, double2* mine,
                                                        double2* other, double* __restrict__ x, Ctrl* ctrl,
-                                                       unsigned long long* dslot, int mode) {
+                                                       unsigned long long* dslot, int mode, long long xstride = 0) {
     if (mode == MODE_SOLVE && ld_ctrl(&ctrl->done)) return;
     if (block_sees_failure(ctrl)) return;
+    if (mode == MODE_SOLVE && xstride && (ld_ctrl(&ctrl->step) & 1)) x += xstride;  // x(t) in ring slot t & 1
     const int nc = COLOUR == 0 ? P.nR : P.nB, no = COLOUR == 0 ? P.nB : P.nR;
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     double dmax = 0.0;

@@ -110,10 +110,12 @@ def test_solve_report_matches_golden(orc, golden, name, layout):
     assert (int(rep.status), rep.iterations, rep.detail) == (rec["status"], rec["iterations"], rec["detail"])
     assert [float(v).hex() for v in rep.residual_history] == rec["history"]
     assert rep.flop_estimate == rec["flops"]
-    # on a pivot stop the reference returns a partly updated x; the fused DIA flood solve
-    # reproduces it exactly (x(k) below the pivot node, x(k-1) from it on)
-    fused = sched.kind == OSched.parallel_flood().kind and eng.info["layout"] == int(g.Layout.Dia)
-    if rec["status"] != 1 or rec["detail"] == "residual blowup" or fused:
+    # on a pivot stop the reference returns a partly updated x; the fused DIA flood solve and
+    # the ordered solves (x ring + visit positions) reproduce it exactly -- only the union-CSR
+    # flood solve reports x of the last complete sweep
+    flood = sched.kind == OSched.parallel_flood().kind
+    fused = flood and eng.info["layout"] == int(g.Layout.Dia)
+    if rec["status"] != 1 or rec["detail"] == "residual blowup" or fused or not flood:
         assert digest(rep.solution) == rec["x"]
 
 
@@ -414,3 +416,28 @@ def test_solve_pinned_and_pageable_buffers_agree(orc):
     assert np.array_equal(rep_pageable.solution, want.solution)
     assert np.array_equal(x_pin.numpy(), want.solution)
     assert np.array_equal(rep_pinned.residual_history, want.residual_history)
+
+
+@pytest.mark.parametrize("sched", ["rb", "levels"])
+def test_ordered_pivot_stop_reports_partial_x(orc, sched):
+    """poisson5(12, 9) with an isolated pair whose second node's precision cancels (test_gabp.cpp:
+    73-85 embedded in a grid): the ordered solve stops at that visit and reports x(k) for the
+    nodes visited before it and x(k-1) for the rest, as gabp.cpp:71-87 leaves it."""
+    A0 = orc.poisson5(12, 9)
+    rows, cols, vals = [], [], []
+    for i in range(A0.n):
+        for p in range(A0.row_offsets[i], A0.row_offsets[i + 1]):
+            rows.append(i), cols.append(int(A0.col_indices[p])), vals.append(float(A0.values[p]))
+    p_, q_ = 4 * 12 + 5, 4 * 12 + 6
+    keep = [(r, c, v) for r, c, v in zip(rows, cols, vals) if r not in (p_, q_) and c not in (p_, q_)]
+    keep += [(p_, p_, 1.0), (q_, q_, 1.0), (p_, q_, 1.0), (q_, p_, 1.0)]
+    r, c, v = zip(*keep)
+    A = orc.make_csr(A0.n, r, c, v)
+    b = orc.rng(6).vector(A.n)
+    s = OSched.red_black_grid(12, 9) if sched == "rb" else OSched.four_color_grid(12, 9)
+    rep = g.GabpEngine(A).solve(b, gsched(s), g.GabpOptions(tol=1e-10, max_iter=500))
+    want = orc.engine(A).solve(b, s, tol=1e-10, max_iter=500)
+    assert (int(rep.status), rep.iterations, rep.detail) == (want.status, want.iterations, want.detail)
+    assert want.status == 1 and "pivot" in want.detail
+    assert np.array_equal(rep.solution, want.solution)
+    assert np.array_equal(rep.residual_history, want.residual_history)
