@@ -777,7 +777,8 @@ const Levels& Engine::levels_for(const bgabp_schedule& s) {
 unsigned nblk_host(long long n, int t) { return (unsigned)std::max<long long>(1, (n + t - 1) / t); }
 static inline unsigned nblk(long long n, int t = 256) { return nblk_host(n, t); }
 
-void Engine::launch_flood(const double* b, double2* m0, double2* m1, double* x, int mode, bool delta) {
+void Engine::launch_flood(const double* b, double2* m0, double2* m1, double* x, int mode, bool delta,
+                          long long xstride) {
     if (n == 0) return;
     const unsigned g = nblk(n);
     if (layout == BGABP_LAYOUT_DIA) {
@@ -785,9 +786,9 @@ void Engine::launch_flood(const double* b, double2* m0, double2* m1, double* x, 
                    else k_flood_dia<SS, false><<<g, 256, 0, st>>>(dia, b, m0, m1, x, d_ctrl, mode));
     } else {
         if (delta)
-            k_flood_csr<true><<<g, 256, 0, st>>>(csr, b, m0, m1, x, d_ctrl, mode);
+            k_flood_csr<true><<<g, 256, 0, st>>>(csr, b, m0, m1, x, d_ctrl, mode, xstride);
         else
-            k_flood_csr<false><<<g, 256, 0, st>>>(csr, b, m0, m1, x, d_ctrl, mode);
+            k_flood_csr<false><<<g, 256, 0, st>>>(csr, b, m0, m1, x, d_ctrl, mode, xstride);
     }
 }
 
@@ -983,7 +984,7 @@ void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bga
     for (int k = 0; k < 2; ++k)
         ck(cudaMemsetAsync(d_msg[k], 0, sizeof(double2) * (size_t)std::max<long long>(nslots, 1), st), "memset");
     ck(cudaMemsetAsync(d_x, 0, sizeof(double) * std::max(n, 1), st), "memset x");
-    if (!solve_flood && !solve_seq) {  // ordered solves on levels / red-black
+    if ((!solve_flood && !solve_seq) || (solve_flood && !solve_fused)) {  // ordered, or union-CSR flood
         if (!d_xord) d_xord = static_cast<double*>(dalloc(sizeof(double) * 2 * (size_t)std::max(n, 1)));
         ck(cudaMemsetAsync(d_xord, 0, sizeof(double) * 2 * (size_t)std::max(n, 1), st), "memset x ring");
     }
@@ -1164,9 +1165,10 @@ void Engine::enqueue_double_kernel(bool attr_only) {
 void Engine::enqueue_step_other() {
     if (solve_flood) {
         if (timed_events) ck(cudaEventRecord((*timed_events)[2 * timed_index], st), "event");
-        launch_flood(solve_b, d_msg[0], d_msg[1], d_x, MODE_SOLVE, solve_stop == BGABP_STOP_MESSAGE_DELTA);
+        // x(k) in slot k & 1 of d_xord: a node-pivot stop composes the partly updated x
+        launch_flood(solve_b, d_msg[0], d_msg[1], d_xord, MODE_SOLVE, solve_stop == BGABP_STOP_MESSAGE_DELTA, n);
         if (timed_events) ck(cudaEventRecord((*timed_events)[2 * timed_index + 1], st), "event");
-        launch_residual(solve_b, d_x, nullptr, nullptr, MODE_SOLVE);
+        launch_residual(solve_b, d_xord, nullptr, nullptr, MODE_SOLVE, n);
         k_solve_finalize<<<1, 1, 0, st>>>(d_ctrl, d_hist);
     } else if (solve_pipe) {  // one pipelined sweep (the timed path; solve_steps batches them)
         if (pipe_next <= solve_max_iter) {
@@ -1318,7 +1320,20 @@ const double* Engine::solve_x() {
         }
         return xs;
     }
-    if (!solve_fused && (solve_flood || solve_seq)) return d_x;
+    if (!solve_fused && solve_flood) {  // union-CSR flood: x(k) in slot k & 1 of d_xord
+        const Ctrl& c = *h_ctrl;
+        if (c.status == BGABP_DIVERGED && c.detail_kind == 2)  // failed edge stage: x of the sweep before
+            return d_xord + (size_t)((c.iterations + 1) & 1) * n;
+        const double* xs = d_xord + (size_t)(c.iterations & 1) * n;
+        if (c.status == BGABP_DIVERGED && c.detail_kind == 1 && n > 0) {  // x-stage stopped at the pivot node
+            k_compose_pivot_x<<<nblk(n), 256, 0, st>>>(xs, d_xord + (size_t)((c.iterations + 1) & 1) * n, d_aux, n,
+                                                       (long long)c.detail_key);
+            ck(cudaGetLastError(), "compose x");
+            return d_aux;
+        }
+        return xs;
+    }
+    if (!solve_fused && solve_seq) return d_x;
     if (!solve_fused) {  // ordered (levels / red-black): x(k) in slot k & 1 of d_xord
         const Ctrl& c = *h_ctrl;  // read by solve_report
         const double* xs = d_xord + (size_t)(c.iterations & 1) * n;

@@ -141,7 +141,8 @@ struct Engine {
     }
     const Levels& levels_for(const bgabp_schedule& s);
 
-    void launch_flood(const double* b, double2* m0, double2* m1, double* x, int mode, bool delta);
+    void launch_flood(const double* b, double2* m0, double2* m1, double* x, int mode, bool delta,
+                      long long xstride = 0);
     void launch_aggregate(const double* b, const double2* msg, double* x, double* beta, unsigned long long* npiv);
     void launch_residual(const double* b, const double* x, double* r, unsigned long long* rmax, int mode,
                          long long xstride = 0);

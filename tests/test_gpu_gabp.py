@@ -110,13 +110,9 @@ def test_solve_report_matches_golden(orc, golden, name, layout):
     assert (int(rep.status), rep.iterations, rep.detail) == (rec["status"], rec["iterations"], rec["detail"])
     assert [float(v).hex() for v in rep.residual_history] == rec["history"]
     assert rep.flop_estimate == rec["flops"]
-    # on a pivot stop the reference returns a partly updated x; the fused DIA flood solve and
-    # the ordered solves (x ring + visit positions) reproduce it exactly -- only the union-CSR
-    # flood solve reports x of the last complete sweep
-    flood = sched.kind == OSched.parallel_flood().kind
-    fused = flood and eng.info["layout"] == int(g.Layout.Dia)
-    if rec["status"] != 1 or rec["detail"] == "residual blowup" or fused or not flood:
-        assert digest(rep.solution) == rec["x"]
+    # on a pivot stop the reference returns a partly updated x (gabp.cpp:71-87, 126-130, 155-158):
+    # every solve path keeps x(k-1) in a two-slot ring and composes it exactly
+    assert digest(rep.solution) == rec["x"]
 
 
 def test_solve_stop_rules_and_edges(orc):
