@@ -984,7 +984,7 @@ void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bga
     for (int k = 0; k < 2; ++k)
         ck(cudaMemsetAsync(d_msg[k], 0, sizeof(double2) * (size_t)std::max<long long>(nslots, 1), st), "memset");
     ck(cudaMemsetAsync(d_x, 0, sizeof(double) * std::max(n, 1), st), "memset x");
-    if ((!solve_flood && !solve_seq) || (solve_flood && !solve_fused)) {  // ordered, or union-CSR flood
+    if (!solve_fused && !(solve_seq && pipe_fits())) {  // ordered (not pipelined), or union-CSR flood
         if (!d_xord) d_xord = static_cast<double*>(dalloc(sizeof(double) * 2 * (size_t)std::max(n, 1)));
         ck(cudaMemsetAsync(d_xord, 0, sizeof(double) * 2 * (size_t)std::max(n, 1), st), "memset x ring");
     }
@@ -1182,15 +1182,12 @@ void Engine::enqueue_step_other() {
             launch_rb_sweep(solve_b, d_xord, false, solve_stop == BGABP_STOP_MESSAGE_DELTA, &d_ctrl->delta[0], MODE_SOLVE,
                             n);
         else if (solve_seq)  // grids too tall for the pipeline's x ring
-            launch_seq_sweep(solve_b, d_msg[0], d_x, solve_stop == BGABP_STOP_MESSAGE_DELTA, &d_ctrl->delta[0],
-                             MODE_SOLVE);
+            launch_seq_sweep(solve_b, d_msg[0], d_xord, solve_stop == BGABP_STOP_MESSAGE_DELTA, &d_ctrl->delta[0],
+                             MODE_SOLVE, n);
         else
             launch_levels(*solve_levels, solve_b, d_msg[0], d_xord, solve_stop == BGABP_STOP_MESSAGE_DELTA,
                           &d_ctrl->delta[0], MODE_SOLVE, n);
-        if (solve_seq)
-            launch_residual(solve_b, d_x, nullptr, nullptr, MODE_SOLVE_ORDERED);
-        else
-            launch_residual(solve_b, d_xord, nullptr, nullptr, MODE_SOLVE_ORDERED, n);
+        launch_residual(solve_b, d_xord, nullptr, nullptr, MODE_SOLVE_ORDERED, n);
         k_solve_finalize_ordered<<<1, 1, 0, st>>>(d_ctrl, d_hist);
     }
 }
@@ -1333,7 +1330,6 @@ const double* Engine::solve_x() {
         }
         return xs;
     }
-    if (!solve_fused && solve_seq) return d_x;
     if (!solve_fused) {  // ordered (levels / red-black): x(k) in slot k & 1 of d_xord
         const Ctrl& c = *h_ctrl;  // read by solve_report
         const double* xs = d_xord + (size_t)(c.iterations & 1) * n;

@@ -175,7 +175,8 @@ struct Engine {
     bool seq_applicable(const bgabp_schedule& s) const {
         return grid5 && s.kind == BGABP_SCHED_SEQUENTIAL && n > 0;
     }
-    void launch_seq_sweep(const double* b, double2* msg, double* x, bool delta, unsigned long long* dslot, int mode);
+    void launch_seq_sweep(const double* b, double2* msg, double* x, bool delta, unsigned long long* dslot, int mode,
+                          long long xstride = 0);
     // pipelined lexicographic sweeps (seqpipe_kernels.cuh): many sweeps per launch
     double* d_xring = nullptr;  // [kPipeR][n] x(t) of the solve
     unsigned long long* d_pprog = nullptr;

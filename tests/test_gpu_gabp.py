@@ -437,3 +437,30 @@ def test_ordered_pivot_stop_reports_partial_x(orc, sched):
     assert want.status == 1 and "pivot" in want.detail
     assert np.array_equal(rep.solution, want.solution)
     assert np.array_equal(rep.residual_history, want.residual_history)
+
+
+@pytest.mark.parametrize("pivot", [False, True])
+def test_sequential_tall_grid_one_sweep_per_launch(orc, pivot):
+    """A 5-point grid too tall for the pipeline's ring (ny = 4200 rows of 3: 132 strips) runs one
+    cooperative k_seq_grid5 launch per sweep; solve reports (and the partly updated x of a pivot
+    stop, composed from the two-slot x ring) equal the oracle's."""
+    nx, ny = 3, 4200
+    A0 = orc.poisson5(nx, ny)
+    A = A0
+    if pivot:
+        rows, cols, vals = [], [], []
+        for i in range(A0.n):
+            for p in range(A0.row_offsets[i], A0.row_offsets[i + 1]):
+                rows.append(i), cols.append(int(A0.col_indices[p])), vals.append(float(A0.values[p]))
+        p_, q_ = 100 * nx, 100 * nx + 1
+        keep = [(r, c, v) for r, c, v in zip(rows, cols, vals) if r not in (p_, q_) and c not in (p_, q_)]
+        keep += [(p_, p_, 1.0), (q_, q_, 1.0), (p_, q_, 1.0), (q_, p_, 1.0)]
+        r, c, v = zip(*keep)
+        A = orc.make_csr(A0.n, r, c, v)
+    b = orc.rng(12).vector(A.n)
+    tol = 1e-6 * np.abs(b).max()
+    rep = g.GabpEngine(A).solve(b, g.Schedule.sequential(), g.GabpOptions(tol=tol, max_iter=400))
+    want = orc.engine(A).solve(b, OSched.sequential(), tol=tol, max_iter=400)
+    assert (int(rep.status), rep.iterations, rep.detail) == (want.status, want.iterations, want.detail)
+    assert np.array_equal(rep.residual_history, want.residual_history)
+    assert np.array_equal(rep.solution, want.solution)
