@@ -904,12 +904,15 @@ int Engine::sweep(const double* b, const bgabp_schedule& s, double* x, std::stri
             err = "zero pivot on edge " + std::to_string(k >> 32) + "->" + std::to_string(k & 0xffffffffu);
             return BGABP_EPIVOT;
         }
-        ck(cudaMemcpyAsync(x, d_x, sizeof(double) * n, cudaMemcpyDeviceToHost, st), "D2H x");
-        ck(cudaStreamSynchronize(st), "sync");
-        if (h_ctrl->npiv[0] != kNone) {
-            err = "zero pivot at node " + std::to_string(h_ctrl->npiv[0]);
+        if (h_ctrl->npiv[0] != kNone) {  // the x-stage stopped at the pivot node (gabp.cpp:155-158)
+            const unsigned long long piv = h_ctrl->npiv[0];
+            if (piv > 0) ck(cudaMemcpyAsync(x, d_x, sizeof(double) * (size_t)piv, cudaMemcpyDeviceToHost, st), "D2H x");
+            ck(cudaStreamSynchronize(st), "sync");
+            err = "zero pivot at node " + std::to_string(piv);
             return BGABP_EPIVOT;
         }
+        ck(cudaMemcpyAsync(x, d_x, sizeof(double) * n, cudaMemcpyDeviceToHost, st), "D2H x");
+        ck(cudaStreamSynchronize(st), "sync");
         return BGABP_OK;
     }
     const Levels& L = levels_for(s);
@@ -928,12 +931,21 @@ int Engine::sweep(const double* b, const bgabp_schedule& s, double* x, std::stri
         launch_levels(L, d_b, d_msg[cur], d_x, false, nullptr, MODE_PLAIN);
     }
     ck(cudaGetLastError(), "level launch");
-    ck(cudaMemcpyAsync(x, d_x, sizeof(double) * n, cudaMemcpyDeviceToHost, st), "D2H x");
     read_ctrl();
     if (h_ctrl->opiv != kNone) {
-        err = ordered_detail(L.order, h_ctrl->opiv);
+        // the visit stopped at position p (gabp.cpp:71-87): nodes visited before it (and the
+        // pivot node on an edge pivot, whose x was written) take the new x, the rest keep the caller's
+        const unsigned long long key = h_ctrl->opiv;
+        const long long p = (long long)(key >> 32) + ((key & 0xffffffffu) ? 1 : 0);
+        std::vector<double> xn((size_t)n);
+        ck(cudaMemcpyAsync(xn.data(), d_x, sizeof(double) * n, cudaMemcpyDeviceToHost, st), "D2H x");
+        ck(cudaStreamSynchronize(st), "sync");
+        for (long long q = 0; q < p && q < n; ++q) x[L.order[q]] = xn[L.order[q]];
+        err = ordered_detail(L.order, key);
         return BGABP_EPIVOT;
     }
+    ck(cudaMemcpyAsync(x, d_x, sizeof(double) * n, cudaMemcpyDeviceToHost, st), "D2H x");
+    ck(cudaStreamSynchronize(st), "sync");
     return BGABP_OK;
 }
 
