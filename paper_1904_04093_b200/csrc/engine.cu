@@ -345,13 +345,14 @@ Stager& stager() {
 }
 }  // namespace
 
+// memory the DMA engines can read or write directly: pinned host, device or managed memory
 static bool is_pinned(const void* p) {
     cudaPointerAttributes a{};
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
         cudaGetLastError();
         return false;
     }
-    return a.type == cudaMemoryTypeHost;
+    return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
 // Host -> device on `st`.  Pinned sources and small copies go straight to the DMA engine; large
@@ -360,7 +361,7 @@ static bool is_pinned(const void* p) {
 void host_to_device(void* dst, const void* src, size_t bytes, cudaStream_t st) {
     if (bytes == 0) return;
     if (bytes <= (size_t(1) << 20) || is_pinned(src)) {
-        ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st), "H2D");
+        ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st), "H2D");
         return;
     }
     Stager& S = stager();
@@ -389,7 +390,7 @@ void host_to_device(void* dst, const void* src, size_t bytes, cudaStream_t st) {
 void device_to_host(void* dst, const void* src, size_t bytes, cudaStream_t st) {
     if (bytes == 0) return;
     if (bytes <= (size_t(1) << 20) || is_pinned(dst)) {
-        ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st), "D2H");
         return;
     }
     Stager& S = stager();
