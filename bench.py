@@ -206,9 +206,6 @@ def run_gpu(args, world, rank, local):
     import paper_1904_04093_b200 as g
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    # time to 1e-8 on configs 3 and 5 first, in a fresh allocator (after the config-2 engine is
-    # freed, new allocations pay for re-zeroed pages and the setups read ~0.1-0.25 s slower)
-    tts_block = time_to_solution(g, torch, args) if (args.config == 2 and not args.no_tts and rank == 0) else None
     P = g.config_problem(args.config)
     n = P.A.n
     eng = g.GabpEngine(P.A)
@@ -335,8 +332,12 @@ def run_gpu(args, world, rank, local):
             "gpu_launches": 2 * args.steps, "clocks": clk.summary()}
     if tts is not None:
         line["solve"] = tts
-    if tts_block is not None:
-        line["time_to_solution"] = tts_block
+    if args.config == 2 and not args.no_tts and rank == 0:
+        # after the headline (its buffers are fresh allocations; the configs' setups below reuse
+        # the engine's cached device blocks once it is gone)
+        del eng
+        torch.cuda.synchronize()
+        line["time_to_solution"] = time_to_solution(g, torch, args)
     if schedules:
         line["schedules"] = schedules  # same system, sweep + residual + stop test per iteration
     if args.config != 2:
