@@ -44,7 +44,7 @@ void ck(cudaError_t e, const char* what) {
 // solve after another, the shards of a re-partitioned system -- reuses its blocks instead of
 // paying cudaFree / cudaMalloc and the driver's re-zeroing of freed pages (~0.15 s for a config-5
 // hierarchy).  Blocks stay whole cudaMalloc allocations (CUDA IPC of shard buffers works).
-// BGABP_NO_BLOCK_CACHE=1 frees immediately; at most 48 GB are held per device.
+// BGABP_NO_BLOCK_CACHE=1 frees immediately; at most 16 GB are held (all devices).
 namespace {
 struct BlockCache {
     std::mutex mu;
@@ -52,7 +52,7 @@ struct BlockCache {
     std::map<void*, std::pair<int, size_t>> sizes;  // every block handed out, with its rounded size
     size_t held = 0;
     bool off = getenv("BGABP_NO_BLOCK_CACHE") != nullptr;
-    static constexpr size_t kMin = size_t(1) << 20, kGran = size_t(2) << 20, kCap = size_t(48) << 30;
+    static constexpr size_t kMin = size_t(1) << 20, kGran = size_t(2) << 20, kCap = size_t(16) << 30;
 };
 BlockCache& block_cache() {
     static BlockCache* c = new BlockCache();
