@@ -225,3 +225,24 @@ struct Engine {
 unsigned nblk_host(long long n, int t = 256);
 
 }  // namespace bgabp
+
+// the C-ABI handle
+struct bgabp_engine {
+    bgabp::Engine E;
+};
+
+#define ABI_GUARD(ERRBUF, ERRLEN, ...)                           \
+    try {                                                        \
+        __VA_ARGS__                                              \
+    } catch (const InvalidArg& ex) {                             \
+        put_err(ERRBUF, ERRLEN, ex.what());                      \
+        return BGABP_EINVAL;                                     \
+    } catch (const CudaError& ex) {                              \
+        put_err(ERRBUF, ERRLEN, ex.what());                      \
+        return BGABP_ECUDA;                                      \
+    } catch (const std::exception& ex) {                         \
+        put_err(ERRBUF, ERRLEN, ex.what());                      \
+        return BGABP_ERUNTIME;                                   \
+    }
+
+
