@@ -1,4 +1,4 @@
-// Device build of the DIA message-graph layout (engine.cu, Engine::build_dia_device).
+// Device build of the DIA message-graph layout (build.cu, Engine::build_dia_device).
 //
 // The reference builds its message graph on the host (make_csr / transpose_pos, sparse.cpp:36-75;
 // build_message_graph, gabp.cpp:8-27).  Here the canonical CSR goes to HBM once and these kernels
@@ -22,7 +22,7 @@ struct DiaOffs {
 
 // thread per row: scatter every off-diagonal entry into (mask, rowv) of its row node and
 // (mask, c) of its column node; the diagonal into diag.  mask, c, rowv are zeroed beforehand.
-__global__ void k_dia_fill(int n, const int* __restrict__ ro, const int* __restrict__ ci,
+static __global__ void k_dia_fill(int n, const int* __restrict__ ro, const int* __restrict__ ci,
                            const double* __restrict__ val, DiaOffs o, uint32_t* mask, double* c, double* rowv,
                            double* diag) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -36,7 +36,8 @@ __global__ void k_dia_fill(int n, const int* __restrict__ ro, const int* __restr
                 continue;
             }
             int s = 0;
-            while (o.off[s] != j - i) ++s;  // <= 8 sorted offsets; presence guaranteed by the host scan
+            while (s < o.S && o.off[s] != j - i) ++s;  // <= 8 sorted offsets, found by the host scan
+            if (s == o.S) continue;
             in |= 1u << s;
             rowv[(size_t)s * n + i] = v;
             const int rs = o.rev[s];
@@ -71,7 +72,7 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
 }
 
 // gx > 0: also test the 5-point grid wrap-around condition for rows of gx nodes
-__global__ void k_dia_facts(int n, int S, const uint32_t* __restrict__ mask, const double* __restrict__ c,
+static __global__ void k_dia_facts(int n, int S, const uint32_t* __restrict__ mask, const double* __restrict__ c,
                             const double* __restrict__ rowv, const double* __restrict__ diag, int gx,
                             DiaFacts* out) {
     unsigned asym = 0u, wrap = 0u;
@@ -125,7 +126,7 @@ __global__ void k_dia_facts(int n, int S, const uint32_t* __restrict__ mask, con
 
 // CSR position -> message slot (s * n + i for the in-edge of row i at offset s; -1 on the diagonal),
 // for get/set_state in CSR order (parity paths only, built on first use)
-__global__ void k_dia_csr2slot(int n, const int* __restrict__ ro, const int* __restrict__ ci, DiaOffs o,
+static __global__ void k_dia_csr2slot(int n, const int* __restrict__ ro, const int* __restrict__ ci, DiaOffs o,
                                long long* out) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         for (int p = ro[i]; p < ro[i + 1]; ++p) {
@@ -135,13 +136,13 @@ __global__ void k_dia_csr2slot(int n, const int* __restrict__ ro, const int* __r
                 continue;
             }
             int s = 0;
-            while (o.off[s] != j - i) ++s;
-            out[p] = (long long)s * n + i;
+            while (s < o.S && o.off[s] != j - i) ++s;
+            out[p] = s < o.S ? (long long)s * n + i : -1;
         }
     }
 }
 
-__global__ void k_fill_value(double* v, long long n, double a) {
+static __global__ void k_fill_value(double* v, long long n, double a) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
         v[i] = a;
 }

@@ -27,6 +27,7 @@ struct CudaError : std::runtime_error {
 };
 
 void put_err(char* err, size_t len, const std::string& s);
+void release_block(void* p);  // engine device blocks back to the cache (memory.cu)
 struct Engine;
 void p2p_forget(Engine* e);  // drop captured multi-shard graphs that use this engine
 // host <-> device copies of caller buffers: direct when pinned, staged (parallel) when pageable
@@ -223,6 +224,14 @@ struct Engine {
 };
 
 unsigned nblk_host(long long n, int t = 256);
+
+template <class T>
+inline T* Engine::upload(const std::vector<T>& v) {
+    T* d = static_cast<T*>(dalloc(sizeof(T) * v.size()));
+    if (!v.empty()) ck(cudaMemcpyAsync(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, st), "H2D");
+    return d;
+}
+
 
 }  // namespace bgabp
 
