@@ -1,9 +1,12 @@
 // Host side of the B200 GaBP engine behind include/gabp_b200.h.
 //
 // Replaces GabpEngine (proj/core/include/belief/gabp.hpp:58-111, src/gabp.cpp) with a handle that
-// owns the device layout of the message graph, the message buffers and a CUDA stream.  Setup is
-// host C++ (layout build, schedule dependency levels); every sweep, residual and reduction runs in
-// the kernels of kernels.cuh.  There is no CPU fallback: a failed CUDA call is BGABP_ECUDA.
+// owns the device layout of the message graph, the message buffers and a CUDA stream.  This file
+// holds the schedules (dependency levels), the sweep / solve loops and the C-ABI; construction is
+// in build.cu, device memory and caller-buffer copies in memory.cu, the sharded solve in
+// shard.cu.  Every sweep, residual and reduction runs in the kernels of kernels.cuh (and
+// rb_ / seq_ / seqpipe_ / flood2_kernels.cuh).  There is no CPU fallback: a failed CUDA call is
+// BGABP_ECUDA.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
