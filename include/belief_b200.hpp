@@ -24,6 +24,7 @@
 
 #include "belief/gabp.hpp"
 #include "belief/multigrid.hpp"
+#include "belief/problems.hpp"
 #include "gabp_b200.h"
 
 namespace belief {
@@ -170,6 +171,12 @@ public:
     }
 
     double sweep_flops() const { return bgabp_sweep_flops(h()); }
+    /// gabp.hpp:62 -- the host message graph (the reference's build_message_graph, gabp.cpp:8-27),
+    /// built on first use; the device keeps its own slot layout of the same edges
+    const MessageGraph& graph() const {
+        if (!graph_) graph_ = std::make_shared<MessageGraph>(build_message_graph(A_));
+        return *graph_;
+    }
     bgabp_engine* handle() const { return h_.get(); }
 
 private:
@@ -190,33 +197,69 @@ private:
 
     const SparseMatrix& A_;
     std::shared_ptr<bgabp_engine> h_;
+    mutable std::shared_ptr<MessageGraph> graph_;
 };
 
-// Hierarchy(problem, J1, J2, params, smoother) (multigrid.hpp:52-86) on the device
+/// GridLevel (multigrid.hpp:42-50) without the host engines: the rediscretised problem, the
+/// smoother's schedule and the frozen-precision flag; the device holds each level's engine.
+struct GridLevel {
+    AssembledProblem prob;
+    Schedule schedule;
+    bool frozen_ok = false;
+};
+
+// Hierarchy (multigrid.hpp:52-86) on the device
 class Hierarchy {
 public:
+    /// Hierarchy(problem, J1, J2, params, smoother): every level rediscretised from the named
+    /// problem (multigrid.cpp:74-83), then the caller-supplied-levels path below
     Hierarchy(const std::string& problem, int J1, int J2, const std::map<std::string, double>& params,
               MgSmoother smoother)
-        : smoother_(smoother) {
-        std::vector<const char*> keys;
-        std::vector<double> vals;
-        for (const auto& kv : params) {
-            keys.push_back(kv.first.c_str());
-            vals.push_back(kv.second);
+        : Hierarchy(assemble_levels(problem, J1, J2, params), smoother) {}
+
+    /// Caller-supplied rediscretised levels, finest first, each a square grid whose size halves
+    /// ((nx - 1) / 2) -- for operators no named problem assembles (BASELINE.json config 5).  The
+    /// setup probe may truncate the hierarchy exactly as the named constructor does
+    /// (multigrid.cpp:89-93).
+    Hierarchy(std::vector<AssembledProblem> levels, MgSmoother smoother) : smoother_(smoother) {
+        std::vector<int> n, nx;
+        std::vector<const int*> ro, ci;
+        std::vector<const double*> v;
+        for (const auto& L : levels) {
+            n.push_back(L.A.n);
+            nx.push_back(L.grid.nx);
+            ro.push_back(L.A.row_offsets.data());
+            ci.push_back(L.A.col_indices.data());
+            v.push_back(L.A.values.data());
         }
         char err[512] = {0};
         bgmg* h = nullptr;
-        detail::check(bgmg_create_named(problem.c_str(), J1, J2, static_cast<int>(keys.size()), keys.data(),
-                                        vals.data(), static_cast<int>(smoother), &h, err, sizeof err),
+        detail::check(bgmg_create(static_cast<int>(levels.size()), n.data(), ro.data(), ci.data(), v.data(), nx.data(),
+                                  static_cast<int>(smoother), &h, err, sizeof err),
                       err);
         h_.reset(h, bgmg_destroy);
-        fine_rhs_.assign(static_cast<size_t>(bgmg_level_n(h, 0)), 0.0);
-        bgmg_fine_rhs(h, fine_rhs_.data());
+        levels.resize(static_cast<size_t>(bgmg_num_levels(h)));
+        for (auto& L : levels) {
+            GridLevel g;
+            g.schedule = schedule_for(smoother, L.grid.nx, L.grid.ny);
+            g.prob = std::move(L);
+            levels_.push_back(std::move(g));
+        }
     }
 
-    int num_levels() const { return bgmg_num_levels(h_.get()); }
-    bool level_frozen_ok(int k) const { return bgmg_level_frozen_ok(h_.get(), k) != 0; }
-    const Vector& fine_rhs() const { return fine_rhs_; }
+    int num_levels() const { return static_cast<int>(levels_.size()); }
+    /// the level's problem, schedule and frozen flag (the frozen precisions are computed on the
+    /// device on first use, so the flag is read then)
+    const GridLevel& level(int k) const {
+        if (!frozen_read_) {
+            for (int q = 0; q < num_levels(); ++q) levels_[q].frozen_ok = bgmg_level_frozen_ok(h_.get(), q) == 1;
+            frozen_read_ = true;
+        }
+        return levels_[k];
+    }
+    bool level_frozen_ok(int k) const { return level(k).frozen_ok; }
+    const Vector& fine_rhs() const { return levels_[0].prob.b; }
+    const Vector& fine_exact() const { return levels_[0].prob.exact; }
     MgSmoother smoother() const { return smoother_; }
 
     void v_cycle(const CycleSpec& spec, const Vector& b, Vector& x) {
@@ -227,14 +270,75 @@ public:
         detail::check(bgmg_vcycle(h_.get(), &c, b.data(), x.data(), err, sizeof err), err);
     }
 
+    /// multigrid.cpp:240-274 (flop_table of analysis.cpp:135-154 by the fine centre row)
+    double cycle_flops_per_unknown(const CycleSpec& spec) const {
+        bgmg_cycle c{spec.pre, spec.post, spec.frozen ? 1 : 0};
+        double out = 0.0;
+        char err[256] = {0};
+        detail::check(bgmg_cycle_flops_per_unknown(h_.get(), &c, &out, err, sizeof err), err);
+        return out;
+    }
+
     bgmg* handle() const { return h_.get(); }
 
 private:
+    static Schedule schedule_for(MgSmoother s, int nx, int ny) {  // multigrid.cpp:25-32
+        switch (s) {
+            case MgSmoother::GabpRedBlack: return Schedule::red_black_grid(nx, ny);
+            case MgSmoother::GabpFourColor: return Schedule::four_color_grid(nx, ny);
+            case MgSmoother::GabpFlood: return Schedule::parallel_flood();
+            case MgSmoother::GabpSequential: return Schedule::sequential(nx * ny);
+            default: return Schedule{};
+        }
+    }
+
+    // assemble(name, J, params) for J = J1 .. J1 - J2 + 1 (problems.cpp:161-226 as restated by
+    // the library's input generator, bit-identical to the reference's)
+    static std::vector<AssembledProblem> assemble_levels(const std::string& problem, int J1, int J2,
+                                                         const std::map<std::string, double>& params) {
+        if (J2 < 1 || J1 - J2 + 1 < 1) throw std::invalid_argument("Hierarchy: need 1 <= J2 and a coarsest exponent >= 1");
+        std::vector<const char*> keys;
+        std::vector<double> vals;
+        for (const auto& kv : params) {
+            keys.push_back(kv.first.c_str());
+            vals.push_back(kv.second);
+        }
+        std::vector<AssembledProblem> out;
+        for (int J = J1; J >= J1 - J2 + 1; --J) {
+            char err[512] = {0};
+            bgabp_problem* p = bgabp_problem_named(problem.c_str(), J, static_cast<int>(keys.size()), keys.data(),
+                                                   vals.data(), err, sizeof err);
+            if (!p) throw std::invalid_argument(err);
+            AssembledProblem a;
+            const int n = bgabp_problem_n(p);
+            const long long nnz = bgabp_problem_nnz(p);
+            a.A.n = n;
+            a.A.row_offsets.assign(bgabp_problem_row_offsets(p), bgabp_problem_row_offsets(p) + n + 1);
+            a.A.col_indices.assign(bgabp_problem_col_indices(p), bgabp_problem_col_indices(p) + nnz);
+            a.A.values.assign(bgabp_problem_values(p), bgabp_problem_values(p) + nnz);
+            a.A.transpose_pos.assign(static_cast<size_t>(nnz), -1);
+            for (int i = 0; i < n; ++i)  // sparse.cpp:70-74
+                for (int q = a.A.row_offsets[i]; q < a.A.row_offsets[i + 1]; ++q)
+                    a.A.transpose_pos[q] = a.A.find(a.A.col_indices[q], i);
+            a.b.assign(bgabp_problem_rhs(p), bgabp_problem_rhs(p) + n);
+            if (const double* ex = bgabp_problem_exact(p)) a.exact.assign(ex, ex + n);
+            a.grid = {bgabp_problem_nx(p), bgabp_problem_nx(p)};
+            a.h = 1.0 / (1 << J);
+            bgabp_problem_free(p);
+            out.push_back(std::move(a));
+        }
+        return out;
+    }
+
     MgSmoother smoother_;
     std::shared_ptr<bgmg> h_;
-    Vector fine_rhs_;
+    mutable std::vector<GridLevel> levels_;
+    mutable bool frozen_read_ = false;
 };
 
+/// mg_solve (multigrid.cpp:276-318): flop_estimate = cycle_flops_per_unknown * n per completed
+/// cycle; a cycle that ended in a smoother breakdown has no residual entry and x is the partly
+/// cycled x, as the reference's exception path leaves it
 inline SolveReport mg_solve(Hierarchy& hier, const CycleSpec& spec, const Vector& b, const MgSolveOptions& opt) {
     SolveReport rep;
     rep.solution.assign(b.size(), 0.0);
@@ -248,8 +352,10 @@ inline SolveReport mg_solve(Hierarchy& hier, const CycleSpec& spec, const Vector
                   detail);
     rep.status = static_cast<SolveStatus>(r.status);
     rep.iterations = r.iterations;
-    rep.residual_history.assign(hist.begin(), hist.begin() + r.iterations + 1);
+    rep.flop_estimate = r.flop_estimate;
     rep.detail = detail;
+    const bool breakdown = rep.status == SolveStatus::Diverged && rep.detail != "residual blowup";
+    rep.residual_history.assign(hist.begin(), hist.begin() + r.iterations + (breakdown ? 0 : 1));
     return rep;
 }
 

@@ -272,10 +272,22 @@ void bgmg_destroy(bgmg* h);
 int bgmg_num_levels(const bgmg* h);
 int bgmg_level_frozen_ok(const bgmg* h, int k);
 int bgmg_level_n(const bgmg* h, int k);
+int bgmg_level_nx(const bgmg* h, int k); /* grid points per axis of level k (GridLevel::prob.grid) */
+/* Hierarchy::cycle_flops_per_unknown (multigrid.hpp:71-73, multigrid.cpp:240-274): the analytic
+ * flop_table (analysis.cpp:135-154) of the pre + post sweeps, by the fine centre row's population */
+int bgmg_cycle_flops_per_unknown(const bgmg* h, const bgmg_cycle* spec, double* out, char* err,
+                                 size_t errlen);
 /* fine-level right-hand side of a named hierarchy (Hierarchy::fine_rhs, multigrid.hpp:62) */
 int bgmg_fine_rhs(const bgmg* h, double* b_out);
+/* Hierarchy::v_cycle (multigrid.cpp:234-238): x updated in place; on a smoother breakdown returns
+ * BGABP_ERUNTIME with the reference's message and x holding the updates made before it. */
 int bgmg_vcycle(bgmg* h, const bgmg_cycle* spec, const double* b, double* x, char* err,
                 size_t errlen);
+/* mg_solve (multigrid.cpp:276-318).  rep->flop_estimate = cycle_flops_per_unknown * n per
+ * completed cycle.  history (max_cycles + 1) receives iterations + 1 residuals, or iterations when
+ * the last cycle ended in a smoother breakdown (status Diverged, detail other than "residual
+ * blowup": that cycle has no residual, multigrid.cpp:288-297); x_out is then the reference's
+ * partly cycled x (the level-0 updates made before the breakdown). */
 int bgmg_solve(bgmg* h, const bgmg_cycle* spec, const double* b, const bgmg_options* opt,
                bgabp_report* rep, double* x_out, double* history, char* detail, size_t detaillen);
 /* device-resident mg_solve: b_dev / x_dev device pointers; synchronises at every cycle's stop test */

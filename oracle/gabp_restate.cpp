@@ -583,6 +583,27 @@ private:
 };
 
 // ---------------------------------------------------------------------------------------------
+// Analytic smoother cost per unknown — analysis.cpp:135-154 (analysis.hpp:49-57)
+// ---------------------------------------------------------------------------------------------
+enum class FlopStencil { FivePoint, NinePoint };
+enum class FlopSmoother { Gabp, LineGabp, Gs, XyGs };
+
+double flop_table(FlopStencil stencil, FlopSmoother smoother, int sweeps) {
+    if (sweeps < 1) throw std::invalid_argument("flop_table: sweeps must be >= 1");
+    const double M = sweeps;
+    const bool five = stencil == FlopStencil::FivePoint;
+    if (smoother == FlopSmoother::Gabp) return five ? 12.0 * M + 6.0 : 24.0 * M + 8.0;
+    if (smoother == FlopSmoother::LineGabp) {
+        if (!five)
+            throw std::invalid_argument(
+                "flop_table: line regions do not cover the nine-point stencil's diagonal couplings");
+        return sweeps == 1 ? 38.0 : 28.0 * M + 9.0;
+    }
+    if (smoother == FlopSmoother::Gs) return five ? 9.0 * M : 17.0 * M;
+    return five ? 14.0 * M : 21.0 * M;  // XyGs
+}
+
+// ---------------------------------------------------------------------------------------------
 // Computation-tree oracle — analysis.cpp:160-215
 // ---------------------------------------------------------------------------------------------
 double computation_tree_solve(const SparseMatrix& A, const Vector& b, int root, int depth,

@@ -164,7 +164,9 @@ class Oracle:
             "orc_mg_level_frozen_ok": (C.c_int, [vp, C.c_int]),
             "orc_mg_vcycle": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, _dp, _dp, C.c_char_p, C.c_size_t]),
             "orc_mg_solve": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, _dp, C.c_double, C.c_int,
-                                       C.c_double, _dp, _dp, _ip, _ip, C.c_char_p, C.c_size_t]),
+                                       C.c_double, _dp, _dp, _ip, _ip, _dp, _ip, C.c_char_p, C.c_size_t]),
+            "orc_mg_cycle_flops": (C.c_double, [vp, C.c_int, C.c_int]),
+            "orc_flop_table": (C.c_double, [C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_size_t]),
             "orc_mg_restrict": (None, [_dp, C.c_int, _dp]),
             "orc_mg_prolong": (None, [_dp, C.c_int, _dp]),
             "orc_gs_sweeps": (C.c_int, [vp, _dp, _dp, _Sched, C.c_int, C.c_char_p, C.c_size_t]),
@@ -325,6 +327,14 @@ class Oracle:
         if rc != 1:
             raise RuntimeError(err.value.decode())
         return x
+
+    def flop_table(self, stencil, smoother, sweeps):
+        """analysis.cpp:135-154; ValueError on the reference's std::invalid_argument."""
+        err = C.create_string_buffer(256)
+        v = self.lib.orc_flop_table(stencil, smoother, sweeps, err, 256)
+        if v == -1.0 and err.value:
+            raise ValueError(err.value.decode())
+        return v
 
     # ---- generators (restatement only) -----------------------------------------------------
     def rng(self, seed):
@@ -556,21 +566,28 @@ class _Hierarchy:
         return bool(self.o.lib.orc_mg_level_frozen_ok(self.h, k))
 
     def v_cycle(self, pre, post, b, x, frozen=False):
+        """One V-cycle.  Returns x; on a smoother breakdown raises RuntimeError with the
+        partly updated x (multigrid.cpp:234-238 updates the caller's x in place) as args[1]."""
         x = f64(x).copy()
         err = C.create_string_buffer(512)
         rc = self.o.lib.orc_mg_vcycle(self.h, pre, post, int(frozen), _d(f64(b)), _d(x), err, 512)
         if rc != 1:
-            raise RuntimeError(err.value.decode())
+            raise RuntimeError(err.value.decode(), x)
         return x
+
+    def cycle_flops_per_unknown(self, pre, post):
+        return self.o.lib.orc_mg_cycle_flops(self.h, pre, post)
 
     def solve(self, pre, post, b, tol=2e-4, max_cycles=200, divergence_factor=1e6, frozen=False):
         x = np.zeros(self.n)
         hist = np.zeros(max_cycles + 1)
-        it, st = C.c_int(0), C.c_int(0)
+        it, st, hl = C.c_int(0), C.c_int(0), C.c_int(0)
+        fl = C.c_double(0.0)
         det = C.create_string_buffer(512)
         self.o.lib.orc_mg_solve(self.h, pre, post, int(frozen), _d(f64(b)), tol, max_cycles,
-                                divergence_factor, _d(x), _d(hist), C.byref(it), C.byref(st), det, 512)
-        return Report(st.value, it.value, hist[: it.value + 1].copy(), 0.0, x, det.value.decode())
+                                divergence_factor, _d(x), _d(hist), C.byref(it), C.byref(st), C.byref(fl),
+                                C.byref(hl), det, 512)
+        return Report(st.value, it.value, hist[: hl.value].copy(), fl.value, x, det.value.decode())
 
 
 def _flatten_lists(lists):

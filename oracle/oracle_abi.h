@@ -102,7 +102,10 @@ int orc_mg_vcycle(orc_mg* h, int pre, int post, int frozen, const double* b, dou
                   size_t errlen);
 int orc_mg_solve(orc_mg* h, int pre, int post, int frozen, const double* b, double tol,
                  int max_cycles, double divergence_factor, double* x_out, double* history,
-                 int* iterations, int* status, char* detail, size_t detaillen);
+                 int* iterations, int* status, double* flops, int* hist_len, char* detail, size_t detaillen);
+/* Hierarchy::cycle_flops_per_unknown (multigrid.cpp:240-274) and flop_table (analysis.cpp:135-154) */
+double orc_mg_cycle_flops(const orc_mg* h, int pre, int post);
+double orc_flop_table(int stencil, int smoother, int sweeps, char* err, size_t errlen);
 void orc_mg_restrict(const double* fine, int mf, double* out);
 void orc_mg_prolong(const double* coarse, int mc, double* out);
 /* Gauss-Seidel in schedule order (classic.cpp:16-30) — comparison smoother */

@@ -449,6 +449,10 @@ void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bga
     k_solve_arm<<<1, 1, 0, st>>>(d_ctrl, d_hist);
     ck(cudaGetLastError(), "solve arm");
     steps_enqueued = 0;
+    // capture (not run) the iteration chunk now, so the first steps call replays it instead of
+    // paying capture + instantiation inside the caller's loop; shard solves use their own graphs
+    if (!r0_override && chunk_graph_eligible())
+        for (int len = kChunk; len >= 1; len >>= 1) chunk_graph(len);
 }
 
 void Engine::enqueue_step() {
@@ -625,6 +629,33 @@ void Engine::enqueue_step_other() {
     }
 }
 
+bool Engine::chunk_graph_eligible() const {
+    const size_t per_step = solve_double ? 3 : solve_fused ? 2 : solve_flood ? 3 : solve_levels->ptr.size() + 1;
+    return per_step * kChunk <= 4096 && n > 0 && !solve_seq;  // cooperative launches stay out of graphs
+}
+
+// The captured graph of `len` iterations of the current solve (len = kChunk or a power of two
+// below it for the remainder of a steps call).  Captured on first use; capture records the
+// launches without running them, so solve_begin takes them all outside the caller's loop.
+cudaGraphExec_t Engine::chunk_graph(int len) {
+    const std::string key = std::string(solve_double ? "D" : solve_fused ? "F" : solve_flood ? "f" : "o") +
+                            std::to_string(solve_stop) + ":" + std::to_string(flood2_h) + ":" +
+                            std::to_string((long long)(uintptr_t)solve_b) + ":" +
+                            std::to_string((long long)(uintptr_t)solve_levels) + ":" + std::to_string(len);
+    auto it = graphs.find(key);
+    if (it == graphs.end()) {
+        cudaGraph_t g;
+        ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture");
+        for (int k = 0; k < len; ++k) enqueue_step();
+        ck(cudaStreamEndCapture(st, &g), "capture end");
+        cudaGraphExec_t ge;
+        ck(cudaGraphInstantiate(&ge, g, 0), "graph instantiate");
+        cudaGraphDestroy(g);
+        it = graphs.emplace(key, ge).first;
+    }
+    return it->second;
+}
+
 void Engine::solve_steps(int nsteps) {
     if (nsteps <= 0) return;
     if (solve_pipe) {  // one launch carries all of them, pipelined (seqpipe_kernels.cuh)
@@ -638,28 +669,17 @@ void Engine::solve_steps(int nsteps) {
     // so one captured chunk is valid for any position in the loop
     const int per_call = solve_double ? 2 : 1;  // iterations per enqueue_step
     if (solve_double) nsteps = (nsteps + 1) / 2;  // enqueue_step calls
-    const size_t per_step = solve_double ? 3 : solve_fused ? 2 : solve_flood ? 3 : solve_levels->ptr.size() + 1;
-    const bool use_graph = per_step * 16 <= 4096 && n > 0 && !solve_seq;  // cooperative launches stay out of graphs
+    const bool use_graph = chunk_graph_eligible();
     int left = nsteps;
     while (left > 0) {
-        const int chunk = use_graph ? std::min(left, 16) : left;
-        if (use_graph && chunk == 16) {
-            const std::string key = std::string(solve_double ? "D" : solve_fused ? "F" : solve_flood ? "f" : "o") +
-                                    std::to_string(solve_stop) + ":" + std::to_string(flood2_h) + ":" +
-                                    std::to_string((long long)(uintptr_t)solve_b) + ":" +
-                                    std::to_string((long long)(uintptr_t)solve_levels);
-            auto it = graphs.find(key);
-            if (it == graphs.end()) {
-                cudaGraph_t g;
-                ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture");
-                for (int k = 0; k < 16; ++k) enqueue_step();
-                ck(cudaStreamEndCapture(st, &g), "capture end");
-                cudaGraphExec_t ge;
-                ck(cudaGraphInstantiate(&ge, g, 0), "graph instantiate");
-                cudaGraphDestroy(g);
-                it = graphs.emplace(key, ge).first;
-            }
-            ck(cudaGraphLaunch(it->second, st), "graph launch");
+        // kChunk-iteration graphs, then the remainder as power-of-two graphs (16 + 4 for 20)
+        int chunk = left;
+        if (use_graph) {
+            chunk = kChunk;
+            while (chunk > left) chunk >>= 1;
+        }
+        if (use_graph) {
+            ck(cudaGraphLaunch(chunk_graph(chunk), st), "graph launch");
         } else {
             for (int k = 0; k < chunk; ++k) enqueue_step();
         }

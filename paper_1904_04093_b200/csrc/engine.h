@@ -207,6 +207,9 @@ struct Engine {
     void* d_pack = nullptr;
     long long pack_cap = 0;
     void solve_steps(int nsteps);
+    static constexpr int kChunk = 16;  // solve iterations per captured graph
+    bool chunk_graph_eligible() const;
+    cudaGraphExec_t chunk_graph(int len);
     bool solve_done();
     void solve_run_to_end();
     void solve_report(bgabp_report& rep, std::string& detail);

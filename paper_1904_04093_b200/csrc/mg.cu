@@ -96,6 +96,27 @@ std::vector<double> dense_inverse(Engine& E) {
     return inv;
 }
 
+// flop_table (analysis.cpp:135-154) for the smoother kinds a Hierarchy can carry: per-unknown
+// cost of `sweeps` smoothing sweeps (SolveReport::flop_estimate of mg_solve, multigrid.cpp:288,302)
+enum class FlopSmoother { Gabp, LineGabp, Gs };
+double flop_table(bool five, FlopSmoother sm, int sweeps) {
+    if (sweeps < 1) throw InvalidArg("flop_table: sweeps must be >= 1");
+    const double M = sweeps;
+    switch (sm) {
+        case FlopSmoother::Gabp: return five ? 12.0 * M + 6.0 : 24.0 * M + 8.0;
+        case FlopSmoother::LineGabp:
+            if (!five)
+                throw InvalidArg("flop_table: line regions do not cover the nine-point stencil's diagonal couplings");
+            return sweeps == 1 ? 38.0 : 28.0 * M + 9.0;
+        case FlopSmoother::Gs: return five ? 9.0 * M : 17.0 * M;
+    }
+    return 0.0;
+}
+
+// thrown by a checked smoothing call at the breakdown (the reference's runtime_error, which stops
+// the cycle before the level's x += e, multigrid.cpp:183-186)
+struct MgBreak {};
+
 // reset every level's Ctrl the way the host template of Engine::reset_ctrl does; one block per level
 __global__ void k_mg_clear(Ctrl* const* c, int nl) {
     if ((int)blockIdx.x >= nl) return;
@@ -149,6 +170,32 @@ struct bgmg {
     unsigned long long* h_sum = nullptr;    // pinned copy of it
     std::vector<CycleGraph> graphs;
     bool use_graphs = true;
+    bool checked = false;       // smoothing calls synchronise and stop at a breakdown (MgBreak)
+    int fine_nx = 0;            // fine grid and the population of its centre row / of A
+    long long fine_center_nnz = 0, fine_nnz = 0;
+
+    // Hierarchy::cycle_flops_per_unknown (multigrid.cpp:240-274): the fine stencil is classified
+    // by its centre row (nine-point when it holds more than 5 entries)
+    double cycle_flops_per_unknown(const bgmg_cycle& spec) const {
+        const bool nine = fine_center_nnz > 5;
+        auto analytic = [&](int sweeps) -> double {
+            if (sweeps <= 0) return 0.0;
+            if (is_gabp(smoother)) return flop_table(!nine, FlopSmoother::Gabp, sweeps);
+            if (smoother == GabpLine && !nine) return flop_table(true, FlopSmoother::LineGabp, sweeps);
+            if (smoother >= Jacobi && smoother <= GsFC) return flop_table(!nine, FlopSmoother::Gs, sweeps);
+            const int n = levels[0].E->n;  // no closed form: multiply-adds per sweep
+            return sweeps * 2.0 * (double)fine_nnz / n;
+        };
+        return analytic(spec.pre) + analytic(spec.post);
+    }
+
+    // checked mode: synchronise after a cold smoothing call and stop at its breakdown
+    void check_breakdown(int k) {
+        if (!checked) return;
+        ck(cudaMemcpyAsync(h_ctrl, levels[k].E->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaStreamSynchronize(st), "sync");
+        if (h_ctrl->halt) throw MgBreak{};
+    }
 
     ~bgmg() {
         if (st) cudaStreamSynchronize(st);
@@ -187,6 +234,7 @@ struct bgmg {
             } else {
                 std::string unused;
                 L.cold_sweeps_dev(L.d_r, levels[k].sched, sweeps, L.d_e, unused, false, seq);
+                check_breakdown(k);
             }
             k_axpy1<<<g, 256, 0, st>>>(x, L.d_e, L.n);
             return;
@@ -202,6 +250,7 @@ struct bgmg {
             ck(cudaMemsetAsync(G.d_fail, 0xff, sizeof(unsigned long long), st), "memset");
             for (int s = 0; s < sweeps; ++s) G.sweep(L.d_r, 0, L.d_e);
             k_line_check<<<1, 1, 0, st>>>(L.d_ctrl, G.d_fail, seq);
+            check_breakdown(k);
             k_axpy1<<<g, 256, 0, st>>>(x, L.d_e, L.n);
             return;
         }
@@ -220,6 +269,7 @@ struct bgmg {
             for (int s = 0; s < sweeps; ++s) L.launch_gs_levels(lv, b, x);
         }
         k_plain_check<<<1, 1, 0, st>>>(L.d_ctrl, seq, 5);
+        check_breakdown(k);
     }
 
     // Hierarchy::cycle (multigrid.cpp:210-232)
@@ -346,6 +396,23 @@ struct bgmg {
         ck(cudaGetLastError(), "v-cycle");
     }
 
+    // One V-cycle as plain launches that stops at the first smoother breakdown, leaving x where
+    // the reference's exception leaves it (multigrid.cpp:234-238, 290-297): only the level-0
+    // updates made before the breakdown.  Breakdowns are rare, so the fast path never pays for
+    // this; the callers re-run a failed cycle in this mode from the same x.
+    void v_cycle_checked(const bgmg_cycle& spec, const double* b, double* x) {
+        prepare(spec);
+        clear_failures();
+        checked = true;
+        try {
+            cycle(0, spec, b, x);
+        } catch (const MgBreak&) {
+        }
+        checked = false;
+        fine_r_b = fine_r_x = nullptr;
+        ck(cudaGetLastError(), "v-cycle");
+    }
+
     void capture(CycleGraph& g, const bgmg_cycle& spec, const double* b, double* x) {
         const double *rb = fine_r_b, *rx = fine_r_x;
         cudaGraph_t graph = nullptr;
@@ -398,9 +465,22 @@ struct bgmg {
         return bits2d(r);
     }
 
-    // mg_solve (multigrid.cpp:276-318) on device vectors; history on the host
+    // mg_solve (multigrid.cpp:276-318) on device vectors; history on the host.  A smoother
+    // breakdown is detected after its cycle; the solve is then replayed (bit-identical up to that
+    // cycle) with the failing cycle checked, so x is the reference's partly cycled x.
     void solve_dev(const bgmg_cycle& spec, const double* b, double* x, const bgmg_options& o, bgabp_report& rep,
                    std::vector<double>& hist, std::string& detail) {
+        solve_loop(spec, b, x, o, rep, hist, detail, 0);
+        if (rep.status == BGABP_DIVERGED && detail != "residual blowup") {
+            bgabp_report r2{};
+            std::vector<double> h2;
+            std::string d2;
+            solve_loop(spec, b, x, o, r2, h2, d2, rep.iterations);
+        }
+    }
+
+    void solve_loop(const bgmg_cycle& spec, const double* b, double* x, const bgmg_options& o, bgabp_report& rep,
+                    std::vector<double>& hist, std::string& detail, int checked_cycle) {
         struct ClearR {  // the saved residual is only valid inside this loop
             bgmg* h;
             ~ClearR() { h->fine_r_b = h->fine_r_x = nullptr; }
@@ -418,8 +498,12 @@ struct bgmg {
             rep.status = BGABP_CONVERGED;
             return;
         }
+        const double per_cycle = cycle_flops_per_unknown(spec) * n;
         for (int it = 1; it <= o.max_cycles; ++it) {
-            v_cycle_dev(spec, b, x);
+            if (it == checked_cycle)
+                v_cycle_checked(spec, b, x);
+            else
+                v_cycle_dev(spec, b, x);
             // stop test and failure summary in one read
             Engine& L = E(0);
             ck(cudaMemsetAsync(&L.d_ctrl->red[2], 0, sizeof(unsigned long long), st), "memset");
@@ -438,6 +522,7 @@ struct bgmg {
                 return;
             }
             hist.push_back(r);
+            rep.flop_estimate += per_cycle;
             if (!std::isfinite(r) || r > o.divergence_factor * r0) {
                 rep.status = BGABP_DIVERGED;
                 detail = "residual blowup";
@@ -485,6 +570,12 @@ static void build_hierarchy(bgmg* h, int nlevels, const int* n, const int* const
     if (nlevels < 1) throw InvalidArg("Hierarchy: need 1 <= J2 and a coarsest exponent >= 1");
     if (!supported(smoother)) throw InvalidArg("Hierarchy: unsupported smoother " + std::to_string(smoother));
     h->smoother = smoother;
+    if (n[0] > 0 && (long long)nx[0] * nx[0] == n[0]) {  // cycle_flops_per_unknown's centre row
+        const int c = (nx[0] / 2) * nx[0] + nx[0] / 2;
+        h->fine_nx = nx[0];
+        h->fine_center_nnz = ro[0][c + 1] - ro[0][c];
+        h->fine_nnz = ro[0][n[0]];
+    }
     ck(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking), "stream");
     ck(cudaMallocHost((void**)&h->h_ctrl, sizeof(Ctrl)), "host ctrl");
     for (int k = 0; k < nlevels; ++k) {
@@ -603,6 +694,14 @@ int bgmg_level_frozen_ok(const bgmg* h, int k) {
     return h->levels[k].frozen_ok ? 1 : 0;
 }
 int bgmg_level_n(const bgmg* h, int k) { return h->levels[k].E->n; }
+int bgmg_level_nx(const bgmg* h, int k) { return h->levels[k].nx; }
+
+int bgmg_cycle_flops_per_unknown(const bgmg* h, const bgmg_cycle* spec, double* out, char* err, size_t errlen) {
+    MG_GUARD(err, errlen, {
+        *out = h->cycle_flops_per_unknown(*spec);
+        return BGABP_OK;
+    })
+}
 void* bgmg_stream(bgmg* h) { return (void*)h->st; }
 
 int bgmg_fine_rhs(const bgmg* h, double* b_out) {
@@ -619,9 +718,13 @@ int bgmg_vcycle(bgmg* h, const bgmg_cycle* spec, const double* b, double* x, cha
         host_to_device(h->d_fine_x, x, sizeof(double) * n, h->st);
         h->fine_r_b = h->fine_r_x = nullptr;
         h->v_cycle_dev(*spec, h->d_fine_b, h->d_fine_x);
+        std::string f = h->failure();
+        if (!f.empty()) {  // replay from the caller's x, stopping where the reference's exception does
+            host_to_device(h->d_fine_x, x, sizeof(double) * n, h->st);
+            h->v_cycle_checked(*spec, h->d_fine_b, h->d_fine_x);
+        }
         device_to_host(x, h->d_fine_x, sizeof(double) * n, h->st);
         ck(cudaStreamSynchronize(h->st), "sync");
-        std::string f = h->failure();
         if (!f.empty()) {
             put_err(err, errlen, f);
             return BGABP_ERUNTIME;

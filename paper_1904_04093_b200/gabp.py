@@ -106,6 +106,8 @@ def lib():
             "bgmg_num_levels": (C.c_int, [_vp]),
             "bgmg_level_frozen_ok": (C.c_int, [_vp, C.c_int]),
             "bgmg_level_n": (C.c_int, [_vp, C.c_int]),
+            "bgmg_level_nx": (C.c_int, [_vp, C.c_int]),
+            "bgmg_cycle_flops_per_unknown": (C.c_int, [_vp, C.POINTER(_Cycle), _dp, C.c_char_p, C.c_size_t]),
             "bgmg_fine_rhs": (C.c_int, [_vp, _dp]),
             "bgmg_vcycle": (C.c_int, [_vp, C.POINTER(_Cycle), _dp, _dp, C.c_char_p, C.c_size_t]),
             "bgmg_solve": (C.c_int, [_vp, C.POINTER(_Cycle), _dp, C.POINTER(_MgOpts), C.POINTER(_Rep), _dp, _dp,
@@ -678,6 +680,17 @@ class Hierarchy:
     def level_n(self, k):
         return lib().bgmg_level_n(self._h, k)
 
+    def level_nx(self, k):
+        return lib().bgmg_level_nx(self._h, k)
+
+    def cycle_flops_per_unknown(self, spec: CycleSpec) -> float:
+        """multigrid.cpp:240-274 (analytic flop_table of the pre + post sweeps)."""
+        out = C.c_double(0.0)
+        err = C.create_string_buffer(256)
+        c = spec._c()
+        _raise(lib().bgmg_cycle_flops_per_unknown(self._h, C.byref(c), C.byref(out), err, 256), err.value.decode())
+        return out.value
+
     def smoother(self):
         return self._smoother
 
@@ -707,8 +720,15 @@ def mg_solve(hier: Hierarchy, spec: CycleSpec, b, opt: MgSolveOptions = MgSolveO
     c, o = spec._c(), opt._c()
     rc = lib().bgmg_solve(hier._h, C.byref(c), _d(_f64(b)), C.byref(o), C.byref(rep), _d(x), _d(hist), det, 512)
     _raise(rc, det.value.decode())
-    return SolveReport(SolveStatus(rep.status), rep.iterations, hist[: rep.iterations + 1].copy(), 0.0, x,
-                       det.value.decode())
+    d = det.value.decode()
+    return SolveReport(SolveStatus(rep.status), rep.iterations, hist[: _mg_hist_len(rep, d)].copy(),
+                       rep.flop_estimate, x, d)
+
+
+def _mg_hist_len(rep, detail):
+    """iterations + 1 residuals, one fewer when the last cycle broke down (multigrid.cpp:288-297)."""
+    breakdown = rep.status == SolveStatus.Diverged and detail != "residual blowup"
+    return rep.iterations + (0 if breakdown else 1)
 
 
 def mg_solve_device(hier: Hierarchy, spec: CycleSpec, b_ptr, x_ptr, opt: MgSolveOptions = MgSolveOptions()):
@@ -719,8 +739,9 @@ def mg_solve_device(hier: Hierarchy, spec: CycleSpec, b_ptr, x_ptr, opt: MgSolve
     rc = lib().bgmg_solve_device(hier._h, C.byref(c), C.c_void_p(b_ptr), C.byref(o), C.byref(rep), C.c_void_p(x_ptr),
                                  _d(hist), det, 512)
     _raise(rc, det.value.decode())
-    return SolveReport(SolveStatus(rep.status), rep.iterations, hist[: rep.iterations + 1].copy(), 0.0,
-                       np.zeros(0), det.value.decode())
+    d = det.value.decode()
+    return SolveReport(SolveStatus(rep.status), rep.iterations, hist[: _mg_hist_len(rep, d)].copy(),
+                       rep.flop_estimate, np.zeros(0), d)
 
 
 def mg_restrict(fine, mf):

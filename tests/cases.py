@@ -141,3 +141,26 @@ CASES = {
 def build_case(o, name):
     """(A, b, schedule) for `name`, built with the restatement's generators (oracle `o`)."""
     return _build(o, name)
+
+
+def grid5_const(orc, nx, d):
+    """nx x nx 5-point matrix, diagonal d, off-diagonals -1 (canonical CSR)."""
+    rows, cols, vals = [], [], []
+    for iy in range(nx):
+        for ix in range(nx):
+            i = iy * nx + ix
+            for dx, dy in ((0, -1), (-1, 0), (0, 0), (1, 0), (0, 1)):
+                jx, jy = ix + dx, iy + dy
+                if 0 <= jx < nx and 0 <= jy < nx:
+                    rows.append(i)
+                    cols.append(jy * nx + jx)
+                    vals.append(d if (dx, dy) == (0, 0) else -1.0)
+    return orc.make_csr(nx * nx, rows, cols, vals)
+
+
+def mg_breakdown_levels(orc, fine_diag):
+    """Three levels (7^2, 3^2, 1) whose fine level breaks the GaBP smoother: with diagonal 1 a
+    flood sweep hits a zero edge pivot in its second sweep, with diagonal 2 a red-black or flood
+    sweep hits a zero node pivot in its first.  The coarse levels are diagonally dominant (the
+    setup probe keeps them)."""
+    return [grid5_const(orc, 7, fine_diag), grid5_const(orc, 3, 8.0), grid5_const(orc, 1, 8.0)], [7, 3, 1]

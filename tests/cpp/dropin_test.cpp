@@ -8,7 +8,9 @@
 #include <string>
 #include <vector>
 
+#include "belief/analysis.hpp"
 #include "belief/gabp.hpp"
+#include "belief/problems.hpp"
 #include "belief/schedule.hpp"
 #include "belief/sparse.hpp"
 #include "belief_b200.hpp"
@@ -76,6 +78,18 @@ int main() {
                    same(r1.solution, r2.solution) && r1.flop_estimate == r2.flop_estimate && r1.detail == r2.detail);
     }
     {
+        const MessageGraph& g1 = ref.graph();
+        const MessageGraph& g2 = gpu.graph();
+        bool ok = g1.n == g2.n && g1.num_edges == g2.num_edges && g1.diag_pos == g2.diag_pos &&
+                  g1.out_edges.size() == g2.out_edges.size();
+        for (size_t j = 0; ok && j < g1.out_edges.size(); ++j) {
+            ok = g1.out_edges[j].size() == g2.out_edges[j].size();
+            for (size_t e = 0; ok && e < g1.out_edges[j].size(); ++e)
+                ok = g1.out_edges[j][e].pos == g2.out_edges[j][e].pos && g1.out_edges[j][e].row == g2.out_edges[j][e].row;
+        }
+        report("graph() equals the reference's message graph", ok);
+    }
+    {
         Schedule rb = Schedule::red_black_grid(24, 20);
         FrozenLambda f1 = ref.precompute_lambda(rb), f2 = gpu.precompute_lambda(rb);
         bool ok = f1.converged == f2.converged && f1.iterations == f2.iterations && same(f1.lambda_tilde, f2.lambda_tilde) &&
@@ -114,6 +128,28 @@ int main() {
         SolveReport r = cuda::mg_solve(h, spec, h.fine_rhs(), o);
         report("Hierarchy + mg_solve (poisson J=6, red-black GaBP V(2,2))",
                h.num_levels() == 4 && r.status == SolveStatus::Converged && r.iterations <= 10);
+        // flop_estimate: cycle_flops_per_unknown * n per cycle, through the reference's own
+        // flop_table (analysis.cpp:135-154, compiled in): 5-point stencil, GaBP, 2 + 2 sweeps
+        const double per = flop_table(FlopStencil::FivePoint, FlopSmoother::Gabp, 2) * 2.0;
+        report("mg_solve flop_estimate = cycles * cycle_flops_per_unknown * n",
+               h.cycle_flops_per_unknown(spec) == per &&
+                   r.flop_estimate == r.iterations * per * static_cast<double>(h.fine_rhs().size()) &&
+                   r.flop_estimate > 0.0);
+        // caller-supplied levels (the reference's own assemble()) give the same hierarchy
+        std::vector<AssembledProblem> lv;
+        for (int J = 6; J >= 3; --J) lv.push_back(assemble("poisson", J));
+        cuda::Hierarchy hl(lv, MgSmoother::GabpRedBlack);
+        SolveReport rl = cuda::mg_solve(hl, spec, lv[0].b, o);
+        bool same_levels = hl.num_levels() == h.num_levels();
+        for (int k = 0; same_levels && k < h.num_levels(); ++k)
+            same_levels = same(hl.level(k).prob.A.values, h.level(k).prob.A.values) &&
+                          hl.level(k).prob.A.transpose_pos == h.level(k).prob.A.transpose_pos &&
+                          hl.level(k).prob.grid.nx == lv[k].grid.nx && hl.level(k).frozen_ok == h.level(k).frozen_ok;
+        report("from-levels Hierarchy == named Hierarchy (levels, report bits)",
+               same_levels && rl.status == r.status && rl.iterations == r.iterations &&
+                   same(rl.residual_history, r.residual_history) && same(rl.solution, r.solution) &&
+                   rl.flop_estimate == r.flop_estimate && same(h.fine_exact(), lv[0].exact) &&
+                   same(h.fine_rhs(), lv[0].b));
         Vector u = rand_vec(49, 1);
         Vector Ru = cuda::mg_restrict(u, 7), Pv = cuda::mg_prolong(rand_vec(9, 2), 3);
         report("mg_restrict / mg_prolong shapes", Ru.size() == 9 && Pv.size() == 49);

@@ -52,3 +52,16 @@ def test_invalid_inputs_rejected_before_any_device_work():
     B = SparseMatrix(2, np.array([0, 2, 4], np.int32), np.array([1, 0, 0, 1], np.int32), np.ones(4))
     with pytest.raises(ValueError, match="canonical"):
         GabpEngine(B)
+
+
+def test_bench_reference_arm_loads_only_the_oracle():
+    """The reference arm's input comes from the oracle's own generators: the product library
+    must not be mapped into that process (the driver records the .so files each arm loads)."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.argv=['bench.py']; import bench; o, kind, A, b = bench.oracle_config2(); "
+            "print(A.n, b.shape[0]); print(open('/proc/self/maps').read())")
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr
+    assert out.stdout.startswith("4194304 4194304")
+    assert "libgabp_b200" not in out.stdout

@@ -125,3 +125,88 @@ def test_restatement_bitwise_equals_reference_library(orc, ref):
             assert all(np.array_equal(p, q) for p, q in zip(so + (xo,), sr + (xr,))), name
             if not oko[0]:
                 break
+
+
+def test_flop_table_restatement_equals_reference(orc, ref):
+    """flop_table (analysis.cpp:135-154): values and the invalid_argument texts."""
+    if ref is None:
+        pytest.skip("oracle/_ref not built")
+    for stencil in (0, 1):
+        for sm in (0, 1, 2, 3):
+            for sweeps in (0, 1, 2, 3, 6):
+                got = want = None
+                try:
+                    want = ref.flop_table(stencil, sm, sweeps)
+                except ValueError as e:
+                    want = str(e)
+                try:
+                    got = orc.flop_table(stencil, sm, sweeps)
+                except ValueError as e:
+                    got = str(e)
+                assert got == want, (stencil, sm, sweeps)
+
+
+MG_ORACLE_CASES = [("poisson", 5, 3, 1, 2, 2, {}), ("poisson", 5, 3, 0, 1, 1, {}), ("poisson", 5, 3, 7, 2, 2, {}),
+                   ("mixed", 5, 3, 2, 0, 4, {}), ("boundary-layer", 6, 6, 3, 2, 2, {"eps": 0.01}),
+                   ("general", 5, 3, 3, 2, 2, {})]
+
+
+@pytest.mark.parametrize("prob,J1,J2,sm,pre,post,params", MG_ORACLE_CASES)
+def test_mg_restatement_bitwise_equals_reference_library(orc, ref, prob, J1, J2, sm, pre, post, params):
+    """The multigrid restatement (abi_impl.inc) over the restated engine equals it over the
+    reference's compiled engine bit for bit: history, x (also after a smoother breakdown, the
+    boundary-layer flood case), flop estimate (flop_table of analysis.cpp) and cycle flops."""
+    if ref is None:
+        pytest.skip("oracle/_ref not built")
+    from oracle.oracle import Csr
+    levels = [ref.assemble(prob, J, params) for J in range(J1, J1 - J2, -1)]
+    mats = [Csr(A.n, A.row_offsets, A.col_indices, A.values) for A, *_ in levels]
+    nxs = [nx for _, _, _, nx, _ in levels]
+    b = levels[0][1]
+    ho, hr = orc.hierarchy(mats, nxs, sm), ref.hierarchy(mats, nxs, sm)
+    assert ho.num_levels == hr.num_levels
+    assert ho.cycle_flops_per_unknown(pre, post) == hr.cycle_flops_per_unknown(pre, post)
+    ro = ho.solve(pre, post, b, tol=1e-8 * np.abs(b).max(), max_cycles=30)
+    rr = hr.solve(pre, post, b, tol=1e-8 * np.abs(b).max(), max_cycles=30)
+    assert (ro.status, ro.iterations, ro.detail, ro.flop_estimate) == (rr.status, rr.iterations, rr.detail,
+                                                                       rr.flop_estimate)
+    assert ro.residual_history.tobytes() == rr.residual_history.tobytes()
+    assert ro.solution.tobytes() == rr.solution.tobytes()
+    if rr.detail.startswith("smoother breakdown"):
+        assert rr.residual_history.size == rr.iterations  # the failed cycle has no residual
+    else:
+        assert rr.residual_history.size == rr.iterations + 1
+        assert rr.flop_estimate == rr.iterations * hr.cycle_flops_per_unknown(pre, post) * b.size
+
+
+@pytest.mark.parametrize("fine_diag,sm,pre,post", [(1.0, 3, 1, 2), (1.0, 3, 2, 2), (2.0, 1, 1, 1), (1.0, 3, 1, 0)])
+def test_mg_breakdown_x_restatement_equals_reference_library(orc, ref, fine_diag, sm, pre, post):
+    """A smoother breakdown stops the cycle where the reference's exception does: x keeps the
+    level-0 updates made before it (multigrid.cpp:290-297; V(1,2) flood breaks in the post-smoothing
+    call, after the pre-smoothing and the coarse correction were added)."""
+    if ref is None:
+        pytest.skip("oracle/_ref not built")
+    from tests.cases import mg_breakdown_levels
+    mats, nxs = mg_breakdown_levels(orc, fine_diag)
+    b = orc.rng(9).vector(49)
+    out = []
+    for o in (orc, ref):
+        h = o.hierarchy(mats, nxs, sm)
+        assert h.num_levels == 3
+        out.append(h.solve(pre, post, b, tol=1e-10, max_cycles=10))
+        try:
+            h.v_cycle(pre, post, b, np.zeros(49))
+            out.append(None)
+        except RuntimeError as e:
+            out.append(e.args)
+    (ro, eo), (rr, er) = out[:2], out[2:]
+    if post == 0:
+        assert rr.status != 1 or rr.detail == "residual blowup"
+        return
+    assert rr.status == 1 and rr.detail.startswith("smoother breakdown on level 0"), rr.detail
+    assert (ro.status, ro.iterations, ro.detail, ro.flop_estimate) == (rr.status, rr.iterations, rr.detail,
+                                                                       rr.flop_estimate)
+    assert ro.residual_history.tobytes() == rr.residual_history.tobytes()
+    assert ro.solution.tobytes() == rr.solution.tobytes()
+    assert eo[0] == er[0] and eo[1].tobytes() == er[1].tobytes() == rr.solution.tobytes()
+    assert (np.abs(rr.solution).max() == 0.0) == (pre >= 2 or fine_diag == 2.0)
