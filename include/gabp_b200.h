@@ -116,6 +116,12 @@ int bgabp_sweep(bgabp_engine* e, const double* b, const bgabp_schedule* sched, d
 
 /* node_precisions(state) (gabp.cpp:403-419) of the handle's current state */
 int bgabp_node_precisions(bgabp_engine* e, double* beta);
+/* Optional message damping of the flood sweep (BASELINE.json north_star; the reference has none,
+ * SPEC.md:197): from now on every message the handle's flood sweeps and solves compute becomes
+ * (1 - alpha) * new + alpha * old on its edge (products rounded before the add).  alpha = 0 (the
+ * default) is the reference's update bit for bit.  EINVAL unless 0 <= alpha < 1; with alpha != 0
+ * ordered schedules and sharded solves return EINVAL. */
+int bgabp_set_damping(bgabp_engine* e, double alpha);
 double bgabp_sweep_flops(const bgabp_engine* e); /* gabp.cpp:165-172 */
 
 /* ---- solve(b, sched, opt) (gabp.cpp:174-219) ------------------------------------------------------

@@ -508,7 +508,7 @@ private:
     }
     // one outgoing message j->i from node aggregates and the reverse message (gabp.cpp:77-96)
     bool emit(int j, const Out& o, double sig, double acc, const MessageState& src,
-              MessageState& dst, std::string* err, double* delta) const {
+              MessageState& dst, std::string* err, double* delta, bool damp = false) const {
         const double a = A_.values[o.pos];
         const int tp = A_.transpose_pos[o.pos];
         const double lr = tp >= 0 ? src.lambda_tilde[tp] : 0.0;
@@ -518,8 +518,12 @@ private:
             if (err) *err = "zero pivot on edge " + std::to_string(j) + "->" + std::to_string(o.dst);
             return false;
         }
-        const double nl = -a / den;
-        const double nm = nl * (acc - mr);
+        double nl = -a / den;
+        double nm = nl * (acc - mr);
+        if (damp) {  // extension (no reference counterpart): convex blend with the old message
+            nl = undamp_ * nl + damping_ * src.lambda_tilde[o.pos];
+            nm = undamp_ * nm + damping_ * src.m[o.pos];
+        }
         if (delta) {
             *delta = std::max(*delta, std::abs(nl - src.lambda_tilde[o.pos]));
             *delta = std::max(*delta, std::abs(nm - src.m[o.pos]));
@@ -561,7 +565,7 @@ private:
             double sig, acc;
             aggregate(j, b[j], prev, sig, acc);
             for (const Out& o : out_[j])
-                if (!emit(j, o, sig, acc, prev, st, err, max_delta ? &delta : nullptr)) return false;
+                if (!emit(j, o, sig, acc, prev, st, err, max_delta ? &delta : nullptr, damping_ != 0.0)) return false;
         }
         for (int i = 0; i < A_.n; ++i) {
             double sig, acc;
@@ -580,6 +584,15 @@ private:
     std::vector<std::vector<Out>> out_;
     std::vector<int> diag_;
     long num_edges_ = 0;
+    double damping_ = 0.0, undamp_ = 1.0;
+
+public:
+    // Optional message damping of the flood sweep (BASELINE.json north_star; the reference has
+    // none): every new message becomes (1 - a) * new + a * old on its edge; 0 = the reference.
+    void set_damping(double a) {
+        damping_ = a;
+        undamp_ = 1.0 - a;
+    }
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -787,4 +800,5 @@ int tree_diameter(int n, const std::vector<std::pair<int, int>>& edges) {  // or
 namespace abi_ns = orc;
 inline long abi_num_edges(const orc::GabpEngine& e) { return e.num_edges(); }
 #define ORC_HAVE_GENERATORS 1
+#define ABI_HAS_DAMPING 1
 #include "abi_impl.inc"

@@ -166,6 +166,7 @@ class Oracle:
             "orc_mg_solve": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, _dp, C.c_double, C.c_int,
                                        C.c_double, _dp, _dp, _ip, _ip, _dp, _ip, C.c_char_p, C.c_size_t]),
             "orc_mg_cycle_flops": (C.c_double, [vp, C.c_int, C.c_int]),
+            "orc_set_damping": (C.c_int, [vp, C.c_double]),
             "orc_flop_table": (C.c_double, [C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_size_t]),
             "orc_mg_restrict": (None, [_dp, C.c_int, _dp]),
             "orc_mg_prolong": (None, [_dp, C.c_int, _dp]),
@@ -460,6 +461,11 @@ class _Engine:
     @property
     def num_edges(self):
         return self.o.lib.orc_engine_num_edges(self.h)
+
+    def set_damping(self, alpha):
+        """Flood message damping (restatement only; the reference engine accepts just 0)."""
+        if self.o.lib.orc_set_damping(self.h, float(alpha)) != 1:
+            raise ValueError("damping is not available in the reference engine")
 
     def sweep_flops(self):
         return self.o.lib.orc_sweep_flops(self.h)

@@ -5,7 +5,7 @@
 // holds the schedules (dependency levels), the sweep / solve loops and the C-ABI; construction is
 // in build.cu, device memory and caller-buffer copies in memory.cu, the sharded solve in
 // shard.cu.  Every sweep, residual and reduction runs in the kernels of kernels.cuh (and
-// rb_ / seq_ / seqpipe_ / flood2_kernels.cuh).  There is no CPU fallback: a failed CUDA call is
+// rb_ / seq_ / seqpipe_kernels.cuh).  There is no CPU fallback: a failed CUDA call is
 // BGABP_ECUDA.
 #include <algorithm>
 #include <cmath>
@@ -202,11 +202,21 @@ void Engine::launch_flood(const double* b, double2* m0, double2* m1, double* x, 
                           long long xstride) {
     if (n == 0) return;
     const unsigned g = nblk(n);
+    const bool damp = damping != 0.0;
     if (layout == BGABP_LAYOUT_DIA) {
-        DIA_SWITCH(S, if (delta) k_flood_dia<SS, true><<<g, 256, 0, st>>>(dia, b, m0, m1, x, d_ctrl, mode);
-                   else k_flood_dia<SS, false><<<g, 256, 0, st>>>(dia, b, m0, m1, x, d_ctrl, mode));
+        if (damp) {
+            DIA_SWITCH(S, if (delta) k_flood_dia<SS, true, true><<<g, 256, 0, st>>>(dia, b, m0, m1, x, d_ctrl, mode);
+                       else k_flood_dia<SS, false, true><<<g, 256, 0, st>>>(dia, b, m0, m1, x, d_ctrl, mode));
+        } else {
+            DIA_SWITCH(S, if (delta) k_flood_dia<SS, true><<<g, 256, 0, st>>>(dia, b, m0, m1, x, d_ctrl, mode);
+                       else k_flood_dia<SS, false><<<g, 256, 0, st>>>(dia, b, m0, m1, x, d_ctrl, mode));
+        }
     } else {
-        if (delta)
+        if (delta && damp)
+            k_flood_csr<true, true><<<g, 256, 0, st>>>(csr, b, m0, m1, x, d_ctrl, mode, xstride);
+        else if (damp)
+            k_flood_csr<false, true><<<g, 256, 0, st>>>(csr, b, m0, m1, x, d_ctrl, mode, xstride);
+        else if (delta)
             k_flood_csr<true><<<g, 256, 0, st>>>(csr, b, m0, m1, x, d_ctrl, mode, xstride);
         else
             k_flood_csr<false><<<g, 256, 0, st>>>(csr, b, m0, m1, x, d_ctrl, mode, xstride);
@@ -310,7 +320,23 @@ std::string Engine::ordered_detail(const std::vector<int>& order, unsigned long 
 // ---------------------------------------------------------------------------------------------
 // one sweep (gabp.cpp:42-47)
 // ---------------------------------------------------------------------------------------------
+void Engine::set_damping(double a) {
+    if (!(a >= 0.0 && a < 1.0)) throw InvalidArg("gabp: damping must lie in [0, 1)");
+    if (a == damping) return;
+    ck(cudaStreamSynchronize(st), "sync");
+    drop_graphs();  // captured solve chunks hold the undamped (or damped) kernels
+    damping = a;
+    dia.damp = csr.damp = a;
+    dia.undamp = csr.undamp = 1.0 - a;
+}
+
+void Engine::check_damping(const bgabp_schedule& s) const {
+    if (damping != 0.0 && s.kind != BGABP_SCHED_FLOOD)
+        throw InvalidArg("gabp: message damping applies to the parallel flood schedule only");
+}
+
 int Engine::sweep(const double* b, const bgabp_schedule& s, double* x, std::string& err) {
+    check_damping(s);
     if (s.kind == BGABP_SCHED_FLOOD) {
         if (n == 0) return BGABP_OK;
         reset_ctrl();
@@ -375,22 +401,10 @@ int Engine::sweep(const double* b, const bgabp_schedule& s, double* x, std::stri
 // ---------------------------------------------------------------------------------------------
 void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bgabp_options& o,
                          const double* r0_override) {
+    check_damping(s);
+    if (damping != 0.0 && r0_override) throw InvalidArg("gabp: message damping is not supported by sharded solves");
     solve_flood = s.kind == BGABP_SCHED_FLOOD;
     solve_fused = solve_flood && layout == BGABP_LAYOUT_DIA;
-    {
-        const char* e = std::getenv("BGABP_FLOOD2");
-        const bool sharded = dia.j0 != 0 || dia.j1 != n || dia.gofs != 0;
-        // opt-in (BGABP_FLOOD2=1): bit-identical and half the DRAM traffic per iteration, but
-        // latency-bound at 168 registers / 12 warps per SM -- on par with the one-iteration step
-        // on the B200, so the one-iteration step stays the default
-        solve_double = solve_fused && grid5 && !sharded && o.stop == BGABP_STOP_RESIDUAL && e && std::atoi(e) != 0;
-        if (const char* hh = std::getenv("BGABP_FLOOD2_H")) flood2_h = std::max(1, std::atoi(hh));
-        if (const char* e2 = std::getenv("BGABP_FLOOD2_ST")) flood2_st = std::min(5, std::max(3, std::atoi(e2)));
-        if (const char* e3 = std::getenv("BGABP_FLOOD2_MINB")) flood2_minb = std::atoi(e3);
-        if (const char* e4 = std::getenv("BGABP_FLOOD2_KIND")) flood2_band = std::string(e4) == "band";
-        if (const char* e5 = std::getenv("BGABP_FLOOD2_R")) flood2_r = std::atoi(e5);
-        if (solve_double) enqueue_double_kernel(true);
-    }
     solve_levels = solve_flood ? nullptr : &levels_for(s);
     solve_rb = !solve_flood && rb_applicable(s);
     solve_seq = !solve_flood && !solve_rb && seq_applicable(s);
@@ -422,9 +436,8 @@ void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bga
         ck(cudaMemsetAsync(d_xord, 0, sizeof(double) * 2 * (size_t)std::max(n, 1), st), "memset x ring");
     }
     if (solve_fused) {
-        // kXRing2 slots: the two-iteration launch keeps x(k) in slot k % 4 (single steps use 0, 1)
-        if (!d_xf) d_xf = static_cast<double*>(dalloc(sizeof(double) * kXRing2 * (size_t)std::max(n, 1)));
-        ck(cudaMemsetAsync(d_xf, 0, sizeof(double) * kXRing2 * (size_t)std::max(n, 1), st), "memset x ring");
+        if (!d_xf) d_xf = static_cast<double*>(dalloc(sizeof(double) * kXRing * (size_t)std::max(n, 1)));
+        ck(cudaMemsetAsync(d_xf, 0, sizeof(double) * kXRing * (size_t)std::max(n, 1), st), "memset x ring");
     }
     ck(cudaMemsetAsync(d_spread, 0, sizeof(unsigned long long) * 8 * kSpread, st), "memset");
     if (d_slots)  // peer-memory shards: words and step flags of the previous solve
@@ -456,12 +469,6 @@ void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bga
 }
 
 void Engine::enqueue_step() {
-    if (solve_double) {  // iterations t and t+1, then their decisions in order
-        enqueue_double_kernel();
-        k_solve_decide_lag2<<<1, kSpread, 0, st>>>(d_ctrl, d_hist, d_spread);
-        k_solve_decide_lag2<<<1, kSpread, 0, st>>>(d_ctrl, d_hist, d_spread);
-        return;
-    }
     if (solve_fused) {
         enqueue_fused_kernel();
         k_solve_decide_lag2<<<1, kSpread, 0, st>>>(d_ctrl, d_hist, d_spread);
@@ -504,6 +511,14 @@ void Engine::enqueue_fused_kernel() {
 #define FUSED(SS_, MB_, DF_, MBU_, DFU_)                                                                            \
     if (sharded) {                                                                                                 \
         launch_sharded_step<SS_, MB_, DF_>(*this, g, dl);                                                          \
+    } else if (damping != 0.0) {  /* damped messages: the general-coefficient step (c arrays exist) */           \
+        if (symmetric) {                                                                                           \
+            if (dl) k_flood_solve_dia<SS_, true, true, MB_, DF_, true, false, false, false, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
+            else k_flood_solve_dia<SS_, false, true, MB_, DF_, true, false, false, false, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
+        } else {                                                                                                   \
+            if (dl) k_flood_solve_dia<SS_, true, false, MB_, DF_, true, false, false, false, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
+            else k_flood_solve_dia<SS_, false, false, MB_, DF_, true, false, false, false, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
+        }                                                                                                          \
     } else if (dia.uniform) {                                                                                      \
         if (dl) k_flood_solve_dia<SS_, true, true, MBU_, DFU_, true, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
         else k_flood_solve_dia<SS_, false, true, MBU_, DFU_, true, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
@@ -529,74 +544,6 @@ void Engine::enqueue_fused_kernel() {
 #undef FUSED
         if (timed_events) ck(cudaEventRecord((*timed_events)[2 * timed_index + 1], st), "event");
     }
-}
-
-template <bool UNIF, bool SYM, int TPB, int MINB, int ST>
-static void launch_flood2(const DiaP& dia, int nx, int ny, int H, const double* b, double2* m0, double2* m1, double* xf,
-                          Ctrl* ctrl, unsigned long long* spread, cudaStream_t st) {
-    const size_t smem = sizeof(Stage5<UNIF, SYM, TPB, ST>);
-    if (!b) {  // attribute pass (solve_begin, outside any stream capture)
-        ck(cudaFuncSetAttribute(k_flood2_grid5<UNIF, SYM, TPB, MINB, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem),
-           "flood2 smem");
-        return;
-    }
-    const dim3 grid((unsigned)((nx + TPB - 5) / (TPB - 4)), (unsigned)((ny + H - 1) / H));
-    k_flood2_grid5<UNIF, SYM, TPB, MINB, ST><<<grid, TPB, smem, st>>>(dia, nx, ny, H, b, m0, m1, xf, ctrl, spread);
-}
-
-template <bool UNIF, bool SYM, int R, int MINB>
-static void launch_flood2b(const DiaP& dia, int nx, int ny, int H, const double* b, double2* m0, double2* m1,
-                           double* xf, Ctrl* ctrl, unsigned long long* spread, cudaStream_t st) {
-    const size_t smem = sizeof(Band5Smem<UNIF, SYM, R>);
-    if (!b) {  // attribute pass (solve_begin, outside any stream capture)
-        ck(cudaFuncSetAttribute(k_flood2b_grid5<UNIF, SYM, R, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem),
-           "flood2b smem");
-        return;
-    }
-    const dim3 grid((unsigned)((nx + 123) / 124), (unsigned)((ny + H - 1) / H));
-    k_flood2b_grid5<UNIF, SYM, R, MINB><<<grid, dim3(128, R), smem, st>>>(dia, nx, ny, H, b, m0, m1, xf, ctrl, spread);
-}
-
-void Engine::enqueue_double_kernel(bool attr_only) {
-    if (flood2_band) {
-        const int nx = grid5_nx, ny = n / std::max(grid5_nx, 1);
-        const double* bb = attr_only ? nullptr : solve_b;
-        if (timed_events) ck(cudaEventRecord((*timed_events)[2 * timed_index], st), "event");
-        if (dia.uniform && flood2_r == 41)
-            launch_flood2b<true, true, 4, 1>(dia, nx, ny, flood2_h, bb, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread, st);
-        else if (dia.uniform && flood2_r == 22)
-            launch_flood2b<true, true, 2, 2>(dia, nx, ny, flood2_h, bb, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread, st);
-        else if (dia.uniform && flood2_r == 12)
-            launch_flood2b<true, true, 1, 2>(dia, nx, ny, flood2_h, bb, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread, st);
-        else if (dia.uniform)
-            launch_flood2b<true, true, 4, 2>(dia, nx, ny, flood2_h, bb, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread, st);
-        else if (symmetric)
-            launch_flood2b<false, true, 4, 1>(dia, nx, ny, flood2_h, bb, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread, st);
-        else
-            launch_flood2b<false, false, 4, 1>(dia, nx, ny, flood2_h, bb, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread, st);
-        ck(cudaGetLastError(), "flood2b");
-        if (timed_events) ck(cudaEventRecord((*timed_events)[2 * timed_index + 1], st), "event");
-        return;
-    }
-    constexpr int TPB = 128;
-    const int nx = grid5_nx, ny = n / std::max(grid5_nx, 1);
-    const double* bb = attr_only ? nullptr : solve_b;
-    if (timed_events) ck(cudaEventRecord((*timed_events)[2 * timed_index], st), "event");
-    if (dia.uniform && flood2_st == 3)
-        launch_flood2<true, true, TPB, 3, 3>(dia, nx, ny, flood2_h, bb, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread, st);
-    else if (dia.uniform && flood2_st == 5)
-        launch_flood2<true, true, TPB, 3, 5>(dia, nx, ny, flood2_h, bb, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread, st);
-    else if (dia.uniform)
-        launch_flood2<true, true, TPB, 3, 4>(dia, nx, ny, flood2_h, bb, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread, st);
-    else if (symmetric)
-        launch_flood2<false, true, TPB, 3, 4>(dia, nx, ny, flood2_h, bb, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread, st);
-    else
-        launch_flood2<false, false, TPB, 2, 4>(dia, nx, ny, flood2_h, bb, d_msg[0], d_msg[1], d_xf, d_ctrl, d_spread,
-                                               st);
-    ck(cudaGetLastError(), "flood2");
-    if (timed_events) ck(cudaEventRecord((*timed_events)[2 * timed_index + 1], st), "event");
 }
 
 void Engine::enqueue_step_other() {
@@ -630,7 +577,7 @@ void Engine::enqueue_step_other() {
 }
 
 bool Engine::chunk_graph_eligible() const {
-    const size_t per_step = solve_double ? 3 : solve_fused ? 2 : solve_flood ? 3 : solve_levels->ptr.size() + 1;
+    const size_t per_step = solve_fused ? 2 : solve_flood ? 3 : solve_levels->ptr.size() + 1;
     return per_step * kChunk <= 4096 && n > 0 && !solve_seq;  // cooperative launches stay out of graphs
 }
 
@@ -638,8 +585,8 @@ bool Engine::chunk_graph_eligible() const {
 // below it for the remainder of a steps call).  Captured on first use; capture records the
 // launches without running them, so solve_begin takes them all outside the caller's loop.
 cudaGraphExec_t Engine::chunk_graph(int len) {
-    const std::string key = std::string(solve_double ? "D" : solve_fused ? "F" : solve_flood ? "f" : "o") +
-                            std::to_string(solve_stop) + ":" + std::to_string(flood2_h) + ":" +
+    const std::string key = std::string(solve_fused ? "F" : solve_flood ? "f" : "o") +
+                            std::to_string(solve_stop) + ":" +
                             std::to_string((long long)(uintptr_t)solve_b) + ":" +
                             std::to_string((long long)(uintptr_t)solve_levels) + ":" + std::to_string(len);
     auto it = graphs.find(key);
@@ -651,6 +598,7 @@ cudaGraphExec_t Engine::chunk_graph(int len) {
         cudaGraphExec_t ge;
         ck(cudaGraphInstantiate(&ge, g, 0), "graph instantiate");
         cudaGraphDestroy(g);
+        ck(cudaGraphUpload(ge, st), "graph upload");  // the first launch then pays no upload
         it = graphs.emplace(key, ge).first;
     }
     return it->second;
@@ -667,8 +615,6 @@ void Engine::solve_steps(int nsteps) {
     }
     // graph-replay chunks of iterations: the kernels read their step index from the device,
     // so one captured chunk is valid for any position in the loop
-    const int per_call = solve_double ? 2 : 1;  // iterations per enqueue_step
-    if (solve_double) nsteps = (nsteps + 1) / 2;  // enqueue_step calls
     const bool use_graph = chunk_graph_eligible();
     int left = nsteps;
     while (left > 0) {
@@ -684,7 +630,7 @@ void Engine::solve_steps(int nsteps) {
             for (int k = 0; k < chunk; ++k) enqueue_step();
         }
         left -= chunk;
-        steps_enqueued += (long long)chunk * per_call;
+        steps_enqueued += chunk;
     }
     ck(cudaGetLastError(), "solve steps");
 }
@@ -704,7 +650,7 @@ void Engine::solve_run_to_end() {
     }
     read_ctrl();
     if (h_ctrl->done) return;
-    const long long total = (long long)solve_max_iter + (solve_double ? 3 : solve_fused ? 2 : 1);
+    const long long total = (long long)solve_max_iter + (solve_fused ? 2 : 1);
     int chunk = 16, inflight = 0, oldest = 0;
     while (true) {
         while (inflight < 2 && steps_enqueued < total) {
@@ -805,7 +751,7 @@ const double* Engine::solve_x() {
         return xs;
     }
     const Ctrl& c = *h_ctrl;  // read by solve_report
-    const int ring = solve_double ? kXRing2 : kXRing;
+    const int ring = kXRing;
     const double* xs = d_xf + (size_t)(c.solx & (ring - 1)) * n;
     if (c.status == BGABP_DIVERGED && c.detail_kind == 1 && n > 0) {
         // the reference stops its x-stage at the pivot node: x(k) below it, x(k-1) from it on
@@ -1208,6 +1154,13 @@ int bgabp_node_precisions(bgabp_engine* h, double* beta) {
 
 double bgabp_sweep_flops(const bgabp_engine* h) { return h->E.sweep_flops(); }
 
+int bgabp_set_damping(bgabp_engine* h, double alpha) {
+    ABI_GUARD(nullptr, 0, {
+        h->E.set_damping(alpha);
+        return BGABP_OK;
+    })
+}
+
 int bgabp_solve(bgabp_engine* h, const double* b, const bgabp_schedule* s, const bgabp_options* opt,
                 bgabp_report* rep, double* x_out, double* history, char* detail, size_t dl) {
     ABI_GUARD(detail, dl, {
@@ -1264,8 +1217,7 @@ int bgabp_solve_device_end(bgabp_engine* h, bgabp_report* rep, double* x_dev, do
 int bgabp_solve_device_steps_timed(bgabp_engine* h, int nsteps, double* hot_ms) {
     ABI_GUARD(nullptr, 0, {
         Engine& E = h->E;
-        // one event pair per launch; a two-iteration launch covers two of the nsteps iterations
-        const int launches = E.solve_double ? (nsteps + 1) / 2 : nsteps;
+        const int launches = nsteps;  // one event pair per launch
         std::vector<cudaEvent_t> ev(2 * (size_t)std::max(launches, 0));
         for (auto& e : ev) ck(cudaEventCreate(&e), "event");
         E.timed_events = &ev;
@@ -1283,7 +1235,7 @@ int bgabp_solve_device_steps_timed(bgabp_engine* h, int nsteps, double* hot_ms) 
             total += ms;
         }
         for (auto& e : ev) cudaEventDestroy(e);
-        E.steps_enqueued += (long long)launches * (E.solve_double ? 2 : 1);
+        E.steps_enqueued += launches;
         *hot_ms = total;
         return BGABP_OK;
     })

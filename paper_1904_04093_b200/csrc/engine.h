@@ -12,7 +12,6 @@
 
 #include "../../include/gabp_b200.h"
 #include "kernels.cuh"
-#include "flood2_kernels.cuh"
 #include "rb_kernels.cuh"
 #include "seq_kernels.cuh"
 #include "seqpipe_kernels.cuh"
@@ -99,17 +98,10 @@ struct Engine {
     // device-resident solve loop
     bool solve_flood = true;
     bool solve_fused = false;
-    bool solve_double = false;
     PeerP peer{};               // sharded solve: peer-memory halos and reduction slots
     bool peer_on = false;
     unsigned long long* d_slots = nullptr;  // [kMaxShards][2][4] reduction words of every shard
-    cudaEvent_t step_ev = nullptr;          // recorded after each p2p step  // fused flood solve, two iterations per launch (flood2_kernels.cuh)
-    int flood2_h = 80;          // tile rows of k_flood2_grid5 (2048^2: 17 x 26 tiles = one wave at 3 per SM)
-    int flood2_st = 3;          // staged rows (cp.async pipeline depth + 1)
-    int flood2_minb = 3;        // resident blocks the uniform variant is compiled for
-    bool flood2_band = false;   // banded variant (k_flood2b_grid5)
-    int flood2_r = 42;          // banded variant: rows per band * 10 + resident blocks
-    void enqueue_double_kernel(bool attr_only = false);
+    cudaEvent_t step_ev = nullptr;          // recorded after each p2p step
     const Levels* solve_levels = nullptr;
     bool solve_rb = false;
     bool solve_seq = false;
@@ -207,6 +199,9 @@ struct Engine {
     void* d_pack = nullptr;
     long long pack_cap = 0;
     void solve_steps(int nsteps);
+    double damping = 0.0;  // flood message damping (bgabp_set_damping); 0 = the reference's update
+    void set_damping(double a);
+    void check_damping(const bgabp_schedule& s) const;
     static constexpr int kChunk = 16;  // solve iterations per captured graph
     bool chunk_graph_eligible() const;
     cudaGraphExec_t chunk_graph(int len);

@@ -105,7 +105,7 @@ int bgabp_shard_peer_slots(bgabp_engine* h, void** slots) {
             E.d_slots = static_cast<unsigned long long*>(E.dalloc(bytes));
             ck(cudaMemsetAsync(E.d_slots, 0, bytes, E.st), "memset");
         }
-        if (!E.d_xf) E.d_xf = static_cast<double*>(E.dalloc(sizeof(double) * kXRing2 * (size_t)std::max(E.n, 1)));
+        if (!E.d_xf) E.d_xf = static_cast<double*>(E.dalloc(sizeof(double) * kXRing * (size_t)std::max(E.n, 1)));
         *slots = E.d_slots;
         return BGABP_OK;
     })
@@ -284,7 +284,7 @@ int bgabp_ipc_close(void* dev_ptr) {
 void* bgabp_shard_msg(bgabp_engine* h, int which) { return (void*)h->E.d_msg[which & 1]; }
 void* bgabp_shard_x(bgabp_engine* h, int which) {  // the slot holding x(which)
     Engine& E = h->E;
-    if (!E.d_xf) E.d_xf = static_cast<double*>(E.dalloc(sizeof(double) * kXRing2 * (size_t)std::max(E.n, 1)));
+    if (!E.d_xf) E.d_xf = static_cast<double*>(E.dalloc(sizeof(double) * kXRing * (size_t)std::max(E.n, 1)));
     return (void*)xslot(E.d_xf, E.n, which);
 }
 

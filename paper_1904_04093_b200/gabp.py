@@ -83,6 +83,7 @@ def lib():
             "bgabp_sweep": (C.c_int, [_vp, _dp, S, _dp, C.c_char_p, C.c_size_t]),
             "bgabp_node_precisions": (C.c_int, [_vp, _dp]),
             "bgabp_sweep_flops": (C.c_double, [_vp]),
+            "bgabp_set_damping": (C.c_int, [_vp, C.c_double]),
             "bgabp_solve": (C.c_int, [_vp, _dp, S, C.POINTER(_Opts), C.POINTER(_Rep), _dp, _dp, C.c_char_p,
                                       C.c_size_t]),
             "bgabp_solve_device_begin": (C.c_int, [_vp, _vp, S, C.POINTER(_Opts)]),
@@ -418,6 +419,11 @@ class GabpEngine:
 
     def sweep_flops(self):
         return lib().bgabp_sweep_flops(self._h)
+
+    def set_damping(self, alpha: float):
+        """Optional message damping of flood sweeps and solves (no reference counterpart):
+        new <- (1 - alpha) new + alpha old per edge; 0 is the reference's update."""
+        _raise(lib().bgabp_set_damping(self._h, float(alpha)), "gabp: damping must lie in [0, 1)")
 
     def solve(self, b, sched: Schedule, opt: GabpOptions = GabpOptions(), x_out=None) -> SolveReport:
         """GabpEngine::solve (gabp.cpp:174-219).  x_out: optional caller buffer (e.g. pinned) for x."""

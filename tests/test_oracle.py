@@ -210,3 +210,21 @@ def test_mg_breakdown_x_restatement_equals_reference_library(orc, ref, fine_diag
     assert ro.solution.tobytes() == rr.solution.tobytes()
     assert eo[0] == er[0] and eo[1].tobytes() == er[1].tobytes() == rr.solution.tobytes()
     assert (np.abs(rr.solution).max() == 0.0) == (pre >= 2 or fine_diag == 2.0)
+
+
+def test_restated_damping_zero_is_the_reference(orc, ref):
+    """Damping (restatement only) at 0 is the reference's update; the reference build has none."""
+    if ref is None:
+        pytest.skip("oracle/_ref not built")
+    A = orc.poisson5(12, 12)
+    b = orc.rng(1).vector(A.n)
+    e = orc.engine(A)
+    e.set_damping(0.0)
+    got = e.solve(b, Schedule.parallel_flood(), tol=1e-8, max_iter=500)
+    want = ref.engine(A).solve(b, Schedule.parallel_flood(), tol=1e-8, max_iter=500)
+    assert got.residual_history.tobytes() == want.residual_history.tobytes()
+    e.set_damping(0.5)
+    damped = e.solve(b, Schedule.parallel_flood(), tol=1e-8, max_iter=500)
+    assert damped.residual_history.tobytes() != want.residual_history.tobytes()
+    with pytest.raises(ValueError):
+        ref.engine(A).set_damping(0.5)
