@@ -80,6 +80,7 @@ typedef struct {
     long long device_bytes;       /* device memory held by the handle */
     int uniform_coefficients;     /* DIA constant-coefficient stencil: coefficients and diagonal are
                                      kernel parameters, not arrays (the solve step reads 32 E + 28 n) */
+    long long sell_slots;         /* CSR layout: slots of the padded SELL solve layout (0 for DIA) */
 } bgabp_info;
 
 typedef struct bgabp_engine bgabp_engine;

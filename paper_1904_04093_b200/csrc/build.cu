@@ -113,6 +113,7 @@ void Engine::build(int n_, const int* ro_, const int* ci_, const double* v_, int
     d_ctrl = static_cast<Ctrl*>(dalloc(sizeof(Ctrl)));
 
     const bool host_build = getenv("BGABP_HOST_BUILD") != nullptr;  // cross-check of the device build
+    use_ucsr_solve = getenv("BGABP_UCSR_SOLVE") != nullptr;         // A/B: the union-CSR solve loop
     if (layout == BGABP_LAYOUT_DIA) {
         S = (int)offs.size();
         std::memset(&dia, 0, sizeof(dia));
@@ -139,9 +140,11 @@ void Engine::build(int n_, const int* ro_, const int* ci_, const double* v_, int
         build_ucsr_host();
         phase("UCSR layout");
     }
+    // the SELL solve layout (general sparsity) pads chunks: its slot count can exceed nslots
+    msg_cap = std::max<long long>(std::max(nslots, sell_slots), 1);
     for (int k = 0; k < 2; ++k) {
-        d_msg[k] = static_cast<double2*>(dalloc(sizeof(double2) * (size_t)std::max<long long>(nslots, 1)));
-        ck(cudaMemsetAsync(d_msg[k], 0, sizeof(double2) * (size_t)std::max<long long>(nslots, 1), st), "memset");
+        d_msg[k] = static_cast<double2*>(dalloc(sizeof(double2) * (size_t)msg_cap));
+        ck(cudaMemsetAsync(d_msg[k], 0, sizeof(double2) * (size_t)msg_cap, st), "memset");
     }
     const size_t vb = sizeof(double) * (size_t)std::max(n, 1);
     d_b = static_cast<double*>(dalloc(vb));
@@ -404,7 +407,7 @@ void Engine::build_ucsr_host() {
     for (int i = 0; i < n; ++i) diag[i] = val[find_pos(i, i)];
     csr2slot.assign(nnz, -1);
     std::vector<uint8_t> flg(U, 0);
-    std::vector<double> uc(U, 0.0);
+    std::vector<double> uc(U, 0.0), urow(U, 0.0);
     std::vector<int> urev(U, -1), undiag(n, 0);
     auto slot = [&](int j, int k) -> long long {  // slot of neighbour k in j's sorted list
         auto b = unbr.begin() + uptr[j], e = unbr.begin() + uptr[j + 1];
@@ -423,6 +426,7 @@ void Engine::build_ucsr_host() {
             flg[si] |= 1;
             flg[sj] |= 2;
             uc[sj] = val[p];
+            urow[si] = val[p];
             csr2slot[p] = si;
         }
     std::memset(&csr, 0, sizeof(csr));
@@ -440,6 +444,7 @@ void Engine::build_ucsr_host() {
     d_ro = const_cast<int*>(csr.ro);
     d_ci = const_cast<int*>(csr.ci);
     d_val = const_cast<double*>(csr.val);
+    build_sell(flg, uc, urow, urev, csr.diag);
 }
 
 

@@ -404,7 +404,8 @@ void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bga
     check_damping(s);
     if (damping != 0.0 && r0_override) throw InvalidArg("gabp: message damping is not supported by sharded solves");
     solve_flood = s.kind == BGABP_SCHED_FLOOD;
-    solve_fused = solve_flood && layout == BGABP_LAYOUT_DIA;
+    // the fused step: DIA stencils, or the SELL layout for general sparsity (not sharded)
+    solve_fused = solve_flood && (layout == BGABP_LAYOUT_DIA || (sell_ready && !r0_override && !use_ucsr_solve));
     solve_levels = solve_flood ? nullptr : &levels_for(s);
     solve_rb = !solve_flood && rb_applicable(s);
     solve_seq = !solve_flood && !solve_rb && seq_applicable(s);
@@ -429,7 +430,7 @@ void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bga
     c.max_iter = o.max_iter;
     ck(cudaMemcpyAsync(d_ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, st), "ctrl");
     for (int k = 0; k < 2; ++k)
-        ck(cudaMemsetAsync(d_msg[k], 0, sizeof(double2) * (size_t)std::max<long long>(nslots, 1), st), "memset");
+        ck(cudaMemsetAsync(d_msg[k], 0, sizeof(double2) * (size_t)std::max<long long>(msg_cap, 1), st), "memset");
     ck(cudaMemsetAsync(d_x, 0, sizeof(double) * std::max(n, 1), st), "memset x");
     if (!solve_fused && !(solve_seq && pipe_fits())) {  // ordered (not pipelined), or union-CSR flood
         if (!d_xord) d_xord = static_cast<double*>(dalloc(sizeof(double) * 2 * (size_t)std::max(n, 1)));
@@ -503,6 +504,12 @@ static void launch_sharded_step(Engine& E, unsigned g, bool dl) {
 }
 
 void Engine::enqueue_fused_kernel() {
+    if (layout != BGABP_LAYOUT_DIA) {  // general sparsity: the SELL step
+        if (timed_events) ck(cudaEventRecord((*timed_events)[2 * timed_index], st), "event");
+        launch_sell_step(solve_stop == BGABP_STOP_MESSAGE_DELTA);
+        if (timed_events) ck(cudaEventRecord((*timed_events)[2 * timed_index + 1], st), "event");
+        return;
+    }
     {
         const bool dl = solve_stop == BGABP_STOP_MESSAGE_DELTA;
         const unsigned g = nblk(std::max(dia.j1 - dia.j0, 1));
@@ -1041,6 +1048,7 @@ int bgabp_get_info(const bgabp_engine* h, bgabp_info* info) {
     info->uniform_coefficients = (E.layout == BGABP_LAYOUT_DIA && E.dia.uniform) ? 1 : 0;
     info->bytes_per_residual = 8.0 * (double)E.nnz + 16.0 * E.n;
     info->device_bytes = E.device_bytes;
+    info->sell_slots = E.sell_slots;
     return BGABP_OK;
 }
 

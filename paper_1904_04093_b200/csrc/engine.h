@@ -15,6 +15,7 @@
 #include "rb_kernels.cuh"
 #include "seq_kernels.cuh"
 #include "seqpipe_kernels.cuh"
+#include "sell_kernels.cuh"
 
 namespace bgabp {
 
@@ -59,6 +60,7 @@ struct Engine {
     std::vector<int> uptr, unbr;  // union neighbour lists
     int layout = BGABP_LAYOUT_DIA, S = 0;
     long long nslots = 0;
+    long long msg_cap = 0;  // elements of each d_msg buffer (>= nslots)
     DiaP dia{};
     CsrP csr{};
     std::vector<long long> csr2slot;
@@ -124,6 +126,14 @@ struct Engine {
     void build_dia_device(const int* ro, const int* ci, const double* v);
     void build_dia_host();
     void build_ucsr_host();
+    // general sparsity: SELL layout of the union graph for the fused solve step (sell.cu)
+    SellP sell[2]{};  // [0] chunks of <= 8 slot rows (register-cached kernel), [1] wider chunks
+    bool sell_ready = false;
+    bool use_ucsr_solve = false;  // BGABP_UCSR_SOLVE=1: the three-launch union-CSR solve loop instead
+    long long sell_slots = 0;
+    void build_sell(const std::vector<uint8_t>& flg, const std::vector<double>& uc, const std::vector<double>& urow,
+                    const std::vector<int>& urev, const double* d_diag);
+    void launch_sell_step(bool dl);
     void host_graph(const int* ro, const int* ci, const double* v);
     void upload_host(void* dst, const void* src, size_t bytes);
     long long find_pos(int r, int c) const;

@@ -1,0 +1,188 @@
+// Fused flood solve step for general sparsity (gabp.cpp:102-163 + 187-218 on matrices that are
+// not a <= 8-offset stencil): the SELL layout of the union message graph.
+//
+// Layout (built on the host from the union-CSR lists, Engine::build_sell):
+//   * nodes are grouped into chunks of 32 (one warp, one node per lane); inside windows of 1024
+//     nodes they are stably sorted by degree first, so a chunk's lanes have similar degrees;
+//   * chunk c holds cwid[c] slot rows; slot s of the node on lane l sits at (crow[c] + s) * 32 + l,
+//     so a warp reading slot s of its 32 nodes touches 32 consecutive elements: every per-edge
+//     array (messages, coefficients, indices) is read fully coalesced, the union-CSR layout's
+//     per-thread strided reads are gone;
+//   * a node's slots follow the sorted union of its row and column neighbours (CSR column
+//     order), so the per-lane sums run in the reference's order and stay bit-identical;
+//   * rev[p]: bit 31 = in-edge (A_jk structural: a message k -> j arrives in slot p and row j has
+//     an entry), bit 30 = out-edge (A_kj structural: j sends to k), bits 0..29 = the slot of j in
+//     k's list, where j's message to k is stored.  Padding slots are 0.
+//   * the messages stay {lambda~, m} double2 per receiving slot (one 16-byte access per edge).
+// Per edge one step reads 16 B of message, 8 B of coefficient (+8 B of row coefficient when A is
+// not bit-symmetric), 8 B of index (rev + nbr), gathers x(t-2)_k for the residual (L2-resident
+// for local graphs), and writes 16 B to the receiver's slot (the one scattered access).
+#pragma once
+
+#include "kernels.cuh"
+
+namespace bgabp {
+
+constexpr unsigned kSellIn = 1u << 31, kSellOut = 1u << 30, kSellSlot = (1u << 30) - 1;
+
+struct SellP {
+    int n;
+    const int* chunks;      // chunk ids of the bucket this launch covers
+    int nchunks;            // entries of `chunks`
+    const long long* crow;  // [C] first slot row of chunk c
+    const int* cwid;        // [C] slot rows of chunk c
+    const int* cnode;       // [32 C] node on lane l of chunk c (-1: empty lane)
+    const unsigned* rev;    // [slots] flags | target slot
+    const int* nbr;         // [slots] neighbour k (0x7fffffff in padding)
+    const double* cout;     // [slots] A_kj: the coefficient of j's message to k
+    const double* rowv;     // [slots] A_jk: row j of A (the residual); == cout when A is symmetric
+    const double* diag;     // [n]
+    double damp, undamp;    // optional message damping (bgabp_set_damping)
+};
+
+// One warp = one chunk of 32 nodes.  W > 0: every chunk of the bucket has at most W slot rows
+// and all per-slot operands stay in registers between the aggregation and the message stage;
+// W == 0: any width, the message stage re-reads its operands (L1/L2 hits).
+template <int W, bool DELTA, bool SYM, bool DAMP>
+static __global__ void __launch_bounds__(256, W > 0 ? 2 : 4) k_flood_solve_sell(SellP P, const double* __restrict__ b,
+                                                                    double2* m0, double2* m1, double* x0,
+                                                                    double* x1, Ctrl* ctrl,
+                                                                    unsigned long long* spread) {
+    if (ld_ctrl(&ctrl->done)) return;
+    const int t = ld_ctrl(&ctrl->step);
+    const double2* __restrict__ min = (t & 1) ? m0 : m1;
+    double2* __restrict__ mout = (t & 1) ? m1 : m0;
+    double* __restrict__ xw = ((t - 1) & 1) ? x1 : x0;        // x(t-1)
+    const double* __restrict__ xr = ((t - 2) & 1) ? x1 : x0;  // x(t-2)
+    const bool res = t >= 3;
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    double rabs = 0.0, dmax = 0.0;
+    if (w < P.nchunks) {
+        const int c = __ldg(P.chunks + w);
+        const int wid = __ldg(P.cwid + c);
+        const int j = __ldg(P.cnode + 32 * c + lane);
+        const long long base = __ldg(P.crow + c) * 32 + lane;
+        const int n = P.n;
+        if (j >= 0) {
+            const double dj = __ldg(P.diag + j), bj = __ldg(b + j);
+            const double xj = res ? __ldg(xr + j) : 0.0;
+            double sig = 0.0, acc = bj, r = bj;
+            bool dsig = false, dres = false;
+            // the diagonal enters both sums at its column position (before the first k > j)
+            auto diag_before = [&](int k) {
+                if (!dsig && k > j) {
+                    sig = dadd(sig, dj);
+                    dsig = true;
+                }
+                if (res && !dres && k > j) {
+                    r = dsub(r, dmul(dj, xj));
+                    dres = true;
+                }
+            };
+            if constexpr (W > 0) {
+                unsigned f[W];
+                int kk[W];
+                double2 v[W];
+                double cs[W], rv[W], xk[W];
+#pragma unroll
+                for (int s = 0; s < W; ++s) {  // every load issued up front (padding slots are valid)
+                    const bool on = s < wid;
+                    const long long p = base + 32ll * s;
+                    f[s] = on ? __ldg(P.rev + p) : 0u;
+                    kk[s] = on ? __ldg(P.nbr + p) : 0x7fffffff;
+                    v[s] = on ? __ldg(min + p) : make_double2(0.0, 0.0);
+                    cs[s] = on ? __ldg(P.cout + p) : 0.0;
+                    rv[s] = (!SYM && on) ? __ldg(P.rowv + p) : 0.0;
+                }
+#pragma unroll
+                for (int s = 0; s < W; ++s) xk[s] = (res && (f[s] & kSellIn)) ? __ldg(xr + kk[s]) : 0.0;
+#pragma unroll
+                for (int s = 0; s < W; ++s) {
+                    if (s >= wid) break;
+                    diag_before(kk[s]);
+                    if (f[s] & kSellIn) {
+                        acc = dadd(acc, v[s].y);
+                        if (f[s] & kSellOut) sig = dadd(sig, dmul(v[s].x, cs[s]));
+                        if (res) r = dsub(r, dmul(SYM ? cs[s] : rv[s], xk[s]));
+                    }
+                }
+                diag_before(0x7fffffff);
+                if (t >= 2) {  // x-stage of sweep t-1
+                    xw[j] = ddiv(acc, sig);
+                    if (fabs(sig) < kPivotFloor) atomicMin(&ctrl->npiv[(t - 1) & 3], (unsigned long long)j);
+                }
+                if (res) rabs = nan_skip_abs(r);
+#pragma unroll
+                for (int s = 0; s < W; ++s) {
+                    if (s >= wid) break;
+                    if (!(f[s] & kSellOut)) continue;
+                    const double2 vi = (f[s] & kSellIn) ? v[s] : make_double2(0.0, 0.0);
+                    const double den = dsub(sig, dmul(vi.x, cs[s]));
+                    if (fabs(den) < kPivotFloor)
+                        atomicMin(&ctrl->epiv[t & 3], ((unsigned long long)j << 32) | (unsigned)kk[s]);
+                    double nl = ddiv(-cs[s], den);
+                    double nm = dmul(nl, dsub(acc, vi.y));
+                    const unsigned tgt = f[s] & kSellSlot;
+                    if (DELTA || DAMP) {
+                        const double2 o = min[tgt];
+                        if (DAMP) {
+                            const double2 q = damp_msg(nl, nm, o, P.damp, P.undamp);
+                            nl = q.x;
+                            nm = q.y;
+                        }
+                        if (DELTA) dmax = fmax(dmax, fmax(nan_skip_abs(dsub(nl, o.x)), nan_skip_abs(dsub(nm, o.y))));
+                    }
+                    mout[tgt] = make_double2(nl, nm);
+                }
+            } else {
+                for (int s = 0; s < wid; ++s) {
+                    const long long p = base + 32ll * s;
+                    const unsigned f = __ldg(P.rev + p);
+                    const int k = __ldg(P.nbr + p);
+                    diag_before(k);
+                    if (f & kSellIn) {
+                        const double2 v = __ldg(min + p);
+                        const double cs = __ldg(P.cout + p);
+                        acc = dadd(acc, v.y);
+                        if (f & kSellOut) sig = dadd(sig, dmul(v.x, cs));
+                        if (res) r = dsub(r, dmul(SYM ? cs : __ldg(P.rowv + p), __ldg(xr + k)));
+                    }
+                }
+                diag_before(0x7fffffff);
+                if (t >= 2) {
+                    xw[j] = ddiv(acc, sig);
+                    if (fabs(sig) < kPivotFloor) atomicMin(&ctrl->npiv[(t - 1) & 3], (unsigned long long)j);
+                }
+                if (res) rabs = nan_skip_abs(r);
+                for (int s = 0; s < wid; ++s) {
+                    const long long p = base + 32ll * s;
+                    const unsigned f = __ldg(P.rev + p);
+                    if (!(f & kSellOut)) continue;
+                    const double2 vi = (f & kSellIn) ? __ldg(min + p) : make_double2(0.0, 0.0);
+                    const double cs = __ldg(P.cout + p);
+                    const double den = dsub(sig, dmul(vi.x, cs));
+                    if (fabs(den) < kPivotFloor)
+                        atomicMin(&ctrl->epiv[t & 3], ((unsigned long long)j << 32) | (unsigned)__ldg(P.nbr + p));
+                    double nl = ddiv(-cs, den);
+                    double nm = dmul(nl, dsub(acc, vi.y));
+                    const unsigned tgt = f & kSellSlot;
+                    if (DELTA || DAMP) {
+                        const double2 o = min[tgt];
+                        if (DAMP) {
+                            const double2 q = damp_msg(nl, nm, o, P.damp, P.undamp);
+                            nl = q.x;
+                            nm = q.y;
+                        }
+                        if (DELTA) dmax = fmax(dmax, fmax(nan_skip_abs(dsub(nl, o.x)), nan_skip_abs(dsub(nm, o.y))));
+                    }
+                    mout[tgt] = make_double2(nl, nm);
+                }
+            }
+        }
+        (void)n;
+    }
+    if (res) warp_max_spread(spread + (size_t)((t - 2) & 3) * kSpread, rabs);
+    if (DELTA) warp_max_spread(spread + (size_t)(4 + (t & 3)) * kSpread, dmax);
+}
+
+}  // namespace bgabp

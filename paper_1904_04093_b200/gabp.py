@@ -47,7 +47,7 @@ class _Info(C.Structure):
     _fields_ = [("n", C.c_int), ("nnz", C.c_longlong), ("num_edges", C.c_longlong), ("layout", C.c_int),
                 ("num_slots", C.c_int), ("symmetric_values", C.c_int), ("bytes_per_sweep", C.c_double),
                 ("bytes_per_residual", C.c_double), ("device_bytes", C.c_longlong),
-                ("uniform_coefficients", C.c_int)]
+                ("uniform_coefficients", C.c_int), ("sell_slots", C.c_longlong)]
 
 
 class _Cycle(C.Structure):
