@@ -96,6 +96,8 @@ double residual_inf_norm(const SparseMatrix& A, const Vector& x, const Vector& b
     if (static_cast<int>(x.size()) != A.n || static_cast<int>(b.size()) != A.n)
         throw std::invalid_argument("residual_inf_norm: dimension mismatch");
     double worst = 0.0;
+    // (std::max never takes a NaN into `worst`, so the maximum is order-free: threads on large n)
+#pragma omp parallel for schedule(static, 4096) reduction(max : worst) if (A.n >= (1 << 16))
     for (int i = 0; i < A.n; ++i) {
         double acc = b[i];
         for (int p = A.row_offsets[i]; p < A.row_offsets[i + 1]; ++p)
@@ -557,8 +559,56 @@ private:
     }
 
     // synchronous sweep from a snapshot, x from the new messages (gabp.cpp:102-163)
+    // Large systems: the same sweep evaluated by OpenMP threads.  Every node's arithmetic is the
+    // serial one on the same snapshot (a parallel flood evaluation is bit-identical
+    // to the serial one), the delta is a max of non-NaN values (order-free); a breakdown restores
+    // the state and reruns the serial sweep, which reproduces the reference's partial updates.
+    static constexpr int kParallelMin = 1 << 16;
+    static void par_copy(std::vector<double>& dst, const std::vector<double>& src) {
+        dst.resize(src.size());
+        const long nn = static_cast<long>(src.size());
+#pragma omp parallel for schedule(static)
+        for (long q = 0; q < nn; q += 65536)
+            std::copy(src.begin() + q, src.begin() + std::min(nn, q + 65536), dst.begin() + q);
+    }
+    bool flood_parallel(const Vector& b, MessageState& st, Vector& x, double* max_delta) const {
+        MessageState& prev = snap_;
+        par_copy(prev.lambda_tilde, st.lambda_tilde);
+        par_copy(prev.m, st.m);
+        int fail = 0;
+        double delta = 0.0;
+#pragma omp parallel for schedule(static, 4096) reduction(max : delta) reduction(| : fail)
+        for (int j = 0; j < A_.n; ++j) {
+            double sig, acc, d = 0.0;
+            aggregate(j, b[j], prev, sig, acc);
+            for (const Out& o : out_[j])
+                if (!emit(j, o, sig, acc, prev, st, nullptr, max_delta ? &d : nullptr, damping_ != 0.0)) fail = 1;
+            delta = std::max(delta, d);
+        }
+        Vector& xt = xtmp_;
+        xt.resize(A_.n);
+        if (!fail) {
+#pragma omp parallel for schedule(static, 4096) reduction(| : fail)
+            for (int i = 0; i < A_.n; ++i) {
+                double sig, acc;
+                aggregate(i, b[i], st, sig, acc);
+                if (std::abs(sig) < kPivotFloor) fail = 1;
+                else xt[i] = acc / sig;
+            }
+        }
+        if (fail) {
+            par_copy(st.lambda_tilde, prev.lambda_tilde);
+            par_copy(st.m, prev.m);
+            return false;
+        }
+        par_copy(x, xt);
+        if (max_delta) *max_delta = delta;
+        return true;
+    }
+
     bool flood(const Vector& b, MessageState& st, Vector& x, std::string* err,
                double* max_delta) const {
+        if (A_.n >= kParallelMin && flood_parallel(b, st, x, max_delta)) return true;
         const MessageState prev = st;
         double delta = 0.0;
         for (int j = 0; j < A_.n; ++j) {
@@ -585,6 +635,8 @@ private:
     std::vector<int> diag_;
     long num_edges_ = 0;
     double damping_ = 0.0, undamp_ = 1.0;
+    mutable MessageState snap_;  // flood_parallel scratch (the snapshot) and x of the sweep
+    mutable Vector xtmp_;
 
 public:
     // Optional message damping of the flood sweep (BASELINE.json north_star; the reference has

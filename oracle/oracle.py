@@ -167,6 +167,7 @@ class Oracle:
                                        C.c_double, _dp, _dp, _ip, _ip, _dp, _ip, C.c_char_p, C.c_size_t]),
             "orc_mg_cycle_flops": (C.c_double, [vp, C.c_int, C.c_int]),
             "orc_set_damping": (C.c_int, [vp, C.c_double]),
+            "orc_set_threads": (C.c_int, [C.c_int]),
             "orc_flop_table": (C.c_double, [C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_size_t]),
             "orc_mg_restrict": (None, [_dp, C.c_int, _dp]),
             "orc_mg_prolong": (None, [_dp, C.c_int, _dp]),
@@ -328,6 +329,10 @@ class Oracle:
         if rc != 1:
             raise RuntimeError(err.value.decode())
         return x
+
+    def set_threads(self, k):
+        """Threads of the restatement's parallel flood evaluation (bit-identical to serial)."""
+        return self.lib.orc_set_threads(int(k))
 
     def flop_table(self, stencil, smoother, sweeps):
         """analysis.cpp:135-154; ValueError on the reference's std::invalid_argument."""

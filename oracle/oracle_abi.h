@@ -69,6 +69,7 @@ int orc_sweep(const orc_engine* e, const double* b, orc_sched s, double* lam, do
 int orc_solve(const orc_engine* e, const double* b, orc_sched s, double tol, int max_iter,
               int stop_kind, double divergence_factor, double* x_out, double* history,
               int* iterations, int* status, double* flops, char* detail, size_t detaillen);
+int orc_set_threads(int k); /* OpenMP threads of the restatement (1 in the reference build) */
 int orc_set_damping(orc_engine* e, double alpha); /* restatement only (no reference damping) */
 int orc_precompute_lambda(const orc_engine* e, orc_sched s, double tol, int max_iter,
                           double* lam_out, double* sigma_out, int* converged, int* iterations);

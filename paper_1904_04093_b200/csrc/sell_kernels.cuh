@@ -25,6 +25,33 @@ namespace bgabp {
 
 constexpr unsigned kSellIn = 1u << 31, kSellOut = 1u << 30, kSellSlot = (1u << 30) - 1;
 
+// L2 cache policy "evict last" for operands a kernel reads twice, and read-only loads carrying it
+__device__ __forceinline__ unsigned long long l2_evict_last_policy() {
+    unsigned long long pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ unsigned ldg_hint(const unsigned* p, unsigned long long pol) {
+    unsigned v;
+    asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ int ldg_hint(const int* p, unsigned long long pol) {
+    int v;
+    asm("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ double ldg_hint(const double* p, unsigned long long pol) {
+    double v;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ double2 ldg_hint(const double2* p, unsigned long long pol) {
+    double2 v;
+    asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+
 struct SellP {
     int n;
     const int* chunks;      // chunk ids of the bucket this launch covers
@@ -42,9 +69,9 @@ struct SellP {
 
 // One warp = one chunk of 32 nodes.  W > 0: every chunk of the bucket has at most W slot rows
 // and all per-slot operands stay in registers between the aggregation and the message stage;
-// W == 0: any width, the message stage re-reads its operands (L1/L2 hits).
+// W == 0: any width, groups of 8 slots, the message stage re-reads its operands (L2 hits).
 template <int W, bool DELTA, bool SYM, bool DAMP>
-static __global__ void __launch_bounds__(256, W > 0 ? 2 : 4) k_flood_solve_sell(SellP P, const double* __restrict__ b,
+static __global__ void __launch_bounds__(256, 2) k_flood_solve_sell(SellP P, const double* __restrict__ b,
                                                                     double2* m0, double2* m1, double* x0,
                                                                     double* x1, Ctrl* ctrl,
                                                                     unsigned long long* spread) {
@@ -135,17 +162,36 @@ static __global__ void __launch_bounds__(256, W > 0 ? 2 : 4) k_flood_solve_sell(
                     mout[tgt] = make_double2(nl, nm);
                 }
             } else {
-                for (int s = 0; s < wid; ++s) {
-                    const long long p = base + 32ll * s;
-                    const unsigned f = __ldg(P.rev + p);
-                    const int k = __ldg(P.nbr + p);
-                    diag_before(k);
-                    if (f & kSellIn) {
-                        const double2 v = __ldg(min + p);
-                        const double cs = __ldg(P.cout + p);
-                        acc = dadd(acc, v.y);
-                        if (f & kSellOut) sig = dadd(sig, dmul(v.x, cs));
-                        if (res) r = dsub(r, dmul(SYM ? cs : __ldg(P.rowv + p), __ldg(xr + k)));
+                // any width: slots in groups of 8, every group's loads issued together; the
+                // message stage reloads its operands (pass-1 loads carry an L2 evict-last policy,
+                // so the reloads of a chunk normally hit L2)
+                const unsigned long long pol = l2_evict_last_policy();
+                for (int g0 = 0; g0 < wid; g0 += 8) {
+                    unsigned f[8];
+                    int kk[8];
+                    double2 v[8];
+                    double cs[8], rv[8], xk[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const bool on = g0 + q < wid;
+                        const long long p = base + 32ll * (g0 + q);
+                        f[q] = on ? ldg_hint(P.rev + p, pol) : 0u;
+                        kk[q] = on ? ldg_hint(P.nbr + p, pol) : 0x7fffffff;
+                        v[q] = on ? ldg_hint(min + p, pol) : make_double2(0.0, 0.0);
+                        cs[q] = on ? ldg_hint(P.cout + p, pol) : 0.0;
+                        rv[q] = (!SYM && on) ? __ldg(P.rowv + p) : 0.0;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) xk[q] = (res && (f[q] & kSellIn)) ? __ldg(xr + kk[q]) : 0.0;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        if (g0 + q >= wid) break;
+                        diag_before(kk[q]);
+                        if (f[q] & kSellIn) {
+                            acc = dadd(acc, v[q].y);
+                            if (f[q] & kSellOut) sig = dadd(sig, dmul(v[q].x, cs[q]));
+                            if (res) r = dsub(r, dmul(SYM ? cs[q] : rv[q], xk[q]));
+                        }
                     }
                 }
                 diag_before(0x7fffffff);
@@ -154,28 +200,42 @@ static __global__ void __launch_bounds__(256, W > 0 ? 2 : 4) k_flood_solve_sell(
                     if (fabs(sig) < kPivotFloor) atomicMin(&ctrl->npiv[(t - 1) & 3], (unsigned long long)j);
                 }
                 if (res) rabs = nan_skip_abs(r);
-                for (int s = 0; s < wid; ++s) {
-                    const long long p = base + 32ll * s;
-                    const unsigned f = __ldg(P.rev + p);
-                    if (!(f & kSellOut)) continue;
-                    const double2 vi = (f & kSellIn) ? __ldg(min + p) : make_double2(0.0, 0.0);
-                    const double cs = __ldg(P.cout + p);
-                    const double den = dsub(sig, dmul(vi.x, cs));
-                    if (fabs(den) < kPivotFloor)
-                        atomicMin(&ctrl->epiv[t & 3], ((unsigned long long)j << 32) | (unsigned)__ldg(P.nbr + p));
-                    double nl = ddiv(-cs, den);
-                    double nm = dmul(nl, dsub(acc, vi.y));
-                    const unsigned tgt = f & kSellSlot;
-                    if (DELTA || DAMP) {
-                        const double2 o = min[tgt];
-                        if (DAMP) {
-                            const double2 q = damp_msg(nl, nm, o, P.damp, P.undamp);
-                            nl = q.x;
-                            nm = q.y;
-                        }
-                        if (DELTA) dmax = fmax(dmax, fmax(nan_skip_abs(dsub(nl, o.x)), nan_skip_abs(dsub(nm, o.y))));
+                for (int g0 = 0; g0 < wid; g0 += 8) {
+                    unsigned f[8];
+                    double2 v[8];
+                    double cs[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const bool on = g0 + q < wid;
+                        const long long p = base + 32ll * (g0 + q);
+                        f[q] = on ? __ldg(P.rev + p) : 0u;
+                        v[q] = on ? __ldg(min + p) : make_double2(0.0, 0.0);
+                        cs[q] = on ? __ldg(P.cout + p) : 0.0;
                     }
-                    mout[tgt] = make_double2(nl, nm);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        if (g0 + q >= wid) break;
+                        if (!(f[q] & kSellOut)) continue;
+                        const double2 vi = (f[q] & kSellIn) ? v[q] : make_double2(0.0, 0.0);
+                        const double den = dsub(sig, dmul(vi.x, cs[q]));
+                        if (fabs(den) < kPivotFloor)
+                            atomicMin(&ctrl->epiv[t & 3],
+                                      ((unsigned long long)j << 32) | (unsigned)__ldg(P.nbr + base + 32ll * (g0 + q)));
+                        double nl = ddiv(-cs[q], den);
+                        double nm = dmul(nl, dsub(acc, vi.y));
+                        const unsigned tgt = f[q] & kSellSlot;
+                        if (DELTA || DAMP) {
+                            const double2 o = min[tgt];
+                            if (DAMP) {
+                                const double2 w2 = damp_msg(nl, nm, o, P.damp, P.undamp);
+                                nl = w2.x;
+                                nm = w2.y;
+                            }
+                            if (DELTA)
+                                dmax = fmax(dmax, fmax(nan_skip_abs(dsub(nl, o.x)), nan_skip_abs(dsub(nm, o.y))));
+                        }
+                        mout[tgt] = make_double2(nl, nm);
+                    }
                 }
             }
         }
