@@ -166,6 +166,10 @@ int bgabp_flood_sweeps_device(bgabp_engine* e, const double* b_dev, int nsweeps)
  * nodes into the neighbour's ghost range.  Every call is stream-ordered on bgabp_stream(e); r0 is
  * the global ||b||_inf.  End with bgabp_solve_device_end.  Pointers are device pointers. */
 int bgabp_shard_set_range(bgabp_engine* e, int own_lo, int own_hi, int gofs);
+/* DIA neighbour offsets of the handle (ascending; returns the slot count, -1 for the CSR layout).
+ * Shards exchange halos slot by slot, so neighbouring shards must hold identical offsets
+ * (shard.py checks this before wiring peers or starting a sharded solve). */
+int bgabp_dia_offsets(const bgabp_engine* e, int* off, int cap);
 int bgabp_shard_solve_begin(bgabp_engine* e, const double* b_dev, const bgabp_options* opt, double r0);
 int bgabp_shard_step_compute(bgabp_engine* e);
 void* bgabp_shard_reduce_buffer(bgabp_engine* e);
@@ -329,6 +333,10 @@ const int* bgabp_problem_col_indices(const bgabp_problem* p);
 const double* bgabp_problem_values(const bgabp_problem* p);
 const double* bgabp_problem_rhs(const bgabp_problem* p);   /* b (n) */
 const double* bgabp_problem_exact(const bgabp_problem* p); /* manufactured solution or NULL */
+
+/* Give the idle device blocks of the process-wide block cache back to the driver (engine
+ * allocations are cached for reuse by later handles; an allocation failure trims automatically). */
+void bgabp_trim_cache(void);
 
 /* library build tag (sm arch, git-independent) */
 const char* bgabp_version(void);

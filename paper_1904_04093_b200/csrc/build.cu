@@ -103,6 +103,7 @@ void Engine::build(int n_, const int* ro_, const int* ci_, const double* v_, int
     layout = (want_layout == BGABP_LAYOUT_CSR || !dia_ok) ? BGABP_LAYOUT_CSR : BGABP_LAYOUT_DIA;
     phase("validate + offsets");
 
+    ck(cudaGetDevice(&device), "device");
     if (shared_stream) {
         st = shared_stream;
         own_stream = false;

@@ -49,9 +49,23 @@ void Engine::drop_graphs() {
 }
 
 Engine::~Engine() {
+    DeviceGuard g(device);  // the engine's device, not whichever one is current
     if (st) cudaStreamSynchronize(st);
     drop_graphs();
-    if (!allocs.empty()) cudaDeviceSynchronize();  // no kernel (a peer shard's included) still uses them
+    if (!allocs.empty()) {
+        // no kernel still uses the blocks: this device's, and a peer shard's on another device
+        // (peers store into these buffers)
+        cudaDeviceSynchronize();
+        if (peer_on) {
+            int nd = 0;
+            cudaGetDeviceCount(&nd);
+            for (int d = 0; d < nd; ++d)
+                if (d != device) {
+                    DeviceGuard gd(d);
+                    cudaDeviceSynchronize();
+                }
+        }
+    }
     for (void* p : allocs) release_block(p);
     if (h_ctrl) cudaFreeHost(h_ctrl);
     if (h_poll) cudaFreeHost(h_poll);

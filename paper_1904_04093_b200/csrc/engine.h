@@ -27,6 +27,21 @@ struct CudaError : std::runtime_error {
 };
 
 void put_err(char* err, size_t len, const std::string& s);
+void trim_block_cache();  // idle cached device blocks back to the driver (memory.cu)
+
+// makes `dev` current for its lifetime (a handle's work runs on the device it was built on)
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (dev < 0) return;
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+        else prev = -1;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
 void release_block(void* p);  // engine device blocks back to the cache (memory.cu)
 struct Engine;
 void p2p_forget(Engine* e);  // drop captured multi-shard graphs that use this engine
@@ -66,6 +81,8 @@ struct Engine {
     std::vector<long long> csr2slot;
 
     // device state
+    int device = -1;  // the device the handle was built on (build())
+    long long peer_gen = 0;  // bumped when shard range / peers change (captured multi-shard graphs)
     cudaStream_t st = nullptr;
     bool own_stream = true;
     Ctrl* d_ctrl = nullptr;

@@ -38,7 +38,26 @@ BlockCache& block_cache() {
 size_t round_block(size_t b) {
     return b < BlockCache::kMin ? b : (b + BlockCache::kGran - 1) / BlockCache::kGran * BlockCache::kGran;
 }
+// free every idle block of device `dev` (-1: all devices); caller holds C.mu
+void trim_locked(BlockCache& C, int dev) {
+    for (auto it = C.free_blocks.begin(); it != C.free_blocks.end();) {
+        if (dev >= 0 && it->first.first != dev) {
+            ++it;
+            continue;
+        }
+        cudaFree(it->second);
+        C.held -= it->first.second;
+        it = C.free_blocks.erase(it);
+    }
+}
 }  // namespace
+
+// idle cached blocks back to the driver (e.g. before another library allocates)
+void trim_block_cache() {
+    BlockCache& C = block_cache();
+    std::lock_guard<std::mutex> lock(C.mu);
+    trim_locked(C, -1);
+}
 
 void* Engine::dalloc(size_t bytes) {
     void* p = nullptr;
@@ -54,11 +73,21 @@ void* Engine::dalloc(size_t bytes) {
             p = it->second;
             C.free_blocks.erase(it);
             C.held -= rb;
-        } else {
+        } else if (cudaMalloc(&p, rb) != cudaSuccess) {
+            // out of memory with idle cached blocks of other sizes: give them back, retry once
+            cudaGetLastError();
+            trim_locked(C, dev);
             ck(cudaMalloc(&p, rb), "cudaMalloc");
         }
         C.sizes[p] = {dev, rb};
-    } else {
+    } else if (cudaMalloc(&p, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        int dev = 0;
+        ck(cudaGetDevice(&dev), "device");
+        {
+            std::lock_guard<std::mutex> lock(C.mu);
+            trim_locked(C, dev);
+        }
         ck(cudaMalloc(&p, bytes), "cudaMalloc");
     }
     allocs.push_back(p);
@@ -89,6 +118,7 @@ void Engine::dfree(void* p) {
     auto it = std::find(allocs.begin(), allocs.end(), p);
     if (it == allocs.end()) return;
     allocs.erase(it);
+    DeviceGuard g(device);
     ck(cudaDeviceSynchronize(), "sync");  // the block may be handed out again at once (as cudaFree)
     release_block(p);
 }
@@ -140,9 +170,10 @@ static bool is_pinned(const void* p) {
     return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
-// Host -> device on `st`.  Pinned sources and small copies go straight to the DMA engine; large
-// pageable ones through the stager: parallel host copies into one pinned chunk overlapped with
-// the DMA of the other.  On return the source may be reused.
+// Host -> device on `st`.  Pinned sources and small copies go straight to the DMA engine (an
+// asynchronous copy: the source must stay valid until `st` is synchronised -- every caller does
+// so before returning); large pageable ones through the stager: parallel host copies into one
+// pinned chunk overlapped with the DMA of the other, after which the source may be reused.
 void host_to_device(void* dst, const void* src, size_t bytes, cudaStream_t st) {
     if (bytes == 0) return;
     if (bytes <= (size_t(1) << 20) || is_pinned(src)) {

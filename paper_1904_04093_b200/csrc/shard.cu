@@ -14,9 +14,21 @@ namespace bgabp {
 
 // captured multi-shard peer-memory iterations (bgabp_shard_p2p_steps), dropped with any of their
 // engines or when one of them reallocates a captured buffer
+// What a captured iteration bakes in per shard: its buffers (history generation), its node range
+// and peer pointers (peer generation), and the solve's stop rule and right-hand side.
+struct P2PKey {
+    long long hist_gen, peer_gen;
+    int stop;
+    const double* b;
+    bool operator==(const P2PKey& o) const {
+        return hist_gen == o.hist_gen && peer_gen == o.peer_gen && stop == o.stop && b == o.b;
+    }
+};
+static P2PKey p2p_key(const Engine& E) { return {E.hist_gen, E.peer_gen, E.solve_stop, E.solve_b}; }
+
 struct P2PGraph {
     std::vector<Engine*> engines;
-    std::vector<long long> gens;
+    std::vector<P2PKey> gens;
     cudaGraphExec_t exec = nullptr;
     std::vector<cudaEvent_t> join;
     cudaEvent_t fork = nullptr;
@@ -57,6 +69,8 @@ int bgabp_shard_set_range(bgabp_engine* h, int own_lo, int own_hi, int gofs) {
         E.dia.j0 = own_lo;
         E.dia.j1 = own_hi;
         E.dia.gofs = gofs;
+        ++E.peer_gen;  // captured multi-shard iterations hold the old range
+        p2p_forget(&E);
         if (!E.d_red4) E.d_red4 = static_cast<unsigned long long*>(E.dalloc(sizeof(unsigned long long) * 4));
         if (!E.d_pack) {
             E.pack_cap = 0;
@@ -120,6 +134,8 @@ int bgabp_shard_set_peers(bgabp_engine* h, int nranks, int rank, void* const* lo
             throw InvalidArg("shard: 1 <= nranks <= 8 and 0 <= rank < nranks");
         if (E.dia.j0 == 0 && E.dia.j1 == E.n && nranks > 1 && !E.d_red4)
             throw InvalidArg("shard: call set_range first");
+        ++E.peer_gen;  // captured multi-shard iterations hold the old peer pointers
+        p2p_forget(&E);
         PeerP& Q = E.peer;
         std::memset(&Q, 0, sizeof Q);
         for (int b2 = 0; b2 < 2; ++b2) {  // lower/upper = {msg0, msg1, x0, x1} of the neighbour (or null)
@@ -208,14 +224,14 @@ int bgabp_shard_p2p_steps(bgabp_engine* const* shards, int count, int nsteps, in
                 if (c.engines.size() != (size_t)count) continue;
                 bool same = true;
                 for (int k = 0; k < count && same; ++k)
-                    same = c.engines[k] == &shards[k]->E && c.gens[k] == shards[k]->E.hist_gen;
+                    same = c.engines[k] == &shards[k]->E && c.gens[k] == p2p_key(shards[k]->E);
                 if (same) g = &c;
             }
             if (!g) {
                 P2PGraph c;
                 for (int k = 0; k < count; ++k) {
                     c.engines.push_back(&shards[k]->E);
-                    c.gens.push_back(shards[k]->E.hist_gen);
+                    c.gens.push_back(p2p_key(shards[k]->E));
                 }
                 ck(cudaEventCreateWithFlags(&c.fork, cudaEventDisableTiming), "event");
                 c.join.resize(count);
@@ -280,6 +296,15 @@ int bgabp_ipc_close(void* dev_ptr) {
         return BGABP_OK;
     })
 }
+
+int bgabp_dia_offsets(const bgabp_engine* h, int* off, int cap) {
+    const Engine& E = h->E;
+    if (E.layout != BGABP_LAYOUT_DIA) return -1;
+    for (int s = 0; s < E.S && s < cap; ++s) off[s] = E.dia.off[s];
+    return E.S;
+}
+
+void bgabp_trim_cache(void) { trim_block_cache(); }
 
 void* bgabp_shard_msg(bgabp_engine* h, int which) { return (void*)h->E.d_msg[which & 1]; }
 void* bgabp_shard_x(bgabp_engine* h, int which) {  // the slot holding x(which)

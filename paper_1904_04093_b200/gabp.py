@@ -84,6 +84,8 @@ def lib():
             "bgabp_node_precisions": (C.c_int, [_vp, _dp]),
             "bgabp_sweep_flops": (C.c_double, [_vp]),
             "bgabp_set_damping": (C.c_int, [_vp, C.c_double]),
+            "bgabp_dia_offsets": (C.c_int, [_vp, _ip, C.c_int]),
+            "bgabp_trim_cache": (None, []),
             "bgabp_solve": (C.c_int, [_vp, _dp, S, C.POINTER(_Opts), C.POINTER(_Rep), _dp, _dp, C.c_char_p,
                                       C.c_size_t]),
             "bgabp_solve_device_begin": (C.c_int, [_vp, _vp, S, C.POINTER(_Opts)]),

@@ -107,6 +107,9 @@ class GpuShard:
         self.eng = GabpEngine(A_local, Layout.Dia)
         _raise(lib().bgabp_shard_set_range(self.eng.handle, L.own_lo, L.own_hi, L.glo), "shard_set_range")
         self.S = int(self.eng.info["num_slots"])
+        off = (C.c_int * 8)()
+        cnt = lib().bgabp_dia_offsets(self.eng.handle, off, 8)
+        self.offsets = tuple(off[:cnt])
         self.device = torch.device(device)
         self.stream = torch.cuda.ExternalStream(self.eng.stream(), device=self.device)
         self.b = torch.as_tensor(np.ascontiguousarray(b_local, np.float64), device=self.device)
@@ -229,6 +232,14 @@ def sharded_solve(shards: dict, layouts, owner, world, b_inf, opt: GabpOptions, 
     ex = Exchange(shards, layouts, owner, world)
     first = next(iter(shards.values()))
     gpu = isinstance(first, GpuShard)
+    if gpu:  # every shard of every rank must hold the same DIA offsets
+        mine = [s.offsets for s in shards.values()]
+        if world > 1:
+            import torch.distributed as dist
+            every = [None] * world
+            dist.all_gather_object(every, mine)
+            mine = [o for r in every for o in r]
+        check_offsets(mine)
     single = len(shards) == 1
     ctx = torch.cuda.stream(first.stream) if (gpu and single) else contextlib.nullcontext()
     sync = torch.cuda.synchronize if (gpu and not single) else (lambda: None)
@@ -260,6 +271,16 @@ def sharded_solve(shards: dict, layouts, owner, world, b_inf, opt: GabpOptions, 
     return res[0], res[1], res[2], out, res[3]
 
 
+def check_offsets(offsets):
+    """Halos move slot by slot (peer stores / pack / unpack use the neighbour's slot order), so
+    every shard must hold the same DIA offsets; a row block that lacks one would land messages in
+    the wrong slots."""
+    offsets = list(offsets)
+    if any(o != offsets[0] for o in offsets):
+        raise ValueError(f"shard: the row blocks have different DIA neighbour offsets {sorted(set(offsets))}; "
+                         "partition so that every block holds every stencil offset")
+
+
 def connect_peers(shards: dict, layouts):
     """Wire every GpuShard of this process to its neighbours for the peer-memory step: each
     shard stores the halo messages / x it computes straight into the neighbour's buffers and its
@@ -269,6 +290,7 @@ def connect_peers(shards: dict, layouts):
     P = len(layouts)
     if sorted(shards) != list(range(P)):
         raise ValueError("connect_peers: every shard must live in this process")
+    check_offsets(shards[k].offsets for k in range(P))
     slots = []
     for k in range(P):
         p = C.c_void_p()
@@ -362,9 +384,10 @@ def sharded_solve_ipc(shard, layouts, b_inf, opt: GabpOptions, poll_every=16, ho
         return buf.raw
 
     mine = {"msg0": export(L.bgabp_shard_msg(h, 0)), "msg1": export(L.bgabp_shard_msg(h, 1)),
-            "x": export(L.bgabp_shard_x(h, 0)), "slots": export(slots.value)}
+            "x": export(L.bgabp_shard_x(h, 0)), "slots": export(slots.value), "offsets": shard.offsets}
     peers = [None] * P
     dist.all_gather_object(peers, mine)
+    check_offsets(p["offsets"] for p in peers)
     opened = []
 
     def imp(handle):
