@@ -6,7 +6,7 @@ package is its Python host mirror of the reference's proj/core API (see gabp.py)
 """
 from .gabp import (AssembledProblem, CycleSpec, FrozenLambda, GabpEngine, GabpOptions, Hierarchy, Layout,  # noqa: F401
                    LineGabpEngine, MessageState, RegionSolveOptions, RegionSweepMode, MgSmoother, MgSolveOptions, Schedule, ScheduleKind, SolveReport, SolveStatus,
-                   SparseMatrix, StopCriterion, assemble, config5_level, config_problem, lib, load_matrix_market, mg_prolong,
+                   SparseMatrix, StopCriterion, assemble, config5_level, varcoef2d_rule_level, config_problem, lib, load_matrix_market, mg_prolong,
                    mg_restrict, mg_solve, mg_solve_device, poisson5)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

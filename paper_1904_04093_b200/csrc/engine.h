@@ -144,7 +144,11 @@ struct Engine {
     void build_dia_host();
     void build_ucsr_host();
     // general sparsity: SELL layout of the union graph for the fused solve step (sell.cu)
-    SellP sell[2]{};  // [0] chunks of <= 8 slot rows (register-cached kernel), [1] wider chunks
+    static constexpr int kSellBuckets = 4;
+    SellP sell[kSellBuckets]{};  // chunks of <= 8 / <= 16 / <= 32 slot rows (TMA-staged), wider (registers)
+    unsigned sell_grid[3] = {0, 0, 0};  // persistent grids of the TMA-staged kernels
+    bool sell_reg = false;  // BGABP_SELL_KIND=reg: the register-cached kernels for every bucket (A/B)
+    void sell_tma_setup();
     bool sell_ready = false;
     bool use_ucsr_solve = false;  // BGABP_UCSR_SOLVE=1: the three-launch union-CSR solve loop instead
     long long sell_slots = 0;

@@ -598,10 +598,12 @@ static void build_hierarchy(bgmg* h, int nlevels, const int* n, const int* const
         h->levels.push_back(std::move(L));
         phase("engine build", k);
     }
+    // BGABP_MG_NO_PROBE=1 (experiments only, tools/config5_coarse_rules.py): keep every level
+    const bool probe = !(std::getenv("BGABP_MG_NO_PROBE") && std::atoi(std::getenv("BGABP_MG_NO_PROBE")) != 0);
     if (is_gabp(smoother)) {
         for (int k = 0; k < (int)h->levels.size(); ++k) {
             MgLevel& L = h->levels[k];
-            if (k > 0 && L.E->sweeps_expand(L.sched)) {  // multigrid.cpp:89-93
+            if (probe && k > 0 && L.E->sweeps_expand(L.sched)) {  // multigrid.cpp:89-93
                 h->levels.resize(k + 1);
                 break;
             }
@@ -620,6 +622,9 @@ static void build_hierarchy(bgmg* h, int nlevels, const int* n, const int* const
     ck(cudaMallocHost((void**)&h->h_sum, 2 * sizeof(unsigned long long)), "host sum");
     if (const char* e = std::getenv("BGABP_MG_GRAPH")) h->use_graphs = std::atoi(e) != 0;
     Engine& C = *h->levels.back().E;
+    if (C.n > 20000)  // a dense n^2 inverse (and its LU) would not fit a sensible setup
+        throw InvalidArg("Hierarchy: coarsest level has " + std::to_string(C.n) +
+                         " unknowns, too many for the dense direct solve");
     std::vector<double> inv = dense_inverse(C);
     phase("coarse inverse", (int)h->levels.size() - 1);
     ck(cudaMalloc(&h->d_inv, sizeof(double) * std::max<size_t>(inv.size(), 1)), "malloc");

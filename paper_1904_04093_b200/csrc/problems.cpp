@@ -295,10 +295,17 @@ struct Config5Field {
     std::vector<double> b;
 };
 
-Config5Field& config5_field(int J, unsigned seed, double sigma, int levels) {
+// Coarse-K rules (rule 0 is the generator's; 1-3 are the alternatives tools/config5_coarse_rules.py
+// measures): 0 full-weighted log K (weighted geometric mean), 1 full-weighted K (arithmetic),
+// 2 full-weighted 1/K (harmonic), 3 injection of the coinciding fine vertex.
+Config5Field& config5_field(int J, unsigned seed, double sigma, int levels, int rule = 0) {
     static Config5Field cache;
-    if (cache.J == J && cache.seed == seed && cache.sigma == sigma && (int)cache.logK.size() >= levels) return cache;
+    static int cache_rule = 0;
+    if (cache.J == J && cache.seed == seed && cache.sigma == sigma && cache_rule == rule &&
+        (int)cache.logK.size() >= levels)
+        return cache;
     cache = Config5Field();
+    cache_rule = rule;
     cache.J = J;
     cache.seed = seed;
     cache.sigma = sigma;
@@ -317,10 +324,19 @@ Config5Field& config5_field(int J, unsigned seed, double sigma, int levels) {
         for (int IY = 0; IY < mc; ++IY)
             for (int IX = 0; IX < mc; ++IX) {
                 const int x = 2 * IX + 1, y = 2 * IY + 1;
-                auto F = [&](int a, int b2) { return f[(size_t)b2 * mf + a]; };
-                const double v = 4.0 * F(x, y) + 2.0 * (F(x - 1, y) + F(x + 1, y) + F(x, y - 1) + F(x, y + 1)) +
-                                 F(x - 1, y - 1) + F(x + 1, y - 1) + F(x - 1, y + 1) + F(x + 1, y + 1);
-                c[(size_t)IY * mc + IX] = v / 16.0;
+                // log K -> the averaged quantity of the rule -> log K
+                auto F = [&](int a, int b2) {
+                    const double l = f[(size_t)b2 * mf + a];
+                    return rule == 1 ? std::exp(l) : rule == 2 ? std::exp(-l) : l;
+                };
+                if (rule == 3) {
+                    c[(size_t)IY * mc + IX] = f[(size_t)y * mf + x];
+                    continue;
+                }
+                const double v = (4.0 * F(x, y) + 2.0 * (F(x - 1, y) + F(x + 1, y) + F(x, y - 1) + F(x, y + 1)) +
+                                  F(x - 1, y - 1) + F(x + 1, y - 1) + F(x - 1, y + 1) + F(x + 1, y + 1)) /
+                                 16.0;
+                c[(size_t)IY * mc + IX] = rule == 1 ? std::log(v) : rule == 2 ? -std::log(v) : v;
             }
         cache.logK.push_back(std::move(c));
         mf = mc;
@@ -328,8 +344,8 @@ Config5Field& config5_field(int J, unsigned seed, double sigma, int levels) {
     return cache;
 }
 
-bgabp_problem* varcoef2d_problem(int Jf, int k, unsigned seed, double sigma) {
-    Config5Field& F = config5_field(Jf, seed, sigma, Jf);  // every level at once: later calls hit the cache
+bgabp_problem* varcoef2d_problem(int Jf, int k, unsigned seed, double sigma, int rule = 0) {
+    Config5Field& F = config5_field(Jf, seed, sigma, Jf, rule);  // every level at once: later calls hit the cache
     if ((int)F.logK.size() <= k) throw std::invalid_argument("config 5: level below the coarsest grid");
     const int J = Jf - k, m = (1 << J) - 1;
     const double h = 1.0 / (1 << J), inv_h2 = 1.0 / (h * h);
@@ -546,6 +562,15 @@ bgabp_problem* bgabp_problem_config(int config, int size, unsigned seed) {
 
 bgabp_problem* bgabp_problem_config5_level(int J_fine, int k, unsigned seed) {
     return bgabp_problem_varcoef2d_level(J_fine, k, seed, 2.0);
+}
+
+bgabp_problem* bgabp_problem_varcoef2d_rule(int J_fine, int k, unsigned seed, double sigma, int rule) {
+    try {
+        if (rule < 0 || rule > 3) return nullptr;
+        return varcoef2d_problem(J_fine, k, seed, sigma, rule);
+    } catch (const std::exception&) {
+        return nullptr;
+    }
 }
 
 bgabp_problem* bgabp_problem_varcoef2d_level(int J_fine, int k, unsigned seed, double sigma) {

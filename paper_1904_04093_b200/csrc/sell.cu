@@ -1,6 +1,8 @@
 // SELL layout of the union message graph and the fused general-sparsity flood solve step
 // (sell_kernels.cuh).  Built once per handle from the union-CSR lists (build.cu).
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 #include <numeric>
 #include <vector>
 
@@ -53,8 +55,10 @@ void Engine::build_sell(const std::vector<uint8_t>& flg, const std::vector<doubl
             cout[p] = uc[u];
             if (!symmetric) rowv[p] = urow[u];
         }
-    std::vector<int> narrow, wide;  // chunk lists per bucket: <= 8 slot rows (register cached) / more
-    for (int c = 0; c < C; ++c) (cwid[c] <= 8 ? narrow : wide).push_back(c);
+    // chunk lists per width bucket: <= 8, <= 16, <= 32 slot rows (shared-memory staged kernels)
+    // and wider (register kernel, any width)
+    std::vector<int> lists[kSellBuckets];
+    for (int c = 0; c < C; ++c) lists[cwid[c] <= 8 ? 0 : cwid[c] <= 16 ? 1 : cwid[c] <= 32 ? 2 : 3].push_back(c);
     SellP P{};
     P.n = n;
     P.crow = upload(crow);
@@ -65,18 +69,70 @@ void Engine::build_sell(const std::vector<uint8_t>& flg, const std::vector<doubl
     P.cout = upload(cout);
     P.rowv = symmetric ? P.cout : upload(rowv);
     P.diag = d_diag;
-    sell[0] = sell[1] = P;
-    sell[0].chunks = upload(narrow);
-    sell[0].nchunks = (int)narrow.size();
-    sell[1].chunks = upload(wide);
-    sell[1].nchunks = (int)wide.size();
+    for (int q = 0; q < kSellBuckets; ++q) {
+        sell[q] = P;
+        sell[q].chunks = upload(lists[q]);
+        sell[q].nchunks = (int)lists[q].size();
+    }
+    sell_tma_setup();
+    if (const char* e = getenv("BGABP_SELL_KIND")) sell_reg = std::string(e) == "reg";
     sell_ready = true;
+}
+
+// TMA-staged kernels: (max rows, warps per block) per bucket, and the persistent grid
+#define SELL_TMA_VARIANTS(X) X(8, 4) X(16, 2) X(32, 1)
+template <int WMAX, int WPB>
+static void sell_tma_attr(int& blocks_per_sm) {
+    const size_t smem = sell_tma_smem<WMAX, WPB>();
+#define SET_ATTR(D_, S_, M_)                                                                                     \
+    ck(cudaFuncSetAttribute(k_flood_solve_sell_tma<WMAX, WPB, D_, S_, M_>,                                       \
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),                             \
+       "sell smem");
+    SET_ATTR(false, false, false) SET_ATTR(true, false, false) SET_ATTR(false, true, false) SET_ATTR(true, true, false)
+    SET_ATTR(false, false, true) SET_ATTR(true, false, true) SET_ATTR(false, true, true) SET_ATTR(true, true, true)
+#undef SET_ATTR
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_flood_solve_sell_tma<WMAX, WPB, false, true, false>,
+                                                     32 * WPB, smem),
+       "occupancy");
+    blocks_per_sm = std::max(blocks_per_sm, 1);
+}
+
+void Engine::sell_tma_setup() {
+    int sms = 148;
+    ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "sm count");
+    int q = 0;
+#define SETUP(W_, P_)                                                                                            \
+    {                                                                                                            \
+        int bps = 1;                                                                                             \
+        sell_tma_attr<W_, P_>(bps);                                                                              \
+        sell_grid[q++] = sms * bps;                                                                              \
+    }
+    SELL_TMA_VARIANTS(SETUP)
+#undef SETUP
+}
+
+template <int WMAX, int WPB>
+static void launch_tma(const SellP& P, unsigned grid, bool dl, bool sym, bool damp, const double* b, double2* m0,
+                       double2* m1, double* x0, double* x1, Ctrl* ctrl, unsigned long long* spread,
+                       cudaStream_t st) {
+    const unsigned g = std::min<unsigned>(grid, (unsigned)((P.nchunks + WPB - 1) / WPB));
+    const size_t smem = sell_tma_smem<WMAX, WPB>();
+#define TMA_K(D_, S_, M_) \
+    k_flood_solve_sell_tma<WMAX, WPB, D_, S_, M_><<<g, 32 * WPB, smem, st>>>(P, b, m0, m1, x0, x1, ctrl, spread)
+    if (damp) {
+        if (sym) { if (dl) TMA_K(true, true, true); else TMA_K(false, true, true); }
+        else { if (dl) TMA_K(true, false, true); else TMA_K(false, false, true); }
+    } else {
+        if (sym) { if (dl) TMA_K(true, true, false); else TMA_K(false, true, false); }
+        else { if (dl) TMA_K(true, false, false); else TMA_K(false, false, false); }
+    }
+#undef TMA_K
 }
 
 // one fused solve step on the SELL layout: one launch per non-empty width bucket
 void Engine::launch_sell_step(bool dl) {
     const bool damp = damping != 0.0;
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < kSellBuckets; ++q) {
         SellP P = sell[q];
         if (P.nchunks == 0) continue;
         P.damp = damping;
@@ -84,6 +140,12 @@ void Engine::launch_sell_step(bool dl) {
         const unsigned g = nblk_host((long long)P.nchunks * 32);
         double2 *m0 = d_msg[0], *m1 = d_msg[1];
         double *x0 = d_xf, *x1 = d_xf + n;
+        if (!sell_reg && q < 3) {  // shared-memory staged (bulk async copies)
+            if (q == 0) launch_tma<8, 4>(P, sell_grid[0], dl, symmetric, damp, solve_b, m0, m1, x0, x1, d_ctrl, d_spread, st);
+            else if (q == 1) launch_tma<16, 2>(P, sell_grid[1], dl, symmetric, damp, solve_b, m0, m1, x0, x1, d_ctrl, d_spread, st);
+            else launch_tma<32, 1>(P, sell_grid[2], dl, symmetric, damp, solve_b, m0, m1, x0, x1, d_ctrl, d_spread, st);
+            continue;
+        }
 #define SELL_LAUNCH(W_)                                                                                          \
     if (damp) {                                                                                                  \
         if (symmetric) {                                                                                         \

@@ -246,3 +246,184 @@ static __global__ void __launch_bounds__(256, 2) k_flood_solve_sell(SellP P, con
 }
 
 }  // namespace bgabp
+
+namespace bgabp {
+
+// ---- TMA-staged SELL step ---------------------------------------------------------------------
+// The same step with the chunk's slot rows moved into shared memory by bulk asynchronous copies
+// (cp.async.bulk, completion on an mbarrier) instead of per-lane loads held in registers: each
+// warp walks its chunks (stride = all warps of the grid) with two buffers, the copies of chunk
+// i+1 in flight while chunk i is evaluated from shared memory.  A chunk's rows of rev, nbr,
+// messages and coefficients are contiguous in HBM (crow[c]*32 ... (crow[c]+wid)*32), so each is
+// one bulk copy; registers no longer limit the bytes in flight (the register-cached kernel ran
+// at 16 warps/SM, long-scoreboard bound).  Per slot row: rev 128 B + nbr 128 B + messages 512 B +
+// coefficients 256 B = 1 KB of shared memory per buffer and row.
+constexpr int kSellRowBytes = 32 * (4 + 4 + 16 + 8);
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+template <int WMAX, int WPB, bool DELTA, bool SYM, bool DAMP>
+static __global__ void __launch_bounds__(32 * WPB) k_flood_solve_sell_tma(SellP P, const double* __restrict__ b,
+                                                                         double2* m0, double2* m1, double* x0,
+                                                                         double* x1, Ctrl* ctrl,
+                                                                         unsigned long long* spread) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    if (ld_ctrl(&ctrl->done)) return;
+    const int t = ld_ctrl(&ctrl->step);
+    const double2* __restrict__ min = (t & 1) ? m0 : m1;
+    double2* __restrict__ mout = (t & 1) ? m1 : m0;
+    double* __restrict__ xw = ((t - 1) & 1) ? x1 : x0;        // x(t-1)
+    const double* __restrict__ xr = ((t - 2) & 1) ? x1 : x0;  // x(t-2)
+    const bool res = t >= 3;
+    const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // per warp: [2 buffers][rev | nbr | msg | cout] rows, then two mbarriers at the block's end
+    unsigned char* wbase = smem + (size_t)wl * 2 * WMAX * kSellRowBytes;
+    unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + (size_t)WPB * 2 * WMAX * kSellRowBytes) + 2 * wl;
+    auto rev_of = [&](int buf) { return reinterpret_cast<unsigned*>(wbase + (size_t)buf * WMAX * kSellRowBytes); };
+    auto nbr_of = [&](int buf) { return reinterpret_cast<int*>(rev_of(buf) + 32 * WMAX); };
+    auto msg_of = [&](int buf) { return reinterpret_cast<double2*>(nbr_of(buf) + 32 * WMAX); };
+    auto cs_of = [&](int buf) { return reinterpret_cast<double*>(msg_of(buf) + 32 * WMAX); };
+    if (lane == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    const int stride = gridDim.x * WPB;
+    auto issue = [&](int idx, int buf) {  // lane 0: the chunk's rows into buffer `buf`
+        const int c = __ldg(P.chunks + idx);
+        const int wid = __ldg(P.cwid + c);
+        const long long r0 = __ldg(P.crow + c) * 32;
+        const unsigned rows = (unsigned)wid;
+        mbar_arrive_tx(&bars[buf], rows * kSellRowBytes);
+        if (rows) {
+            bulk_g2s(rev_of(buf), P.rev + r0, rows * 128u, &bars[buf]);
+            bulk_g2s(nbr_of(buf), P.nbr + r0, rows * 128u, &bars[buf]);
+            bulk_g2s(msg_of(buf), min + r0, rows * 512u, &bars[buf]);
+            bulk_g2s(cs_of(buf), P.cout + r0, rows * 256u, &bars[buf]);
+        }
+    };
+    double rabs = 0.0, dmax = 0.0;
+    int idx = blockIdx.x * WPB + wl, buf = 0;
+    unsigned phase[2] = {0u, 0u};
+    if (idx < P.nchunks && lane == 0) issue(idx, 0);
+    while (idx < P.nchunks) {
+        const int nxt = idx + stride;
+        if (nxt < P.nchunks && lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of buf^1
+            issue(nxt, buf ^ 1);
+        }
+        const int c = __ldg(P.chunks + idx);
+        const int wid = __ldg(P.cwid + c);
+        const int j = __ldg(P.cnode + 32 * c + lane);
+        const long long base = __ldg(P.crow + c) * 32 + lane;
+        mbar_wait(&bars[buf], phase[buf]);
+        phase[buf] ^= 1u;
+        const unsigned* sr = rev_of(buf);
+        const int* sn = nbr_of(buf);
+        const double2* sm = msg_of(buf);
+        const double* sc = cs_of(buf);
+        if (j >= 0) {
+            const double dj = __ldg(P.diag + j), bj = __ldg(b + j);
+            const double xj = res ? __ldg(xr + j) : 0.0;
+            double sig = 0.0, acc = bj, r = bj;
+            bool dsig = false, dres = false;
+            for (int g0 = 0; g0 < wid; g0 += 8) {
+                double xk[8], rv[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {  // the residual's gathers, issued together
+                    const int s = g0 + q;
+                    const bool in = s < wid && (sr[32 * s + lane] & kSellIn);
+                    xk[q] = (res && in) ? __ldg(xr + sn[32 * s + lane]) : 0.0;
+                    rv[q] = (!SYM && res && in) ? __ldg(P.rowv + base + 32ll * s) : 0.0;
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int s = g0 + q;
+                    if (s >= wid) break;
+                    const unsigned f = sr[32 * s + lane];
+                    const int k = sn[32 * s + lane];
+                    if (k > j) {
+                        if (!dsig) {
+                            sig = dadd(sig, dj);
+                            dsig = true;
+                        }
+                        if (res && !dres) {
+                            r = dsub(r, dmul(dj, xj));
+                            dres = true;
+                        }
+                    }
+                    if (f & kSellIn) {
+                        const double2 v = sm[32 * s + lane];
+                        const double cs = sc[32 * s + lane];
+                        acc = dadd(acc, v.y);
+                        if (f & kSellOut) sig = dadd(sig, dmul(v.x, cs));
+                        if (res) r = dsub(r, dmul(SYM ? cs : rv[q], xk[q]));
+                    }
+                }
+            }
+            if (!dsig) sig = dadd(sig, dj);
+            if (res && !dres) r = dsub(r, dmul(dj, xj));
+            if (t >= 2) {  // x-stage of sweep t-1
+                xw[j] = ddiv(acc, sig);
+                if (fabs(sig) < kPivotFloor) atomicMin(&ctrl->npiv[(t - 1) & 3], (unsigned long long)j);
+            }
+            if (res) rabs = fmax(rabs, nan_skip_abs(r));
+            for (int s = 0; s < wid; ++s) {
+                const unsigned f = sr[32 * s + lane];
+                if (!(f & kSellOut)) continue;
+                const double cs = sc[32 * s + lane];
+                const double2 vi = (f & kSellIn) ? sm[32 * s + lane] : make_double2(0.0, 0.0);
+                const double den = dsub(sig, dmul(vi.x, cs));
+                if (fabs(den) < kPivotFloor)
+                    atomicMin(&ctrl->epiv[t & 3], ((unsigned long long)j << 32) | (unsigned)sn[32 * s + lane]);
+                double nl = ddiv(-cs, den);
+                double nm = dmul(nl, dsub(acc, vi.y));
+                const unsigned tgt = f & kSellSlot;
+                if (DELTA || DAMP) {
+                    const double2 o = min[tgt];
+                    if (DAMP) {
+                        const double2 w2 = damp_msg(nl, nm, o, P.damp, P.undamp);
+                        nl = w2.x;
+                        nm = w2.y;
+                    }
+                    if (DELTA) dmax = fmax(dmax, fmax(nan_skip_abs(dsub(nl, o.x)), nan_skip_abs(dsub(nm, o.y))));
+                }
+                mout[tgt] = make_double2(nl, nm);
+            }
+        }
+        __syncwarp();  // every lane is done with `buf` before it is refilled
+        buf ^= 1;
+        idx = nxt;
+    }
+    if (res) warp_max_spread(spread + (size_t)((t - 2) & 3) * kSpread, rabs);
+    if (DELTA) warp_max_spread(spread + (size_t)(4 + (t & 3)) * kSpread, dmax);
+}
+
+template <int WMAX, int WPB>
+constexpr size_t sell_tma_smem() {
+    return (size_t)WPB * 2 * WMAX * kSellRowBytes + (size_t)WPB * 2 * sizeof(unsigned long long);
+}
+
+}  // namespace bgabp

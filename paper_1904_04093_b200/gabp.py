@@ -127,6 +127,7 @@ def lib():
             "bgabp_problem_config": (_vp, [C.c_int, C.c_int, C.c_uint]),
             "bgabp_problem_config5_level": (_vp, [C.c_int, C.c_int, C.c_uint]),
             "bgabp_problem_varcoef2d_level": (_vp, [C.c_int, C.c_int, C.c_uint, C.c_double]),
+            "bgabp_problem_varcoef2d_rule": (_vp, [C.c_int, C.c_int, C.c_uint, C.c_double, C.c_int]),
             "bgabp_problem_free": (None, [_vp]),
             "bgabp_problem_n": (C.c_int, [_vp]),
             "bgabp_problem_nnz": (C.c_longlong, [_vp]),
@@ -825,6 +826,15 @@ def config_problem(config, size=0, seed=None) -> AssembledProblem:
     p = lib().bgabp_problem_config(config, size, seed)
     if not p:
         raise ValueError(f"config {config}: bad size {size}")
+    return _take_problem(p)
+
+
+def varcoef2d_rule_level(J_fine, k, rule, seed=4, sigma=2.0) -> AssembledProblem:
+    """Config-5 family level with another coarse-K rule (0 = the generator's full-weighted log K,
+    1 = full-weighted K, 2 = full-weighted 1/K, 3 = injection)."""
+    p = lib().bgabp_problem_varcoef2d_rule(J_fine, k, seed, sigma, rule)
+    if not p:
+        raise ValueError(f"varcoef2d: bad level / rule ({J_fine}, {k}, {rule})")
     return _take_problem(p)
 
 
