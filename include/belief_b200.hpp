@@ -102,8 +102,10 @@ public:
         rep.status = static_cast<SolveStatus>(r.status);
         rep.iterations = r.iterations;
         rep.flop_estimate = r.flop_estimate;
-        rep.residual_history.assign(hist.begin(), hist.begin() + r.iterations + 1);
         rep.detail = detail;
+        // a pivot stop pushes no residual for its iteration (gabp.cpp:193-199)
+        const bool pivot = rep.status == SolveStatus::Diverged && rep.detail.rfind("zero pivot", 0) == 0;
+        rep.residual_history.assign(hist.begin(), hist.begin() + r.iterations + (pivot ? 0 : 1));
         return rep;
     }
 

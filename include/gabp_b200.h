@@ -127,7 +127,9 @@ double bgabp_sweep_flops(const bgabp_engine* e); /* gabp.cpp:165-172 */
 
 /* ---- solve(b, sched, opt) (gabp.cpp:174-219) ------------------------------------------------------
  * Starts from make_state() and leaves the handle's state at the last sweep run.  x_out (n) gets
- * the solution, history (max_iter+1, nullable) the residual history; detail gets
+ * the solution, history (max_iter+1, nullable) the residual history -- iterations + 1 entries, or
+ * iterations on a pivot stop (detail "zero pivot ...": the failed sweep has no residual,
+ * gabp.cpp:193-199; the buffer's next entry is then unspecified); detail gets
  * SolveReport::detail.  Iteration counts, statuses, details, histories and x follow the reference
  * exactly -- on a pivot stop x is the reference's partly updated x (gabp.cpp:71-87, 126-130,
  * 155-158).  b and x_out may be pageable (staged copies) or pinned (direct copies). */

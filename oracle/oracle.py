@@ -168,6 +168,7 @@ class Oracle:
             "orc_mg_cycle_flops": (C.c_double, [vp, C.c_int, C.c_int]),
             "orc_set_damping": (C.c_int, [vp, C.c_double]),
             "orc_set_threads": (C.c_int, [C.c_int]),
+
             "orc_flop_table": (C.c_double, [C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_size_t]),
             "orc_mg_restrict": (None, [_dp, C.c_int, _dp]),
             "orc_mg_prolong": (None, [_dp, C.c_int, _dp]),
@@ -195,6 +196,9 @@ class Oracle:
             "orc_random_tree": (vp, [vp, C.c_int, _ip]),
             "orc_random_cycle_chords": (vp, [vp, C.c_int]),
             "orc_poisson5": (vp, [C.c_int, C.c_int]),
+            "orc_config3": (vp, [C.c_int, C.c_double, C.c_double, C.c_uint, _dp]),
+            "orc_config4": (vp, [C.c_int, C.c_double, C.c_double, C.c_double, C.c_uint, _dp]),
+            "orc_config5_level": (vp, [C.c_int, C.c_int, C.c_uint, C.c_double, _dp]),
             "orc_example7x7": (vp, []),
             "orc_tree_diameter": (C.c_int, [C.c_int, _ip]),
         }
@@ -349,6 +353,33 @@ class Oracle:
     def poisson5(self, nx, ny) -> Csr:
         return self._own(self.lib.orc_poisson5(nx, ny))
 
+    def config_problem(self, config, size=0, seed=None, sigma=2.0):
+        """BASELINE.json configs 1-5 from the oracle's own generators (restatement only):
+        (A, b).  Config 5 is its finest level (J with 2^J - 1 = size, default 4095)."""
+        seed = {1: 0, 2: 1, 3: 2, 4: 3, 5: 4}[config] if seed is None else seed
+        if config in (1, 2):
+            N = size or (64 if config == 1 else 2048)
+            A = self.poisson5(N, N)
+            return A, self.rng(seed).vector(A.n)
+        if config == 3:
+            N = size or 1024
+            b = np.zeros(N * N)
+            return self._own(self.lib.orc_config3(N, 2.0, 0.3, seed, _d(b))), b
+        if config == 4:
+            N = size or 256
+            b = np.zeros(N ** 3)
+            return self._own(self.lib.orc_config4(N, 1.0, 1.0, 0.01, seed, _d(b))), b
+        if config == 5:
+            return self.config5_level(int(np.log2((size or 4095) + 1)), 0, seed, sigma)
+        raise ValueError(f"config {config}")
+
+    def config5_level(self, J, k, seed=4, sigma=2.0):
+        m = (1 << (J - k)) - 1
+        b = np.zeros(((1 << J) - 1) ** 2) if k == 0 else None
+        A = self._own(self.lib.orc_config5_level(J, k, seed, sigma, _d(b) if b is not None else None))
+        assert A.n == m * m
+        return A, b
+
     def example7x7(self) -> Csr:
         return self._own(self.lib.orc_example7x7())
 
@@ -496,7 +527,10 @@ class _Engine:
                                   _d(x), _d(hist), C.byref(it), C.byref(st), C.byref(fl), det, 512)
         if rc < 0:
             raise ValueError(det.value.decode())
-        return Report(st.value, it.value, hist[: it.value + 1].copy(), fl.value, x, det.value.decode())
+        d = det.value.decode()
+        # a pivot stop pushes no residual for its iteration (gabp.cpp:193-199)
+        nh = it.value + (0 if st.value == 1 and d.startswith("zero pivot") else 1)
+        return Report(st.value, it.value, hist[:nh].copy(), fl.value, x, d)
 
     def precompute_lambda(self, sched: Schedule, tol=1e-10, max_iter=500):
         lam = np.zeros(self.A.nnz)

@@ -70,6 +70,10 @@ int orc_solve(const orc_engine* e, const double* b, orc_sched s, double tol, int
               int stop_kind, double divergence_factor, double* x_out, double* history,
               int* iterations, int* status, double* flops, char* detail, size_t detaillen);
 int orc_set_threads(int k); /* OpenMP threads of the restatement (1 in the reference build) */
+/* BASELINE.json configs 3-5 (restatement only): matrix, b into b_out */
+orc_matrix* orc_config3(int N, double pe_cell, double theta, unsigned seed, double* b_out);
+orc_matrix* orc_config4(int N, double wx, double wy, double wz, unsigned seed, double* b_out);
+orc_matrix* orc_config5_level(int J, int k, unsigned seed, double sigma, double* b_out);
 int orc_set_damping(orc_engine* e, double alpha); /* restatement only (no reference damping) */
 int orc_precompute_lambda(const orc_engine* e, orc_sched s, double tol, int max_iter,
                           double* lam_out, double* sigma_out, int* converged, int* iterations);

@@ -439,8 +439,9 @@ class GabpEngine:
         o = opt._c()
         rc = lib().bgabp_solve(self._h, _d(_f64(b)), sp, C.byref(o), C.byref(rep), _d(x), _d(hist), det, 512)
         _raise(rc, det.value.decode())
-        return SolveReport(SolveStatus(rep.status), rep.iterations, hist[: rep.iterations + 1].copy(),
-                           rep.flop_estimate, x, det.value.decode())
+        d = det.value.decode()
+        return SolveReport(SolveStatus(rep.status), rep.iterations, hist[: solve_history_len(rep, d)].copy(),
+                           rep.flop_estimate, x, d)
 
     def residual_inf_norm(self, x, b):
         out = C.c_double(0)
@@ -732,6 +733,13 @@ def mg_solve(hier: Hierarchy, spec: CycleSpec, b, opt: MgSolveOptions = MgSolveO
     d = det.value.decode()
     return SolveReport(SolveStatus(rep.status), rep.iterations, hist[: _mg_hist_len(rep, d)].copy(),
                        rep.flop_estimate, x, d)
+
+
+def solve_history_len(rep, detail):
+    """GabpEngine::solve's residual history: iterations + 1 entries, one fewer on a pivot stop
+    (the failed sweep pushes no residual, gabp.cpp:193-199)."""
+    pivot = rep.status == SolveStatus.Diverged and detail.startswith("zero pivot")
+    return rep.iterations + (0 if pivot else 1)
 
 
 def _mg_hist_len(rep, detail):

@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 
 import paper_1904_04093_b200 as g
-from oracle.oracle import Csr, Oracle, Schedule as OSched
+from oracle.oracle import Oracle, Schedule as OSched
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
@@ -30,10 +30,13 @@ def checker():
     return o
 
 
-def _compare(checker, P, tol, cap, stop=0):
-    A = Csr(P.A.n, P.A.row_offsets, P.A.col_indices, P.A.values)
+def _compare(checker, P, tol, cap, stop=0, config=None):
+    # the checker's input from the oracle's own generators (equal to the product's, bit for bit)
+    A, b = Oracle.restatement().config_problem(config)
+    assert np.array_equal(A.row_offsets, P.A.row_offsets) and np.array_equal(A.col_indices, P.A.col_indices)
+    assert A.values.tobytes() == P.A.values.tobytes() and b.tobytes() == P.b.tobytes()
     got = g.GabpEngine(P.A).solve(P.b, g.Schedule.parallel_flood(), g.GabpOptions(tol=tol, max_iter=cap, stop=stop))
-    want = checker.engine(A).solve(P.b, OSched.parallel_flood(), tol=tol, max_iter=cap, stop=stop)
+    want = checker.engine(A).solve(b, OSched.parallel_flood(), tol=tol, max_iter=cap, stop=stop)
     assert (int(got.status), got.iterations, got.detail) == (want.status, want.iterations, want.detail)
     assert got.residual_history.tobytes() == want.residual_history.tobytes()
     assert got.solution.tobytes() == want.solution.tobytes()
@@ -46,7 +49,7 @@ def test_config2_checkpoints(checker, checkpoint):
     """poisson5(2048, 2048), b ~ U[-1,1] seed 1: iterations 1..100 and 1..500 of the solve loop
     (the tolerance 1e-8 ||b|| needs ~6.7M sweeps, so both stop at the cap)."""
     P = g.config_problem(2)
-    rep = _compare(checker, P, 1e-8 * np.abs(P.b).max(), checkpoint)
+    rep = _compare(checker, P, 1e-8 * np.abs(P.b).max(), checkpoint, config=2)
     assert rep.status == g.SolveStatus.MaxIter and rep.iterations == checkpoint
 
 
@@ -54,12 +57,12 @@ def test_config3_full_solve_to_1e8(checker):
     """1024^2 upwind convection-diffusion, nonsymmetric GaBP to rel. residual 1e-8: the same
     iteration count (1967) and every residual of the way, bit for bit."""
     P = g.config_problem(3)
-    rep = _compare(checker, P, 1e-8 * np.abs(P.b).max(), 20000)
+    rep = _compare(checker, P, 1e-8 * np.abs(P.b).max(), 20000, config=3)
     assert rep.status == g.SolveStatus.Converged and rep.iterations == 1967
 
 
 def test_config4_twenty_sweeps(checker):
     """256^3 anisotropic lognormal diffusion (100M edges), 20 sweeps of the solve loop."""
     P = g.config_problem(4)
-    rep = _compare(checker, P, 0.0, 20)
+    rep = _compare(checker, P, 0.0, 20, config=4)
     assert rep.iterations == 20

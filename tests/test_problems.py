@@ -110,3 +110,26 @@ def test_config5_levels_coarsen_consistently():
     _is_m_matrix_rows(fine.A)
     # rows scaled by 1/h^2: the coarse operator of a constant K would be 1/4 of the fine one
     assert fine.A.values.max() > 100.0
+
+
+@pytest.mark.parametrize("config,size", [(3, 40), (3, 1), (4, 12), (4, 3), (1, 0), (2, 48)])
+def test_config_generators_equal_the_oracles(orc, config, size):
+    """The product's config generators (direct CSR) equal the oracle's independent restatement of
+    the SURVEY.md 8(d) recipes (triplets through make_csr), bit for bit -- so the reference arm and
+    the CPU checks take their inputs from the oracle alone."""
+    p = g.config_problem(config, size=size)
+    A, b = orc.config_problem(config, size=size)
+    assert np.array_equal(p.A.row_offsets, A.row_offsets) and np.array_equal(p.A.col_indices, A.col_indices)
+    assert p.A.values.tobytes() == A.values.tobytes()
+    assert p.b.tobytes() == b.tobytes()
+
+
+@pytest.mark.parametrize("sigma", [2.0, 1.0])
+def test_config5_levels_equal_the_oracles(orc, sigma):
+    for k in range(4):
+        p = g.config5_level(7, k, sigma=sigma)
+        A, b = orc.config5_level(7, k, sigma=sigma)
+        assert np.array_equal(p.A.row_offsets, A.row_offsets) and np.array_equal(p.A.col_indices, A.col_indices)
+        assert p.A.values.tobytes() == A.values.tobytes()
+        if k == 0:
+            assert p.b.tobytes() == b.tobytes()
