@@ -151,8 +151,9 @@ class GpuShard:
         x = self.torch.empty(n, dtype=self.torch.float64, device=self.device)
         hist = self.torch.empty(max_iter + 2, dtype=self.torch.float64, device=self.device)
         status, its, flops, detail = self.eng.solve_device_end(x.data_ptr(), hist.data_ptr())
+        nh = its + (0 if int(status) == 1 and detail.startswith("zero pivot") else 1)  # gabp.cpp:193-199
         return (int(status), its, detail, x[self.L.own_lo:self.L.own_hi].cpu().numpy(),
-                hist[:its + 1].cpu().numpy())
+                hist[:nh].cpu().numpy())
 
 
 class Exchange:

@@ -216,4 +216,5 @@ class CpuShard:
             glob = np.arange(self.n) + self.L.glo
             x = np.where(glob < self.detail_key, x, self.x[(self.solx - 1) & 1].numpy())
         x = x[self.L.own_lo:self.L.own_hi]
-        return self.status, self.iterations, detail, x, self.hist[:self.iterations + 1].copy()
+        nh = self.iterations + (0 if self.status == 1 and detail.startswith("zero pivot") else 1)
+        return self.status, self.iterations, detail, x, self.hist[:nh].copy()
