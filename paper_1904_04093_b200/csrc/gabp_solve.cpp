@@ -207,7 +207,10 @@ int main(int argc, char** argv) {
             throw std::invalid_argument("solver '" + s.solver +
                                         "' is not on the GPU path (gabp | generalized-gabp | mg:<smoother>)");
         }
-        hist.resize((size_t)rep.iterations + 1);
+        // a failed sweep / cycle (pivot, smoother breakdown) pushes no residual: the reference's
+        // history then has `iterations` entries (gabp.cpp:193-199, multigrid.cpp:288-297)
+        const bool failed = rep.status == BGABP_DIVERGED && !detail.empty() && detail != "residual blowup";
+        hist.resize((size_t)rep.iterations + (failed ? 0 : 1));
         if (!s.out.empty()) {
             std::ofstream f(s.out);
             if (!f) throw std::runtime_error("cannot open " + s.out);
