@@ -76,22 +76,25 @@ void Engine::build_sell(const std::vector<uint8_t>& flg, const std::vector<doubl
     }
     sell_tma_setup();
     if (const char* e = getenv("BGABP_SELL_KIND")) sell_reg = std::string(e) == "reg";
+    if (const char* e = getenv("BGABP_SELL_TMA")) sell_variant = std::atoi(e) == 1 ? 1 : 0;
     sell_ready = true;
 }
 
-// TMA-staged kernels: (max rows, warps per block) per bucket, and the persistent grid
-#define SELL_TMA_VARIANTS(X) X(8, 4) X(16, 2) X(32, 1)
-template <int WMAX, int WPB>
+// TMA-staged kernels: (max rows, warps per block, buffers) per bucket variant, and persistent grids
+// (BGABP_SELL_TMA=v selects variant v of every bucket: 0 = double-buffered, 1 = one buffer with
+// twice the warps per block)
+#define SELL_TMA_VARIANTS(X) X(8, 4, 2) X(16, 2, 2) X(32, 1, 2) X(8, 8, 1) X(16, 4, 1) X(32, 2, 1)
+template <int WMAX, int WPB, int NB>
 static void sell_tma_attr(int& blocks_per_sm) {
-    const size_t smem = sell_tma_smem<WMAX, WPB>();
+    const size_t smem = sell_tma_smem<WMAX, WPB, NB>();
 #define SET_ATTR(D_, S_, M_)                                                                                     \
-    ck(cudaFuncSetAttribute(k_flood_solve_sell_tma<WMAX, WPB, D_, S_, M_>,                                       \
+    ck(cudaFuncSetAttribute(k_flood_solve_sell_tma<WMAX, WPB, NB, D_, S_, M_>,                                   \
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),                             \
        "sell smem");
     SET_ATTR(false, false, false) SET_ATTR(true, false, false) SET_ATTR(false, true, false) SET_ATTR(true, true, false)
     SET_ATTR(false, false, true) SET_ATTR(true, false, true) SET_ATTR(false, true, true) SET_ATTR(true, true, true)
 #undef SET_ATTR
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_flood_solve_sell_tma<WMAX, WPB, false, true, false>,
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_flood_solve_sell_tma<WMAX, WPB, NB, false, true, false>,
                                                      32 * WPB, smem),
        "occupancy");
     blocks_per_sm = std::max(blocks_per_sm, 1);
@@ -101,24 +104,24 @@ void Engine::sell_tma_setup() {
     int sms = 148;
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "sm count");
     int q = 0;
-#define SETUP(W_, P_)                                                                                            \
+#define SETUP(W_, P_, N_)                                                                                        \
     {                                                                                                            \
         int bps = 1;                                                                                             \
-        sell_tma_attr<W_, P_>(bps);                                                                              \
+        sell_tma_attr<W_, P_, N_>(bps);                                                                          \
         sell_grid[q++] = sms * bps;                                                                              \
     }
     SELL_TMA_VARIANTS(SETUP)
 #undef SETUP
 }
 
-template <int WMAX, int WPB>
+template <int WMAX, int WPB, int NB>
 static void launch_tma(const SellP& P, unsigned grid, bool dl, bool sym, bool damp, const double* b, double2* m0,
                        double2* m1, double* x0, double* x1, Ctrl* ctrl, unsigned long long* spread,
                        cudaStream_t st) {
     const unsigned g = std::min<unsigned>(grid, (unsigned)((P.nchunks + WPB - 1) / WPB));
-    const size_t smem = sell_tma_smem<WMAX, WPB>();
+    const size_t smem = sell_tma_smem<WMAX, WPB, NB>();
 #define TMA_K(D_, S_, M_) \
-    k_flood_solve_sell_tma<WMAX, WPB, D_, S_, M_><<<g, 32 * WPB, smem, st>>>(P, b, m0, m1, x0, x1, ctrl, spread)
+    k_flood_solve_sell_tma<WMAX, WPB, NB, D_, S_, M_><<<g, 32 * WPB, smem, st>>>(P, b, m0, m1, x0, x1, ctrl, spread)
     if (damp) {
         if (sym) { if (dl) TMA_K(true, true, true); else TMA_K(false, true, true); }
         else { if (dl) TMA_K(true, false, true); else TMA_K(false, false, true); }
@@ -141,9 +144,18 @@ void Engine::launch_sell_step(bool dl) {
         double2 *m0 = d_msg[0], *m1 = d_msg[1];
         double *x0 = d_xf, *x1 = d_xf + n;
         if (!sell_reg && q < 3) {  // shared-memory staged (bulk async copies)
-            if (q == 0) launch_tma<8, 4>(P, sell_grid[0], dl, symmetric, damp, solve_b, m0, m1, x0, x1, d_ctrl, d_spread, st);
-            else if (q == 1) launch_tma<16, 2>(P, sell_grid[1], dl, symmetric, damp, solve_b, m0, m1, x0, x1, d_ctrl, d_spread, st);
-            else launch_tma<32, 1>(P, sell_grid[2], dl, symmetric, damp, solve_b, m0, m1, x0, x1, d_ctrl, d_spread, st);
+#define TMA_L(W_, P_, N_, G_) \
+    launch_tma<W_, P_, N_>(P, sell_grid[G_], dl, symmetric, damp, solve_b, m0, m1, x0, x1, d_ctrl, d_spread, st)
+            if (sell_variant == 0) {
+                if (q == 0) TMA_L(8, 4, 2, 0);
+                else if (q == 1) TMA_L(16, 2, 2, 1);
+                else TMA_L(32, 1, 2, 2);
+            } else {
+                if (q == 0) TMA_L(8, 8, 1, 3);
+                else if (q == 1) TMA_L(16, 4, 1, 4);
+                else TMA_L(32, 2, 1, 5);
+            }
+#undef TMA_L
             continue;
         }
 #define SELL_LAUNCH(W_)                                                                                          \

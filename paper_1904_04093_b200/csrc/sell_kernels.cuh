@@ -252,8 +252,8 @@ namespace bgabp {
 // ---- TMA-staged SELL step ---------------------------------------------------------------------
 // The same step with the chunk's slot rows moved into shared memory by bulk asynchronous copies
 // (cp.async.bulk, completion on an mbarrier) instead of per-lane loads held in registers: each
-// warp walks its chunks (stride = all warps of the grid) with two buffers, the copies of chunk
-// i+1 in flight while chunk i is evaluated from shared memory.  A chunk's rows of rev, nbr,
+// warp walks its chunks (stride = all warps of the grid) with NB buffers: two = the copies of
+// chunk i+1 in flight while chunk i is evaluated from shared memory; one = more warps per SM.  A chunk's rows of rev, nbr,
 // messages and coefficients are contiguous in HBM (crow[c]*32 ... (crow[c]+wid)*32), so each is
 // one bulk copy; registers no longer limit the bytes in flight (the register-cached kernel ran
 // at 16 warps/SM, long-scoreboard bound).  Per slot row: rev 128 B + nbr 128 B + messages 512 B +
@@ -283,7 +283,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                  : "memory");
 }
 
-template <int WMAX, int WPB, bool DELTA, bool SYM, bool DAMP>
+template <int WMAX, int WPB, int NB, bool DELTA, bool SYM, bool DAMP>
 static __global__ void __launch_bounds__(32 * WPB) k_flood_solve_sell_tma(SellP P, const double* __restrict__ b,
                                                                          double2* m0, double2* m1, double* x0,
                                                                          double* x1, Ctrl* ctrl,
@@ -298,8 +298,8 @@ static __global__ void __launch_bounds__(32 * WPB) k_flood_solve_sell_tma(SellP 
     const bool res = t >= 3;
     const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // per warp: [2 buffers][rev | nbr | msg | cout] rows, then two mbarriers at the block's end
-    unsigned char* wbase = smem + (size_t)wl * 2 * WMAX * kSellRowBytes;
-    unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + (size_t)WPB * 2 * WMAX * kSellRowBytes) + 2 * wl;
+    unsigned char* wbase = smem + (size_t)wl * NB * WMAX * kSellRowBytes;
+    unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + (size_t)WPB * NB * WMAX * kSellRowBytes) + 2 * wl;
     auto rev_of = [&](int buf) { return reinterpret_cast<unsigned*>(wbase + (size_t)buf * WMAX * kSellRowBytes); };
     auto nbr_of = [&](int buf) { return reinterpret_cast<int*>(rev_of(buf) + 32 * WMAX); };
     auto msg_of = [&](int buf) { return reinterpret_cast<double2*>(nbr_of(buf) + 32 * WMAX); };
@@ -330,7 +330,7 @@ static __global__ void __launch_bounds__(32 * WPB) k_flood_solve_sell_tma(SellP 
     if (idx < P.nchunks && lane == 0) issue(idx, 0);
     while (idx < P.nchunks) {
         const int nxt = idx + stride;
-        if (nxt < P.nchunks && lane == 0) {
+        if (NB == 2 && nxt < P.nchunks && lane == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of buf^1
             issue(nxt, buf ^ 1);
         }
@@ -414,16 +414,20 @@ static __global__ void __launch_bounds__(32 * WPB) k_flood_solve_sell_tma(SellP 
             }
         }
         __syncwarp();  // every lane is done with `buf` before it is refilled
-        buf ^= 1;
+        if (NB == 1 && nxt < P.nchunks && lane == 0) {  // one buffer: refill it now
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(nxt, 0);
+        }
+        if (NB == 2) buf ^= 1;
         idx = nxt;
     }
     if (res) warp_max_spread(spread + (size_t)((t - 2) & 3) * kSpread, rabs);
     if (DELTA) warp_max_spread(spread + (size_t)(4 + (t & 3)) * kSpread, dmax);
 }
 
-template <int WMAX, int WPB>
+template <int WMAX, int WPB, int NB>
 constexpr size_t sell_tma_smem() {
-    return (size_t)WPB * 2 * WMAX * kSellRowBytes + (size_t)WPB * 2 * sizeof(unsigned long long);
+    return (size_t)WPB * NB * WMAX * kSellRowBytes + (size_t)WPB * 2 * sizeof(unsigned long long);
 }
 
 }  // namespace bgabp

@@ -99,6 +99,8 @@ def main():
     ap.add_argument("--J", type=int, default=10)
     ap.add_argument("--cycles", type=int, default=40)
     ap.add_argument("--sigmas", type=float, nargs="+", default=[2.0, 1.0])
+    ap.add_argument("--rules", nargs="+", default=list(RULES) + ["galerkin"])
+    ap.add_argument("--no-two-grid", action="store_true")
     args = ap.parse_args()
     J, nl = args.J, args.J - 4  # down to 31^2 as config 5
     out = {"J": J, "levels": nl, "cycle": "V(2,2)", "tol": "1e-8 ||b||_inf", "max_cycles": args.cycles,
@@ -111,6 +113,8 @@ def main():
     assert np.allclose(4.0 * restriction(15).T @ v, g.mg_prolong(v, 7), rtol=0, atol=1e-15)
     for sigma in args.sigmas:
         for name, rule in RULES.items():
+            if name not in args.rules:
+                continue
             levels = [g.varcoef2d_rule_level(J, k, rule, sigma=sigma) for k in range(nl)]
             b = levels[0].b
             for smn, sm in (("gabp_red_black", S.GabpRedBlack), ("gs_red_black", S.GsRedBlack)):
@@ -118,12 +122,16 @@ def main():
                 out["multilevel"][f"sigma{sigma:g}/{name}/{smn}"] = r
                 print(f"sigma {sigma} {name:8s} {smn:15s} {r}", file=sys.stderr, flush=True)
             # two-grid with the exact coarse solve (fine 127^2 -> coarse 63^2, dense)
+            if args.no_two_grid:
+                continue
             tg = [g.varcoef2d_rule_level(7, k, rule, sigma=sigma) for k in range(2)]
             for smn, sm in (("gabp_red_black", S.GabpRedBlack), ("gs_red_black", S.GsRedBlack)):
                 r = run([p.A for p in tg], [p.nx for p in tg], tg[0].b, sm, args.cycles)
                 out["two_grid_exact"][f"sigma{sigma:g}/{name}/{smn}"] = r
                 print(f"sigma {sigma} two-grid {name:8s} {smn:15s} {r}", file=sys.stderr, flush=True)
         # Galerkin coarse operators from the fine level of the generator
+        if "galerkin" not in args.rules:
+            continue
         fine = g.varcoef2d_rule_level(J, 0, 0, sigma=sigma)
         mats, nxs = [csr(fine.A)], [fine.nx]
         while len(mats) < nl:
