@@ -206,6 +206,9 @@ int bgabp_shard_p2p_decide(bgabp_engine* e, int spin);
 /* nsteps iterations of the peer-memory solve for the shards of one process (event-ordered);
  * use_graph: replay 16-iteration chunks from a CUDA graph captured across the shards' streams */
 int bgabp_shard_p2p_steps(bgabp_engine* const* shards, int count, int nsteps, int use_graph);
+/* one shard per process (peers mapped by CUDA IPC): nsteps iterations of p2p_compute followed by a
+ * decision that waits on the peers' step flags on the device (spin), no host synchronisation */
+int bgabp_shard_p2p_steps_ipc(bgabp_engine* e, int nsteps);
 /* CUDA IPC of device allocations (64-byte handles) for shards in different processes */
 int bgabp_ipc_get(const void* dev_ptr, void* handle_out);
 int bgabp_ipc_open(const void* handle, void** dev_ptr);

@@ -147,7 +147,7 @@ struct Engine {
     static constexpr int kSellBuckets = 4;
     SellP sell[kSellBuckets]{};  // chunks of <= 8 / <= 16 / <= 32 slot rows (TMA-staged), wider (registers)
     unsigned sell_grid[6] = {0, 0, 0, 0, 0, 0};  // persistent grids of the TMA-staged kernel variants
-    int sell_variant = 0;  // BGABP_SELL_TMA: 0 double-buffered, 1 single buffer / more warps
+    int sell_variant = 1;  // BGABP_SELL_TMA: 0 double-buffered, 1 single buffer / more warps (default)
     bool sell_reg = false;  // BGABP_SELL_KIND=reg: the register-cached kernels for every bucket (A/B)
     void sell_tma_setup();
     bool sell_ready = false;

@@ -210,6 +210,22 @@ static void p2p_enqueue_iteration(bgabp_engine* const* sh, int count) {
     }
 }
 
+// one process per shard (CUDA IPC peers): nsteps iterations of (step + peer stores + fold, then the
+// decision after a device-side wait on the peers' step flags), enqueued without host round trips
+int bgabp_shard_p2p_steps_ipc(bgabp_engine* h, int nsteps) {
+    ABI_GUARD(nullptr, 0, {
+        Engine& E = h->E;
+        if (!E.solve_fused || !E.peer_on) throw InvalidArg("shard: call set_peers and shard_solve_begin first");
+        for (int k = 0; k < nsteps; ++k) {
+            E.enqueue_fused_kernel();
+            k_shard_fold_p2p<<<1, kSpread, 0, E.st>>>(E.d_ctrl, E.d_spread, E.d_red4, E.peer);
+            k_shard_decide_p2p<<<1, 1, 0, E.st>>>(E.d_ctrl, E.d_hist, E.d_slots, E.peer.nranks, E.d_red4, E.peer.rank, 1);
+        }
+        ck(cudaGetLastError(), "p2p ipc steps");
+        return BGABP_OK;
+    })
+}
+
 int bgabp_shard_p2p_steps(bgabp_engine* const* shards, int count, int nsteps, int use_graph) {
     ABI_GUARD(nullptr, 0, {
         if (count < 1) throw InvalidArg("shard: no shards");

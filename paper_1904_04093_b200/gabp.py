@@ -166,6 +166,7 @@ def lib():
             "bgabp_shard_p2p_wait": (C.c_int, [_vp, _vp]),
             "bgabp_shard_p2p_decide": (C.c_int, [_vp, C.c_int]),
             "bgabp_shard_p2p_steps": (C.c_int, [C.POINTER(_vp), C.c_int, C.c_int, C.c_int]),
+            "bgabp_shard_p2p_steps_ipc": (C.c_int, [_vp, C.c_int]),
             "bgabp_ipc_get": (C.c_int, [_vp, _vp]),
             "bgabp_ipc_open": (C.c_int, [_vp, C.POINTER(_vp)]),
             "bgabp_ipc_close": (C.c_int, [_vp]),

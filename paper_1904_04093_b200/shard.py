@@ -360,6 +360,95 @@ def sharded_solve_p2p(shards: dict, layouts, b_inf, opt: GabpOptions, poll_every
     return res[0], res[1], res[2], out, res[3]
 
 
+class IpcSolve:
+    """The one-shard-per-process peer-memory solve as a stepping object (bench.py's multi-GPU
+    mode): connect() maps the neighbours' buffers and every rank's slot array with CUDA IPC,
+    begin() resets this rank, steps(k) enqueues k iterations (fused step with peer stores, fold,
+    device-side wait on the peers' step flags, decision) with no host synchronisation, end()
+    returns (status, iterations, detail, owned x, history)."""
+
+    def __init__(self, shard, layouts, host_barrier=False):
+        import torch.distributed as dist
+        self.dist, self.shard, self.layouts, self.host_barrier = dist, shard, layouts, host_barrier
+        self.L = lib()
+        self.rank, self.P = dist.get_rank(), dist.get_world_size()
+        if len(layouts) != self.P:
+            raise ValueError("sharded_solve_ipc: one shard per rank")
+        self.opened = []
+
+    def connect(self):
+        L, h, rank, P, layouts, dist = self.L, self.shard.eng.handle, self.rank, self.P, self.layouts, self.dist
+        slots = C.c_void_p()
+        _raise(L.bgabp_shard_peer_slots(h, C.byref(slots)), "peer slots")
+
+        def export(ptr):
+            buf = C.create_string_buffer(64)
+            _raise(L.bgabp_ipc_get(C.c_void_p(ptr), buf), "ipc get")
+            return buf.raw
+
+        mine = {"msg0": export(L.bgabp_shard_msg(h, 0)), "msg1": export(L.bgabp_shard_msg(h, 1)),
+                "x": export(L.bgabp_shard_x(h, 0)), "slots": export(slots.value), "offsets": self.shard.offsets}
+        peers = [None] * P
+        dist.all_gather_object(peers, mine)
+        check_offsets(p["offsets"] for p in peers)
+
+        def imp(handle):
+            p = C.c_void_p()
+            _raise(L.bgabp_ipc_open(handle, C.byref(p)), "ipc open")
+            self.opened.append(p.value)
+            return p.value
+
+        slot_ptrs = [slots.value if q == rank else imp(peers[q]["slots"]) for q in range(P)]
+
+        def nbr(q):
+            xb = imp(peers[q]["x"])
+            return (C.c_void_p * 4)(imp(peers[q]["msg0"]), imp(peers[q]["msg1"]), xb, xb + 8 * layouts[q].n_local)
+
+        Lk = layouts[rank]
+        lower = nbr(rank - 1) if rank > 0 else None
+        upper = nbr(rank + 1) if rank + 1 < P else None
+        _raise(L.bgabp_shard_set_peers(h, P, rank, lower, layouts[rank - 1].n_local if rank > 0 else 0,
+                                       Lk.glo - layouts[rank - 1].glo if rank > 0 else 0, upper,
+                                       layouts[rank + 1].n_local if rank + 1 < P else 0,
+                                       Lk.glo - layouts[rank + 1].glo if rank + 1 < P else 0,
+                                       layouts[rank - 1].ghi - Lk.glo if rank > 0 else 0,
+                                       layouts[rank + 1].glo - Lk.glo if rank + 1 < P else Lk.n_local,
+                                       (C.c_void_p * P)(*slot_ptrs)), "set peers")
+
+    def begin(self, opt: GabpOptions, r0: float):
+        import torch
+        self.opt = opt
+        self.shard.begin(opt, r0)  # zeroes this rank's buffers and slots
+        torch.cuda.synchronize()
+        self.dist.barrier()  # nobody stores into a peer before every peer has been reset
+
+    def steps(self, k):
+        import torch
+        if not self.host_barrier:
+            _raise(self.L.bgabp_shard_p2p_steps_ipc(self.shard.eng.handle, int(k)), "p2p ipc steps")
+            return
+        h = self.shard.eng.handle
+        for _ in range(k):
+            _raise(self.L.bgabp_shard_p2p_compute(h), "p2p compute")
+            torch.cuda.synchronize()
+            self.dist.barrier()
+            _raise(self.L.bgabp_shard_p2p_decide(h, 1), "p2p decide")
+
+    def done(self):
+        return self.shard.done()
+
+    def end(self):
+        return self.shard.end(self.opt.max_iter)
+
+    def close(self):
+        import torch
+        torch.cuda.synchronize()
+        self.dist.barrier()  # every peer is done storing before the mappings go
+        for p in self.opened:
+            self.L.bgabp_ipc_close(C.c_void_p(p))
+        self.opened = []
+
+
 def sharded_solve_ipc(shard, layouts, b_inf, opt: GabpOptions, poll_every=16, host_barrier=False):
     """One shard per process (one process per GPU, torch.distributed initialised): the neighbours'
     message buffers / x ring and every rank's slot array are mapped with CUDA IPC once, then each
@@ -369,69 +458,18 @@ def sharded_solve_ipc(shard, layouts, b_inf, opt: GabpOptions, poll_every=16, ho
     between the steps and the decisions (every peer flag is already set when a decision runs):
     the mode for ranks sharing one GPU, where device-side waits between processes must not be
     used.  Returns (status, iterations, detail, owned x, history)."""
-    import torch
-    import torch.distributed as dist
-    L = lib()
-    rank, P = dist.get_rank(), dist.get_world_size()
-    if len(layouts) != P:
-        raise ValueError("sharded_solve_ipc: one shard per rank")
-    h = shard.eng.handle
-    slots = C.c_void_p()
-    _raise(L.bgabp_shard_peer_slots(h, C.byref(slots)), "peer slots")
-
-    def export(ptr):
-        buf = C.create_string_buffer(64)
-        _raise(L.bgabp_ipc_get(C.c_void_p(ptr), buf), "ipc get")
-        return buf.raw
-
-    mine = {"msg0": export(L.bgabp_shard_msg(h, 0)), "msg1": export(L.bgabp_shard_msg(h, 1)),
-            "x": export(L.bgabp_shard_x(h, 0)), "slots": export(slots.value), "offsets": shard.offsets}
-    peers = [None] * P
-    dist.all_gather_object(peers, mine)
-    check_offsets(p["offsets"] for p in peers)
-    opened = []
-
-    def imp(handle):
-        p = C.c_void_p()
-        _raise(L.bgabp_ipc_open(handle, C.byref(p)), "ipc open")
-        opened.append(p.value)
-        return p.value
-
-    slot_ptrs = [slots.value if q == rank else imp(peers[q]["slots"]) for q in range(P)]
-
-    def nbr(q):
-        xb = imp(peers[q]["x"])
-        return (C.c_void_p * 4)(imp(peers[q]["msg0"]), imp(peers[q]["msg1"]), xb, xb + 8 * layouts[q].n_local)
-
-    Lk = layouts[rank]
-    lower = nbr(rank - 1) if rank > 0 else None
-    upper = nbr(rank + 1) if rank + 1 < P else None
-    _raise(L.bgabp_shard_set_peers(h, P, rank, lower, layouts[rank - 1].n_local if rank > 0 else 0,
-                                   Lk.glo - layouts[rank - 1].glo if rank > 0 else 0, upper,
-                                   layouts[rank + 1].n_local if rank + 1 < P else 0,
-                                   Lk.glo - layouts[rank + 1].glo if rank + 1 < P else 0,
-                                   layouts[rank - 1].ghi - Lk.glo if rank > 0 else 0,
-                                   layouts[rank + 1].glo - Lk.glo if rank + 1 < P else Lk.n_local,
-                                   (C.c_void_p * P)(*slot_ptrs)), "set peers")
-    shard.begin(opt, b_inf)  # zeroes this rank's buffers and slots
-    torch.cuda.synchronize()
-    dist.barrier()  # nobody stores into a peer before every peer has been reset
-    t, cap = 1, opt.max_iter + 2
-    done = shard.done()
+    s = IpcSolve(shard, layouts, host_barrier)
+    s.connect()
     try:
+        s.begin(opt, b_inf)
+        t, cap = 1, opt.max_iter + 2
+        done = s.done()
         while not done and t <= cap:
-            _raise(L.bgabp_shard_p2p_compute(h), "p2p compute")
-            if host_barrier:
-                torch.cuda.synchronize()
-                dist.barrier()
-            _raise(L.bgabp_shard_p2p_decide(h, 1), "p2p decide")
+            s.steps(1)
             t += 1
             if t % poll_every == 0 or t > cap or host_barrier:
-                done = shard.done()
-        out = shard.end(opt.max_iter)
+                done = s.done()
+        out = s.end()
     finally:
-        torch.cuda.synchronize()
-        dist.barrier()  # every peer is done storing before the mappings go
-        for p in opened:
-            L.bgabp_ipc_close(C.c_void_p(p))
+        s.close()
     return out
