@@ -1,5 +1,6 @@
 // Host side of the pipelined lexicographic sweep (seq_kernels.cuh).
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "engine.h"
@@ -87,8 +88,20 @@ void Engine::launch_pipe(const double* b, double* x, int t0, int nsweeps, bool s
     // 64 sweeps ahead of the stop decision; a deeper gate or a register cap (more resident blocks,
     // with spills) measured no faster / slower on 2048^2 (0.39 ms per iteration)
     Q.gate = kPipeR;
+    const bool uni = dia.uniform != 0 && getenv("BGABP_PIPE_NOUNI") == nullptr;
+    static const int pipe_minb = getenv("BGABP_PIPE_MINB") ? atoi(getenv("BGABP_PIPE_MINB")) : 1;
+    if (uni) {
+        for (int q = 0; q < 4; ++q) Q.cu[q] = dia.cu[q];
+        Q.du = dia.du;
+    }
     if (solve) {
-        if (symmetric) {
+        if (uni && pipe_minb == 16) {  // experiment: register cap for 16 resident warps per SM
+            if (delta) k_seq_pipe<true, true, true, true, 16><<<grid, 32, 0, st>>>(Q);
+            else k_seq_pipe<false, true, true, true, 16><<<grid, 32, 0, st>>>(Q);
+        } else if (uni) {  // constant stencil (config 2): no coefficient / diagonal loads
+            if (delta) k_seq_pipe<true, true, true, true><<<grid, 32, 0, st>>>(Q);
+            else k_seq_pipe<false, true, true, true><<<grid, 32, 0, st>>>(Q);
+        } else if (symmetric) {
             if (delta) k_seq_pipe<true, true, true><<<grid, 32, 0, st>>>(Q);
             else k_seq_pipe<false, true, true><<<grid, 32, 0, st>>>(Q);
         } else {
@@ -96,7 +109,8 @@ void Engine::launch_pipe(const double* b, double* x, int t0, int nsweeps, bool s
             else k_seq_pipe<false, true, false><<<grid, 32, 0, st>>>(Q);
         }
     } else {
-        k_seq_pipe<false, false, true><<<grid, 32, 0, st>>>(Q);
+        if (uni) k_seq_pipe<false, false, true, true><<<grid, 32, 0, st>>>(Q);
+        else k_seq_pipe<false, false, true><<<grid, 32, 0, st>>>(Q);
         k_pipe_failure<<<1, 1, 0, st>>>(d_ctrl, d_pred, t0, nsweeps);
     }
     ck(cudaGetLastError(), "pipelined sequential sweeps");

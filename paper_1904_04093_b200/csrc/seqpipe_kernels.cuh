@@ -49,6 +49,9 @@ struct PipeP {
     const int* order;  // ticket -> (sweep - t0) << 12 | strip, in order of 2 * sweep + strip
     int strips, t0, nsweeps;
     int gate;  // sweeps that may run ahead of the last stop decision (<= kPipeR)
+    // constant-coefficient stencil (DiaP::uniform: bit-symmetric, one out-edge coefficient per
+    // slot, one diagonal): the UNI kernels take cu / du instead of loading c / rowv / diag
+    double cu[4], du;
 };
 
 __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
@@ -91,7 +94,7 @@ struct PipeNode {
     double2 old[4];
 };
 
-template <bool DELTA, bool SOLVE, bool SYMR>
+template <bool DELTA, bool SOLVE, bool SYMR, bool UNI>
 __device__ __forceinline__ void pipe_load(PipeNode& o, const PipeP& Q, int j, bool valid) {
     o.mk = 0u;
     o.b = o.d = 0.0;
@@ -107,13 +110,13 @@ __device__ __forceinline__ void pipe_load(PipeNode& o, const PipeP& Q, int j, bo
     o.mk = __ldg(P.mask + j);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        o.cc[q] = __ldg(P.c + q * n + j);
+        o.cc[q] = UNI ? Q.cu[q] : __ldg(P.c + q * n + j);
         if (SOLVE && !SYMR) o.rv[q] = __ldg(Q.rowv + q * n + j);
     }
     o.inE = __ldcg(Q.msg + 2 * n + j);  // written by sweep t-1 on another SM
     o.inN = __ldcg(Q.msg + 3 * n + j);
     o.b = __ldg(Q.b + j);
-    o.d = __ldg(P.diag + j);
+    o.d = UNI ? Q.du : __ldg(P.diag + j);
     if (DELTA) {  // previous-sweep values of this node's four out-slots (only this node writes them)
         const long long nb[4] = {(long long)j - P.nx, (long long)j - 1, (long long)j + 1, (long long)j + P.nx};
 #pragma unroll
@@ -169,8 +172,9 @@ __device__ __forceinline__ void pipe_decide(volatile Ctrl* c, double* history, i
     }
 }
 
-// SYMR: A is bit-symmetric, so the residual's row coefficients are the out-edge coefficients
-template <bool DELTA, bool SOLVE, bool SYMR, int MINB = 1>
+// SYMR: A is bit-symmetric, so the residual's row coefficients are the out-edge coefficients;
+// UNI (implies SYMR): constant stencil, coefficients and diagonal from Q.cu / Q.du
+template <bool DELTA, bool SOLVE, bool SYMR, bool UNI = false, int MINB = 1>
 static __global__ void __launch_bounds__(32, MINB) k_seq_pipe(PipeP Q) {
     constexpr unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x;
@@ -236,7 +240,7 @@ static __global__ void __launch_bounds__(32, MINB) k_seq_pipe(PipeP Q) {
         __syncwarp();
     }
     PipeNode cur, nxt;
-    pipe_load<DELTA, SOLVE, SYMR>(cur, Q, r * nx, row_ok && lane == 0);
+    pipe_load<DELTA, SOLVE, SYMR, UNI>(cur, Q, r * nx, row_ok && lane == 0);
     double2 west = make_double2(0.0, 0.0), north_out = make_double2(0.0, 0.0);
     double dmax = 0.0, rmax = 0.0;
     // own-row history for the residual two columns behind: x, b, diag, mask, A row of c-1 / c-2
@@ -268,20 +272,22 @@ static __global__ void __launch_bounds__(32, MINB) k_seq_pipe(PipeP Q) {
                 __syncwarp();
             }
         }
-        pipe_load<DELTA, SOLVE, SYMR>(nu, Q, j + 1, row_ok && c + 1 >= 0 && c + 1 < nx);
+        pipe_load<DELTA, SOLVE, SYMR, UNI>(nu, Q, j + 1, row_ok && c + 1 >= 0 && c + 1 < nx);
         {
             const int cp = c + kSeqPrefetch;
             if (row_ok && cp >= 0 && cp < nx && (cp & 7) == 0) {
                 const size_t jp = (size_t)r * nx + cp, nn = (size_t)n;
                 prefetch_l1(P.mask + jp);
+                if (!UNI) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) prefetch_l1(P.c + q * nn + jp);
+                    for (int q = 0; q < 4; ++q) prefetch_l1(P.c + q * nn + jp);
+                }
                 if (SOLVE && !SYMR) {
 #pragma unroll
                     for (int q = 0; q < 4; ++q) prefetch_l1(Q.rowv + q * nn + jp);
                 }
                 prefetch_l1(Q.b + jp);
-                prefetch_l1(P.diag + jp);
+                if (!UNI) prefetch_l1(P.diag + jp);
             }
         }
         double2 south;
@@ -402,9 +408,10 @@ static __global__ void __launch_bounds__(32, MINB) k_seq_pipe(PipeP Q) {
                     const size_t jp = (size_t)(r0 - 1) * nx + cn;
                     pmk = __ldg(P.mask + jp);
                     pb = __ldg(Q.b + jp);
-                    pd = __ldg(P.diag + jp);
+                    pd = UNI ? Q.du : __ldg(P.diag + jp);
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) prv[q] = __ldg((SYMR ? P.c : Q.rowv) + (size_t)q * n + jp);
+                    for (int q = 0; q < 4; ++q)
+                        prv[q] = UNI ? Q.cu[q] : __ldg((SYMR ? P.c : Q.rowv) + (size_t)q * n + jp);
                 }
             }
         }

@@ -3,7 +3,8 @@ words must reproduce the single-process solve bit for bit.
 
 CPU: the driver (paper_1904_04093_b200.shard) over numpy shards (tests/shard_emu.py), in one
 process and with world_size 2 over gloo, against the oracle's GabpEngine::solve.
-GPU: the driver over CUDA shards in one process against the single-engine CUDA solve.
+GPU: the driver over CUDA shards (one process, peer memory, CUDA IPC) against the CPU oracle directly
+and against the single-engine CUDA solve.
 """
 import os
 import socket
@@ -194,7 +195,7 @@ def test_gloo_world2_matches_oracle(orc, name, owner):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", sorted(PROBLEMS))
-def test_gpu_shards_match_single_engine(name):
+def test_gpu_shards_match_single_engine(orc, name):
     from paper_1904_04093_b200.gabp import GabpEngine, Layout
     from paper_1904_04093_b200.gabp import Schedule as GSchedule
     from paper_1904_04093_b200.shard import GpuShard
@@ -206,12 +207,13 @@ def test_gpu_shards_match_single_engine(name):
     status, its, detail, xs, hist = sharded_solve(shards, layouts, [0] * count, 1, _r0(b), opt)
     rep = GabpEngine(A, Layout.Dia).solve(b, GSchedule.parallel_flood(), opt)
     _assert_same(rep, status, its, detail, _gather(layouts, xs), hist)
+    _assert_same(_oracle_solve(orc, A, b, opt), status, its, detail, _gather(layouts, xs), hist)
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", sorted(PROBLEMS))
 @pytest.mark.parametrize("mode", ["event", "spin", "graph"])
-def test_gpu_peer_shards_match_single_engine(name, mode):
+def test_gpu_peer_shards_match_single_engine(orc, name, mode):
     """The peer-memory step (halo messages and x stored by the step kernel into the neighbour's
     buffers, stop words into every shard's slots; bgabp_shard_p2p_*) against the single engine."""
     from paper_1904_04093_b200.gabp import GabpEngine, Layout
@@ -226,10 +228,11 @@ def test_gpu_peer_shards_match_single_engine(name, mode):
                                                       graph=mode == "graph")
     rep = GabpEngine(A, Layout.Dia).solve(b, GSchedule.parallel_flood(), opt)
     _assert_same(rep, status, its, detail, _gather(layouts, xs), hist)
+    _assert_same(_oracle_solve(orc, A, b, opt), status, its, detail, _gather(layouts, xs), hist)
 
 
 @pytest.mark.gpu
-def test_gpu_peer_shards_config2_slab():
+def test_gpu_peer_shards_config2_slab(orc):
     """Eight peer-connected shards of a 512 x 512 Poisson system (the config-2 operator), 300
     iterations: bit-identical to the single engine."""
     import paper_1904_04093_b200 as g
@@ -242,6 +245,7 @@ def test_gpu_peer_shards_config2_slab():
     status, its, detail, xs, hist = sharded_solve_p2p(shards, layouts, _r0(b), opt, graph=True)
     rep = g.GabpEngine(A).solve(b, g.Schedule.parallel_flood(), opt)
     _assert_same(rep, status, its, detail, _gather(layouts, xs), hist)
+    _assert_same(_oracle_solve(orc, A, b, opt), status, its, detail, _gather(layouts, xs), hist)
 
 
 def _ipc_worker(rank, world, port, name, q):
@@ -268,7 +272,7 @@ def _ipc_worker(rank, world, port, name, q):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", ["grid5_sym", "grid5_nonsym", "grid7"])
-def test_gpu_ipc_ranks_match_single_engine(name):
+def test_gpu_ipc_ranks_match_single_engine(orc, name):
     """Two processes, one shard each, neighbour buffers and slot arrays mapped with CUDA IPC."""
     import torch.multiprocessing as mp
     from paper_1904_04093_b200.gabp import GabpEngine, Layout
@@ -293,3 +297,4 @@ def test_gpu_ipc_ranks_match_single_engine(name):
     assert outs[0][1:4] == outs[1][1:4]
     rep = GabpEngine(A, Layout.Dia).solve(b, GSchedule.parallel_flood(), opt)
     _assert_same(rep, outs[0][1], outs[0][2], outs[0][3], _gather(layouts, xs), outs[0][5])
+    _assert_same(_oracle_solve(orc, A, b, opt), outs[0][1], outs[0][2], outs[0][3], _gather(layouts, xs), outs[0][5])

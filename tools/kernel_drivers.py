@@ -44,7 +44,7 @@ def main():
     ap.add_argument("family")
     ap.add_argument("--n", type=int, default=0)
     a = ap.parse_args()
-    f = a.family
+    f = a.family.rstrip("0123456789") if a.family not in ("flood3",) else a.family  # mg2.. = mg (ncu passes)
     if f in ("flood", "flood3"):
         P = g.config_problem(2 if f == "flood" else 3, size=a.n)
         print(f, steps(g.GabpEngine(P.A), P.b, g.Schedule.parallel_flood(), 40))

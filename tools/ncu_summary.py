@@ -1,6 +1,6 @@
 """Summarise an ncu capture / launch list into profiles/ (JSON).
 
-    python tools/ncu_summary.py report <file.ncu-rep> <out.json> <algorithmic_bytes> [note]
+    python tools/ncu_summary.py report <file.ncu-rep | raw.csv> <out.json> <algorithmic_bytes | 0> [note]
     python tools/ncu_summary.py launches <launches.csv> <out.json>
 """
 import csv
@@ -16,31 +16,53 @@ def _scale(unit):
             "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3}.get(unit, 1.0)
 
 
-def report(path, out, alg_bytes, note=""):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+def _raw_rows(path):
+    """Rows of `ncu -i <rep> --page raw --csv` (a .ncu-rep is exported first; a .csv is read as is)."""
+    if path.endswith(".ncu-rep"):
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    else:
+        raw = open(path).read()
     rows = list(csv.reader(io.StringIO(raw)))
-    h, u, r = rows[0], rows[1], rows[2]
+    return rows[0], rows[1], rows[2:]
 
+
+def _one(h, u, r, alg_bytes, peak_gbs):
     def g(k):
-        return float(r[h.index(k)]) * _scale(u[h.index(k)]) if k in h else None
+        return float(r[h.index(k)].replace(",", "")) * _scale(u[h.index(k)]) if k in h else None
+
+    def f(k):
+        return float(r[h.index(k)].replace(",", "")) if k in h else None
 
     stalls = {k.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", ""): float(r[h.index(k)])
               for k in h if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio")}
     stalls = {k: v for k, v in sorted(stalls.items(), key=lambda kv: -kv[1]) if v > 0.05}
     rd, wr = g("dram__bytes_read.sum"), g("dram__bytes_write.sum")
     dur = g("gpu__time_duration.sum")
-    res = {"kernel": r[h.index("Kernel Name")], "note": note, "duration_us": dur * 1e6,
+    res = {"kernel": r[h.index("Kernel Name")], "duration_us": dur * 1e6,
            "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
-           "algorithmic_bytes_per_launch": alg_bytes, "traffic_over_algorithmic": (rd + wr) / alg_bytes,
            "dram_GBps_during_kernel": (rd + wr) / dur / 1e9,
-           "dram_throughput_pct_of_peak": float(r[h.index("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")]),
-           "registers_per_thread": float(r[h.index("launch__registers_per_thread")]),
-           "warps_active_pct": float(r[h.index("sm__warps_active.avg.pct_of_peak_sustained_active")]),
-           "issue_active_pct": float(r[h.index("smsp__issue_active.avg.pct_of_peak_sustained_active")]),
-           "fp64_pipe_pct": float(r[h.index("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active")]),
-           "instructions": float(r[h.index("smsp__inst_executed.sum")]), "stall_reasons_per_issue": stalls}
+           "dram_frac_of_measured_peak": (rd + wr) / dur / 1e9 / peak_gbs,
+           "dram_throughput_pct_of_peak": f("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+           "registers_per_thread": f("launch__registers_per_thread"),
+           "block_size": f("launch__block_size"), "grid_size": f("launch__grid_size"),
+           "warps_active_pct": f("sm__warps_active.avg.pct_of_peak_sustained_active"),
+           "issue_active_pct": f("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+           "l2_hit_rate_pct": f("lts__t_sector_hit_rate.pct"),
+           "fp64_pipe_pct": f("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
+           "instructions": f("smsp__inst_executed.sum"), "stall_reasons_per_issue": stalls}
+    if alg_bytes:
+        res.update({"algorithmic_bytes_per_launch": alg_bytes, "traffic_over_algorithmic": (rd + wr) / alg_bytes,
+                    "algorithmic_GBps": alg_bytes / dur / 1e9, "algorithmic_frac_of_measured_peak": alg_bytes / dur / 1e9 / peak_gbs})
+    return res
+
+
+def report(path, out, alg_bytes, note="", peak_gbs=6542.4):
+    """Every captured launch of a `--set full` report (or its raw CSV export)."""
+    h, u, rows = _raw_rows(path)
+    launches_ = [_one(h, u, r, alg_bytes, peak_gbs) for r in rows if r and r[0] != ""]
+    res = {"source": path, "note": note, "peak_GBps": peak_gbs, "launches": launches_}
     json.dump(res, open(out, "w"), indent=1)
-    print(json.dumps(res, indent=1))
+    print(json.dumps(res, indent=1)[:2500])
 
 
 def launches(path, out):
