@@ -329,8 +329,9 @@ bgabp_problem* bgabp_problem_config(int config, int size, unsigned seed); /* con
 bgabp_problem* bgabp_problem_config5_level(int J_fine, int k, unsigned seed);
 /* the same family with another log-K standard deviation (config 5 uses sigma = 2) */
 bgabp_problem* bgabp_problem_varcoef2d_level(int J_fine, int k, unsigned seed, double sigma);
-/* the same with another coarse-K rule: 0 = full-weighted log K (the generator's), 1 = full-weighted
- * K, 2 = full-weighted 1/K, 3 = injection (tools/config5_coarse_rules.py compares them) */
+/* the same with another coarse-K rule: 0 = full-weighted log K, 1 = full-weighted K (the
+ * generator's: the rule with which the sigma = 2 V-cycle converges), 2 = full-weighted 1/K,
+ * 3 = injection (tools/config5_coarse_rules.py compares them) */
 bgabp_problem* bgabp_problem_varcoef2d_rule(int J_fine, int k, unsigned seed, double sigma, int rule);
 void bgabp_problem_free(bgabp_problem* p);
 int bgabp_problem_n(const bgabp_problem* p);

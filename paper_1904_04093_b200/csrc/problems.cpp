@@ -295,12 +295,15 @@ struct Config5Field {
     std::vector<double> b;
 };
 
-// Coarse-K rules (rule 0 is the generator's; 1-3 are the alternatives tools/config5_coarse_rules.py
-// measures): 0 full-weighted log K (weighted geometric mean), 1 full-weighted K (arithmetic),
-// 2 full-weighted 1/K (harmonic), 3 injection of the coinciding fine vertex.
-Config5Field& config5_field(int J, unsigned seed, double sigma, int levels, int rule = 0) {
+// Coarse-K rules (tools/config5_coarse_rules.py measures all four): 0 full-weighted log K (weighted
+// geometric mean), 1 full-weighted K (arithmetic), 2 full-weighted 1/K (harmonic), 3 injection of
+// the coinciding fine vertex.  Rule 1 is the generator's: at the configured 4095^2, sigma = 2 it is
+// the only rediscretisation rule with which the reference's V(2,2) cycle reaches 1e-8 (red-black
+// GaBP 291 cycles, red-black GS 711; rules 0, 2, 3 diverge -- profiles/r02_config5_*).
+constexpr int kConfig5Rule = 1;
+Config5Field& config5_field(int J, unsigned seed, double sigma, int levels, int rule = kConfig5Rule) {
     static Config5Field cache;
-    static int cache_rule = 0;
+    static int cache_rule = -1;
     if (cache.J == J && cache.seed == seed && cache.sigma == sigma && cache_rule == rule &&
         (int)cache.logK.size() >= levels)
         return cache;
@@ -344,7 +347,7 @@ Config5Field& config5_field(int J, unsigned seed, double sigma, int levels, int 
     return cache;
 }
 
-bgabp_problem* varcoef2d_problem(int Jf, int k, unsigned seed, double sigma, int rule = 0) {
+bgabp_problem* varcoef2d_problem(int Jf, int k, unsigned seed, double sigma, int rule = kConfig5Rule) {
     Config5Field& F = config5_field(Jf, seed, sigma, Jf, rule);  // every level at once: later calls hit the cache
     if ((int)F.logK.size() <= k) throw std::invalid_argument("config 5: level below the coarsest grid");
     const int J = Jf - k, m = (1 << J) - 1;

@@ -238,31 +238,32 @@ def test_acceptance_cycle_bands():
     assert st == g.SolveStatus.Converged and 10 <= it <= 20
 
 
-@pytest.mark.parametrize("sigma,sm,expect", [(2.0, S.GabpRedBlack, g.SolveStatus.Diverged),
-                                             (2.0, S.GsRedBlack, None),
-                                             (1.0, S.GabpRedBlack, g.SolveStatus.Converged),
-                                             (1.0, S.GsRedBlack, g.SolveStatus.Converged),
-                                             (1.0, S.GabpFlood, None)])
+@pytest.mark.parametrize("sigma,sm,expect", [(2.0, S.GabpRedBlack, (g.SolveStatus.Converged, 202)),
+                                             (2.0, S.GsRedBlack, (g.SolveStatus.Converged, 381)),
+                                             (1.0, S.GabpRedBlack, (g.SolveStatus.Converged, 28)),
+                                             (1.0, S.GsRedBlack, (g.SolveStatus.Converged, 34)),
+                                             (1.0, S.GabpFlood, (g.SolveStatus.MaxIter, 40))])
 def test_config5_family_matches_restatement(orc, ref, sigma, sm, expect):
-    """BASELINE.json config 5 recipe at J=8 (255^2 -> 31^2, 4 levels), V(2,2) to 1e-8.  With the
-    configured log-K std 2 the reference's V-cycle (rediscretised operators, bilinear transfers)
-    diverges with every smoother; std 1 converges.  GPU and CPU must agree either way."""
+    """BASELINE.json config 5 recipe at J=8 (255^2 -> 31^2, 4 levels), V(2,2) to 1e-8, coarse K by
+    arithmetic full weighting (the generator's rule): with the configured log-K std 2 red-black
+    GaBP converges in 202 cycles and red-black GS in 381 (the same on the CPU restatement over
+    the reference's engine); the flood smoother stalls.  GPU and CPU must agree bit for bit."""
     O = _oracle_for(ref, orc)
     from oracle.oracle import Csr
     levels = [g.config5_level(8, k, sigma=sigma) for k in range(4)]
     b = levels[0].b
     tol = 1e-8 * np.abs(b).max()
     h = g.Hierarchy.from_levels([p.A for p in levels], [p.nx for p in levels], sm)
-    got = g.mg_solve(h, g.CycleSpec(2, 2, sm), b, g.MgSolveOptions(tol=tol, max_cycles=40))
+    cap = 40 if sm == S.GabpFlood else 400
+    got = g.mg_solve(h, g.CycleSpec(2, 2, sm), b, g.MgSolveOptions(tol=tol, max_cycles=cap))
     oh = O.hierarchy([Csr(p.A.n, p.A.row_offsets, p.A.col_indices, p.A.values) for p in levels],
                      [p.nx for p in levels], int(sm))
-    want = oh.solve(2, 2, b, tol=tol, max_cycles=40)
+    want = oh.solve(2, 2, b, tol=tol, max_cycles=cap)
     assert (int(got.status), got.iterations, got.detail) == (want.status, want.iterations, want.detail)
     assert got.flop_estimate == want.flop_estimate
     assert got.residual_history.tobytes() == want.residual_history.tobytes()
     assert got.solution.tobytes() == want.solution.tobytes()
-    if expect is not None:
-        assert got.status == expect
+    assert (got.status, got.iterations) == expect
 
 
 @pytest.mark.parametrize("fine_diag,sm,pre,post", [(1.0, S.GabpFlood, 1, 2), (1.0, S.GabpFlood, 2, 2),
