@@ -88,6 +88,10 @@ void Engine::launch_pipe(const double* b, double* x, int t0, int nsweeps, bool s
     // 64 sweeps ahead of the stop decision; a deeper gate or a register cap (more resident blocks,
     // with spills) measured no faster / slower on 2048^2 (0.39 ms per iteration)
     Q.gate = kPipeR;
+    static const int pub = getenv("BGABP_PIPE_PUB") ? atoi(getenv("BGABP_PIPE_PUB")) : kSeqPublish;
+    static const int gate = getenv("BGABP_PIPE_GATE") ? atoi(getenv("BGABP_PIPE_GATE")) : kPipeR;
+    Q.pub = pub;
+    Q.gate = std::min(gate, kPipeR);
     const bool uni = dia.uniform != 0 && getenv("BGABP_PIPE_NOUNI") == nullptr;
     static const int pipe_minb = getenv("BGABP_PIPE_MINB") ? atoi(getenv("BGABP_PIPE_MINB")) : 1;
     if (uni) {
