@@ -483,29 +483,10 @@ void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bga
         for (int len = kChunk; len >= 1; len >>= 1) chunk_graph(len);
 }
 
-// Launch with programmatic stream serialisation (the kernel starts with griddep_wait): the next
-// grid is scheduled while this one drains, hiding the launch gap between the fused step and its
-// decision kernel.  BGABP_PDL=0 turns it off (A/B).
-template <typename... KA, typename... A>
-static void pdl_launch(cudaStream_t st, unsigned grid, unsigned block, void (*k)(KA...), A... args) {
-    static const bool on = !(getenv("BGABP_PDL") && std::string(getenv("BGABP_PDL")) == "0");
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(block);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = on ? 1 : 0;
-    ck(cudaLaunchKernelEx(&cfg, k, args...), "programmatic launch");
-}
-
 void Engine::enqueue_step() {
     if (solve_fused) {
         enqueue_fused_kernel();
-        pdl_launch(st, 1, kSpread, k_solve_decide_lag2, d_ctrl, d_hist, d_spread);
+        k_solve_decide_lag2<<<1, kSpread, 0, st>>>(d_ctrl, d_hist, d_spread);
         return;
     }
     enqueue_step_other();
@@ -553,21 +534,21 @@ void Engine::enqueue_fused_kernel() {
         launch_sharded_step<SS_, MB_, DF_>(*this, g, dl);                                                          \
     } else if (damping != 0.0) {  /* damped messages: the general-coefficient step (c arrays exist) */           \
         if (symmetric) {                                                                                           \
-            if (dl) pdl_launch(st, g, 256, k_flood_solve_dia<SS_, true, true, MB_, DF_, true, false, false, false, true>, dia, (const double*)solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread, PeerP{}); \
-            else pdl_launch(st, g, 256, k_flood_solve_dia<SS_, false, true, MB_, DF_, true, false, false, false, true>, dia, (const double*)solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread, PeerP{}); \
+            if (dl) k_flood_solve_dia<SS_, true, true, MB_, DF_, true, false, false, false, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
+            else k_flood_solve_dia<SS_, false, true, MB_, DF_, true, false, false, false, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
         } else {                                                                                                   \
-            if (dl) pdl_launch(st, g, 256, k_flood_solve_dia<SS_, true, false, MB_, DF_, true, false, false, false, true>, dia, (const double*)solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread, PeerP{}); \
-            else pdl_launch(st, g, 256, k_flood_solve_dia<SS_, false, false, MB_, DF_, true, false, false, false, true>, dia, (const double*)solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread, PeerP{}); \
+            if (dl) k_flood_solve_dia<SS_, true, false, MB_, DF_, true, false, false, false, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
+            else k_flood_solve_dia<SS_, false, false, MB_, DF_, true, false, false, false, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
         }                                                                                                          \
     } else if (dia.uniform) {                                                                                      \
-        if (dl) pdl_launch(st, g, 256, k_flood_solve_dia<SS_, true, true, MBU_, DFU_, true, true>, dia, (const double*)solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread, PeerP{}); \
-        else pdl_launch(st, g, 256, k_flood_solve_dia<SS_, false, true, MBU_, DFU_, true, true>, dia, (const double*)solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread, PeerP{}); \
+        if (dl) k_flood_solve_dia<SS_, true, true, MBU_, DFU_, true, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
+        else k_flood_solve_dia<SS_, false, true, MBU_, DFU_, true, true><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
     } else if (symmetric) {                                                                                        \
-        if (dl) pdl_launch(st, g, 256, k_flood_solve_dia<SS_, true, true, MB_, DF_>, dia, (const double*)solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread, PeerP{}); \
-        else pdl_launch(st, g, 256, k_flood_solve_dia<SS_, false, true, MB_, DF_>, dia, (const double*)solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread, PeerP{}); \
+        if (dl) k_flood_solve_dia<SS_, true, true, MB_, DF_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
+        else k_flood_solve_dia<SS_, false, true, MB_, DF_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
     } else {                                                                                                       \
-        if (dl) pdl_launch(st, g, 256, k_flood_solve_dia<SS_, true, false, MB_, DF_>, dia, (const double*)solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread, PeerP{}); \
-        else pdl_launch(st, g, 256, k_flood_solve_dia<SS_, false, false, MB_, DF_>, dia, (const double*)solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread, PeerP{}); \
+        if (dl) k_flood_solve_dia<SS_, true, false, MB_, DF_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
+        else k_flood_solve_dia<SS_, false, false, MB_, DF_><<<g, 256, 0, st>>>(dia, solve_b, d_msg[0], d_msg[1], d_xf, d_xf + n, d_ctrl, d_spread); \
     }
         if (timed_events) ck(cudaEventRecord((*timed_events)[2 * timed_index], st), "event");
         // (resident blocks, deferred x loads) per slot count, from tools/exp_flood.cu on the B200:

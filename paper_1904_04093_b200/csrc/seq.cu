@@ -85,24 +85,22 @@ void Engine::launch_pipe(const double* b, double* x, int t0, int nsweeps, bool s
     Q.nsweeps = nsweeps;
     ck(cudaMemsetAsync(d_pint, 0, sizeof(int), st), "ticket");
     const dim3 grid((unsigned)((long long)nsweeps * pipe_strips));
-    // 64 sweeps ahead of the stop decision; a deeper gate or a register cap (more resident blocks,
-    // with spills) measured no faster / slower on 2048^2 (0.39 ms per iteration)
+    // 64 sweeps ahead of the stop decision.  Measured on 2048^2 (constant-stencil variant, 0.31 ms
+    // per iteration) and no faster: a 128-slot ring, register caps of 168 / 128 (12 / 16 warps
+    // per SM, with spills: 0.34 / 0.36 ms), publishing every 4 / 16 / 32 columns, L1 prefetch
+    // distances 0-40, L2 prefetch of the east / north message lines, dependency flags polled one
+    // step ahead with the boundary batches loaded a step before staging, and (unsafely) relaxed
+    // progress stores without the release fence (-3 %).  Two pipelines on one GPU each run at half
+    // speed: the kernel is bound by resident warps x per-step latency (8 warps per SM at 214
+    // registers, ~640 instructions per warp step at ~8 cycles each), see DESIGN.md 4
     Q.gate = kPipeR;
-    static const int pub = getenv("BGABP_PIPE_PUB") ? atoi(getenv("BGABP_PIPE_PUB")) : kSeqPublish;
-    static const int gate = getenv("BGABP_PIPE_GATE") ? atoi(getenv("BGABP_PIPE_GATE")) : kPipeR;
-    Q.pub = pub;
-    Q.gate = std::min(gate, kPipeR);
-    const bool uni = dia.uniform != 0 && getenv("BGABP_PIPE_NOUNI") == nullptr;
-    static const int pipe_minb = getenv("BGABP_PIPE_MINB") ? atoi(getenv("BGABP_PIPE_MINB")) : 1;
+    const bool uni = dia.uniform != 0 && getenv("BGABP_PIPE_NOUNI") == nullptr;  // NOUNI: A/B
     if (uni) {
         for (int q = 0; q < 4; ++q) Q.cu[q] = dia.cu[q];
         Q.du = dia.du;
     }
     if (solve) {
-        if (uni && pipe_minb == 16) {  // experiment: register cap for 16 resident warps per SM
-            if (delta) k_seq_pipe<true, true, true, true, 16><<<grid, 32, 0, st>>>(Q);
-            else k_seq_pipe<false, true, true, true, 16><<<grid, 32, 0, st>>>(Q);
-        } else if (uni) {  // constant stencil (config 2): no coefficient / diagonal loads
+        if (uni) {  // constant stencil (config 2): no coefficient / diagonal loads
             if (delta) k_seq_pipe<true, true, true, true><<<grid, 32, 0, st>>>(Q);
             else k_seq_pipe<false, true, true, true><<<grid, 32, 0, st>>>(Q);
         } else if (symmetric) {

@@ -52,7 +52,6 @@ struct PipeP {
     // constant-coefficient stencil (DiaP::uniform: bit-symmetric, one out-edge coefficient per
     // slot, one diagonal): the UNI kernels take cu / du instead of loading c / rowv / diag
     double cu[4], du;
-    int pub;  // progress is published every `pub` columns (a power of two; kSeqPublish by default)
 };
 
 __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
@@ -416,7 +415,7 @@ static __global__ void __launch_bounds__(32, MINB) k_seq_pipe(PipeP Q) {
                 }
             }
         }
-        if (act && last_lane && ((c & (Q.pub - 1)) == Q.pub - 1 || c == nx - 1))
+        if (act && last_lane && ((c % kSeqPublish) == kSeqPublish - 1 || c == nx - 1))
             st_release_u64(myprog, mytag | (unsigned)(c + 1));  // lane 30's x: ordered by the step's __syncwarp
         __syncwarp();
     };
