@@ -92,7 +92,9 @@ void Engine::launch_pipe(const double* b, double* x, int t0, int nsweeps, bool s
     // step ahead with the boundary batches loaded a step before staging, and (unsafely) relaxed
     // progress stores without the release fence (-3 %).  Two pipelines on one GPU each run at half
     // speed: the kernel is bound by resident warps x per-step latency (8 warps per SM at 214
-    // registers, ~640 instructions per warp step at ~8 cycles each), see DESIGN.md 4
+    // registers, ~640 instructions per warp step at ~8 cycles each), see DESIGN.md 4.  A
+    // 164-register build of the constant-stencil kernel (no copies of the stencil constants, no
+    // spills: 12 warps per SM) ran 0.339 ms: the SM's warp-step rate stays at ~2.9 per us.
     Q.gate = kPipeR;
     const bool uni = dia.uniform != 0 && getenv("BGABP_PIPE_NOUNI") == nullptr;  // NOUNI: A/B
     if (uni) {
