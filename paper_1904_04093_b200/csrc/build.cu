@@ -161,12 +161,20 @@ void Engine::build(int n_, const int* ro_, const int* ci_, const double* v_, int
 
 // the matrix in HBM (row offsets, columns, values) and the DIA arrays derived from it on the device
 void Engine::build_dia_device(const int* ro_, const int* ci_, const double* v_) {
+    Phase phase;
+    auto sync_phase = [&](const char* what) {
+        if (!phase.on) return;
+        ck(cudaStreamSynchronize(st), "sync");
+        phase(what);
+    };
     d_ro = static_cast<int*>(dalloc(sizeof(int) * ((size_t)n + 1)));
     d_ci = static_cast<int*>(dalloc(sizeof(int) * (size_t)std::max<long long>(nnz, 1)));
     d_val = static_cast<double*>(dalloc(sizeof(double) * (size_t)std::max<long long>(nnz, 1)));
+    sync_phase("  dia: csr allocations");
     upload_host(d_ro, ro_, sizeof(int) * ((size_t)n + 1));
     upload_host(d_ci, ci_, sizeof(int) * (size_t)nnz);
     upload_host(d_val, v_, sizeof(double) * (size_t)nnz);
+    sync_phase("  dia: csr upload");
     uint32_t* mask = static_cast<uint32_t*>(dalloc(sizeof(uint32_t) * (size_t)std::max(n, 1)));
     double* c = static_cast<double*>(dalloc(sizeof(double) * (size_t)std::max<long long>(nslots, 1)));
     double* rowv = static_cast<double*>(dalloc(sizeof(double) * (size_t)std::max<long long>(nslots, 1)));
@@ -174,6 +182,7 @@ void Engine::build_dia_device(const int* ro_, const int* ci_, const double* v_) 
     ck(cudaMemsetAsync(mask, 0, sizeof(uint32_t) * (size_t)std::max(n, 1), st), "memset");
     ck(cudaMemsetAsync(c, 0, sizeof(double) * (size_t)std::max<long long>(nslots, 1), st), "memset");
     ck(cudaMemsetAsync(rowv, 0, sizeof(double) * (size_t)std::max<long long>(nslots, 1), st), "memset");
+    sync_phase("  dia: layout allocations");
     DiaOffs o{};
     o.S = S;
     for (int s = 0; s < S; ++s) {
@@ -196,6 +205,7 @@ void Engine::build_dia_device(const int* ro_, const int* ci_, const double* v_) 
     ck(cudaGetLastError(), "dia build");
     ck(cudaMemcpyAsync(&hf, d_f, sizeof hf, cudaMemcpyDeviceToHost, st), "D2H");
     ck(cudaStreamSynchronize(st), "dia build sync");
+    phase("  dia: fill + facts kernels");
     symmetric = hf.asym == 0u;
     grid5 = gx > 0 && hf.wrap == 0u;
     grid5_nx = gx;
