@@ -964,9 +964,20 @@ int Engine::cold_sweeps_dev(const double* r_dev, const bgabp_schedule& s, int sw
 // if max|m| is non-finite after any sweep, or if it grows more than 6.19x from sweep 20 to 30.
 bool Engine::sweeps_expand(const bgabp_schedule& s) {
     if (n == 0) return false;
+    const bool timing = getenv("BGABP_TIMING") != nullptr;
+    auto t_last = std::chrono::steady_clock::now();
+    auto phase = [&](const char* what) {
+        if (!timing) return;
+        ck(cudaStreamSynchronize(st), "sync");
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[probe] n=%d %-18s %8.2f ms\n", n, what,
+                     std::chrono::duration<double, std::milli>(now - t_last).count());
+        t_last = now;
+    };
     const bool flood = s.kind == BGABP_SCHED_FLOOD;
     const bool rbp = rb_applicable(s);
     if (rbp) rb_build(s.nx);
+    phase("layout");
     const Levels* L = (flood || rbp) ? nullptr : &levels_for(s);
     unsigned long long* d_norms = static_cast<unsigned long long*>(dalloc(sizeof(unsigned long long) * 32));
     ck(cudaMemsetAsync(d_norms, 0, sizeof(unsigned long long) * 32, st), "memset");
@@ -978,6 +989,7 @@ bool Engine::sweeps_expand(const bgabp_schedule& s) {
     ck(cudaMemsetAsync(d_e, 0, sizeof(double) * n, st), "memset");
     cur = 0;
     const unsigned gr = std::min<unsigned>(nblk(nslots), 1184);
+    phase("buffers");
     for (int k = 0; k < 30; ++k) {
         if (flood) {
             launch_flood(d_ones, d_msg[cur], d_msg[cur ^ 1], nullptr, k == 0 ? MODE_PLAIN : MODE_PLAIN_X, false);
@@ -995,6 +1007,7 @@ bool Engine::sweeps_expand(const bgabp_schedule& s) {
         k_max_abs_m<<<gr, 256, 0, st>>>(rbp ? d_rbmsg : d_msg[cur], nslots, d_norms + k);
     }
     ck(cudaGetLastError(), "probe");
+    phase("30 sweeps");
     unsigned long long hn[32];
     ck(cudaMemcpyAsync(hn, d_norms, sizeof(hn), cudaMemcpyDeviceToHost, st), "D2H");
     read_ctrl();
@@ -1003,6 +1016,7 @@ bool Engine::sweeps_expand(const bgabp_schedule& s) {
     ck(cudaStreamSynchronize(st), "sync");
     dfree(d_ones);
     dfree(d_norms);
+    phase("read back");
     if (h_ctrl->halt) return true;
     for (int k = 0; k < 30; ++k)
         if (!std::isfinite(bits2d(hn[k]))) return true;

@@ -209,6 +209,15 @@ struct Engine {
     int* d_pint = nullptr;  // [0] ticket, [1] decided
     int pipe_strips = 0, pipe_next = 1;
     std::map<int, int*> pipe_orders;  // ticket orders per batch size
+    // lane-skewed copies of the pipeline's read-only node operands (seqpipe_kernels.cuh): element
+    // (strip k, step s, lane i) = node (row 32k + i, column s - i), so the 32 lanes of a strip
+    // read 32 consecutive elements at every step
+    long long pipe_sn = 0;            // elements per skewed array (strips x (nx + 31) x 32)
+    uint32_t* d_skmask = nullptr;     // [sn]
+    double* d_skc = nullptr;          // [4][sn] out-edge coefficients (general coefficients only)
+    double* d_skrow = nullptr;        // [4][sn] row coefficients (A not bit-symmetric)
+    double* d_skdiag = nullptr;       // [sn]
+    double* d_skb = nullptr;          // [sn] b of the current launch
     void pipe_setup(bool ring);
     bool pipe_fits() const { return (n / std::max(grid5_nx, 1) + 31) / 32 + 1 < 2 * kPipeR; }
     bool solve_pipe = false;  // the sequential solve runs pipelined (else one k_seq_grid5 per sweep)

@@ -43,6 +43,25 @@ void Engine::pipe_setup(bool ring) {
         d_pint = static_cast<int*>(dalloc(sizeof(int) * 2));
     }
     if (ring && !d_xring) d_xring = static_cast<double*>(dalloc(sizeof(double) * (size_t)kPipeR * std::max(n, 1)));
+    if (!d_skb) {  // lane-skewed read-only operands, built once per handle (b: every launch)
+        const int nx = grid5_nx, ny = n / grid5_nx, sstep = nx + 31;
+        pipe_sn = (long long)strips * sstep * 32;
+        const unsigned g = std::min<unsigned>(nblk_host(pipe_sn), 148u * 16u);
+        d_skmask = static_cast<uint32_t*>(dalloc(sizeof(uint32_t) * (size_t)pipe_sn));
+        k_pipe_skew<uint32_t><<<g, 256, 0, st>>>(dia.mask, d_skmask, nx, ny, sstep, pipe_sn, 1, pipe_sn, n);
+        if (!dia.uniform || getenv("BGABP_PIPE_NOUNI")) {
+            d_skc = static_cast<double*>(dalloc(sizeof(double) * 4 * (size_t)pipe_sn));
+            d_skdiag = static_cast<double*>(dalloc(sizeof(double) * (size_t)pipe_sn));
+            k_pipe_skew<double><<<g, 256, 0, st>>>(dia.c, d_skc, nx, ny, sstep, pipe_sn, 4, pipe_sn, n);
+            k_pipe_skew<double><<<g, 256, 0, st>>>(dia.diag, d_skdiag, nx, ny, sstep, pipe_sn, 1, pipe_sn, n);
+            if (!symmetric) {
+                d_skrow = static_cast<double*>(dalloc(sizeof(double) * 4 * (size_t)pipe_sn));
+                k_pipe_skew<double><<<g, 256, 0, st>>>(dia.rowv, d_skrow, nx, ny, sstep, pipe_sn, 4, pipe_sn, n);
+            }
+        }
+        d_skb = static_cast<double*>(dalloc(sizeof(double) * (size_t)pipe_sn));
+        ck(cudaGetLastError(), "pipeline skew");
+    }
 }
 
 void Engine::pipe_reset() {
@@ -93,9 +112,22 @@ void Engine::launch_pipe(const double* b, double* x, int t0, int nsweeps, bool s
     // progress stores without the release fence (-3 %).  Two pipelines on one GPU each run at half
     // speed: the kernel is bound by resident warps x per-step latency (8 warps per SM at 214
     // registers, ~640 instructions per warp step at ~8 cycles each), see DESIGN.md 4.  A
-    // 164-register build of the constant-stencil kernel (no copies of the stencil constants, no
-    // spills: 12 warps per SM) ran 0.339 ms: the SM's warp-step rate stays at ~2.9 per us.
+    // 164-register build of the constant-stencil kernel (12 warps per SM) ran 0.339 ms, and 0.325
+    // ms with the lane-skewed operands (0.315 at 8 warps): the SM's warp-step rate stays at ~2.9
+    // per us.  The lane-skewed operands took the general-coefficient kernel 0.393 -> 0.331 ms.
     Q.gate = kPipeR;
+    {  // b of this launch in the lane-skewed layout (the multigrid smoother passes a new residual)
+        const int nx = grid5_nx, ny = n / grid5_nx;
+        Q.sstep = nx + 31;
+        Q.sslot = pipe_sn;
+        const unsigned g = std::min<unsigned>(nblk_host(pipe_sn), 148u * 16u);
+        k_pipe_skew<double><<<g, 256, 0, st>>>(b, d_skb, nx, ny, Q.sstep, pipe_sn, 1, pipe_sn, n);
+        Q.smask = d_skmask;
+        Q.sb = d_skb;
+        Q.sc = d_skc;
+        Q.sd = d_skdiag;
+        Q.srow = d_skrow;
+    }
     const bool uni = dia.uniform != 0 && getenv("BGABP_PIPE_NOUNI") == nullptr;  // NOUNI: A/B
     if (uni) {
         for (int q = 0; q < 4; ++q) Q.cu[q] = dia.cu[q];

@@ -11,6 +11,9 @@
 //   south   (t, k-1) has published column c            -- strip boundary, staged in batches
 //   east    (t-1, k) has published column c+2          -- previous sweep, same strip
 //   north   (t-1, k+1) has published column c+1        -- lane 31 only
+// The read-only node operands (mask, b, coefficients, diagonal) are read from lane-skewed copies
+// (k_pipe_skew): at every step the 32 lanes of a strip read 32 consecutive elements (one line per
+// array) instead of 32 rows' streams through L1.
 // Every write-after-read hazard of the in-place message array is ordered by these waits (a slot
 // is rewritten by sweep t+1 only after sweep t+1's node passed a point that itself waited for
 // sweep t's reader).  Messages written by other sweeps are read through L2 (ld.cg).
@@ -52,7 +55,29 @@ struct PipeP {
     // constant-coefficient stencil (DiaP::uniform: bit-symmetric, one out-edge coefficient per
     // slot, one diagonal): the UNI kernels take cu / du instead of loading c / rowv / diag
     double cu[4], du;
+    // lane-skewed read-only operands (Engine::pipe_sn): element (strip k, step s, lane i) holds
+    // node (32k + i, s - i); sstep = nx + 31 steps per strip, sslot = the per-slot stride
+    const uint32_t* smask;
+    const double *sb, *sc, *sd, *srow;
+    long long sslot;
+    int sstep;
 };
+
+// lane-skewed copy of `nslots` node arrays [q][n] -> [q][sslot] (zero where the (row, column)
+// falls outside the grid); consecutive elements are consecutive lanes of one strip step
+template <typename T>
+static __global__ void k_pipe_skew(const T* __restrict__ src, T* __restrict__ dst, int nx, int ny, int sstep,
+                                   long long total, int nslots, long long sslot, long long n) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long per = (long long)sstep * 32, k = e / per, rem = e - k * per;
+        const int s = (int)(rem >> 5), i = (int)(rem & 31);
+        const long long r = k * 32 + i;
+        const int c = s - i;
+        const bool ok = r < ny && c >= 0 && c < nx;
+        for (int q = 0; q < nslots; ++q) dst[q * sslot + e] = ok ? src[q * n + r * nx + c] : T(0);
+    }
+}
 
 __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
     return *(volatile const unsigned long long*)p;
@@ -94,8 +119,9 @@ struct PipeNode {
     double2 old[4];
 };
 
+// j: the node (natural index, for the messages); e: its lane-skewed index (read-only operands)
 template <bool DELTA, bool SOLVE, bool SYMR, bool UNI>
-__device__ __forceinline__ void pipe_load(PipeNode& o, const PipeP& Q, int j, bool valid) {
+__device__ __forceinline__ void pipe_load(PipeNode& o, const PipeP& Q, int j, long long e, bool valid) {
     o.mk = 0u;
     o.b = o.d = 0.0;
     o.inE = o.inN = make_double2(0.0, 0.0);
@@ -107,16 +133,16 @@ __device__ __forceinline__ void pipe_load(PipeNode& o, const PipeP& Q, int j, bo
     if (!valid) return;
     const SeqP& P = Q.P;
     const size_t n = (size_t)P.n;
-    o.mk = __ldg(P.mask + j);
+    o.mk = __ldg(Q.smask + e);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        o.cc[q] = UNI ? Q.cu[q] : __ldg(P.c + q * n + j);
-        if (SOLVE && !SYMR) o.rv[q] = __ldg(Q.rowv + q * n + j);
+        if (!UNI) o.cc[q] = __ldg(Q.sc + q * Q.sslot + e);
+        if (SOLVE && !SYMR) o.rv[q] = __ldg(Q.srow + q * Q.sslot + e);
     }
     o.inE = __ldcg(Q.msg + 2 * n + j);  // written by sweep t-1 on another SM
     o.inN = __ldcg(Q.msg + 3 * n + j);
-    o.b = __ldg(Q.b + j);
-    o.d = UNI ? Q.du : __ldg(P.diag + j);
+    o.b = __ldg(Q.sb + e);
+    if (!UNI) o.d = __ldg(Q.sd + e);
     if (DELTA) {  // previous-sweep values of this node's four out-slots (only this node writes them)
         const long long nb[4] = {(long long)j - P.nx, (long long)j - 1, (long long)j + 1, (long long)j + P.nx};
 #pragma unroll
@@ -240,7 +266,11 @@ static __global__ void __launch_bounds__(32, MINB) k_seq_pipe(PipeP Q) {
         __syncwarp();
     }
     PipeNode cur, nxt;
-    pipe_load<DELTA, SOLVE, SYMR, UNI>(cur, Q, r * nx, row_ok && lane == 0);
+    // this lane's skewed element at step s is ebase + 32 s; row r0 - 1 (lane 31 of the previous
+    // strip) at column c is pbase + 32 (c + 31)
+    const long long ebase = (long long)strip * Q.sstep * 32 + lane;
+    const long long pbase = (long long)(strip - 1) * Q.sstep * 32 + 31;
+    pipe_load<DELTA, SOLVE, SYMR, UNI>(cur, Q, r * nx, ebase, row_ok && lane == 0);
     double2 west = make_double2(0.0, 0.0), north_out = make_double2(0.0, 0.0);
     double dmax = 0.0, rmax = 0.0;
     // own-row history for the residual two columns behind: x, b, diag, mask, A row of c-1 / c-2
@@ -272,24 +302,8 @@ static __global__ void __launch_bounds__(32, MINB) k_seq_pipe(PipeP Q) {
                 __syncwarp();
             }
         }
-        pipe_load<DELTA, SOLVE, SYMR, UNI>(nu, Q, j + 1, row_ok && c + 1 >= 0 && c + 1 < nx);
-        {
-            const int cp = c + kSeqPrefetch;
-            if (row_ok && cp >= 0 && cp < nx && (cp & 7) == 0) {
-                const size_t jp = (size_t)r * nx + cp, nn = (size_t)n;
-                prefetch_l1(P.mask + jp);
-                if (!UNI) {
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) prefetch_l1(P.c + q * nn + jp);
-                }
-                if (SOLVE && !SYMR) {
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) prefetch_l1(Q.rowv + q * nn + jp);
-                }
-                prefetch_l1(Q.b + jp);
-                if (!UNI) prefetch_l1(P.diag + jp);
-            }
-        }
+        // next node: the skewed operands of step s + 1 are one coalesced line per array
+        pipe_load<DELTA, SOLVE, SYMR, UNI>(nu, Q, j + 1, ebase + 32ll * (s + 1), row_ok && c + 1 >= 0 && c + 1 < nx);
         double2 south;
         south.x = __shfl_up_sync(FULL, north_out.x, 1);
         south.y = __shfl_up_sync(FULL, north_out.y, 1);
@@ -324,11 +338,11 @@ static __global__ void __launch_bounds__(32, MINB) k_seq_pipe(PipeP Q) {
             in[3] = (mk & 8u) ? cu.inN : make_double2(0.0, 0.0);
             double cc[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) cc[q] = (mk & (1u << (16 + q))) ? cu.cc[q] : 0.0;
+            for (int q = 0; q < 4; ++q) cc[q] = (mk & (1u << (16 + q))) ? (UNI ? Q.cu[q] : cu.cc[q]) : 0.0;
             double sig = 0.0, acc = cu.b;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                if (q == 2) sig = dadd(sig, cu.d);
+                if (q == 2) sig = dadd(sig, UNI ? Q.du : cu.d);
                 const bool iq = mk & (1u << q), both = iq && (mk & (1u << (16 + q)));
                 const double a2 = dadd(acc, in[q].y), s2 = dadd(sig, dmul(in[q].x, cc[q]));
                 acc = iq ? a2 : acc;
@@ -379,13 +393,13 @@ static __global__ void __launch_bounds__(32, MINB) k_seq_pipe(PipeP Q) {
             const int cr = c - 2;
             if (row_ok && cr >= 0 && cr < nx && (lane < 31 || r == ny - 1)) {
                 const double below = lane == 0 ? ring_x1[cr & (kSeqRing - 1)] : xb;
-                rmax = fmax(rmax, pipe_residual(mkh2, bh2, dh2, rvh2, below, xh3, xh2, xh1, xa));
+                rmax = fmax(rmax, pipe_residual(mkh2, bh2, UNI ? Q.du : dh2, UNI ? Q.cu : rvh2, below, xh3, xh2, xh1, xa));
             }
             // lane 0 also closes row r0-1 of the previous strip (its lane 31 cannot see row r0)
             if (lane == 0 && boundary && cr >= 0 && cr < nx) {
                 const double xw = cr > 0 ? ring_x1[(cr - 1) & (kSeqRing - 1)] : 0.0;
                 const double xe = cr + 1 < nx ? ring_x1[(cr + 1) & (kSeqRing - 1)] : 0.0;
-                rmax = fmax(rmax, pipe_residual(pmk, pb, pd, prv, ring_x2[cr & (kSeqRing - 1)], xw,
+                rmax = fmax(rmax, pipe_residual(pmk, pb, UNI ? Q.du : pd, UNI ? Q.cu : prv, ring_x2[cr & (kSeqRing - 1)], xw,
                                                 ring_x1[cr & (kSeqRing - 1)], xe, xh2));
             }
             // shift the histories; lane 0 fetches row r0-1's operands for the next step's column
@@ -393,25 +407,27 @@ static __global__ void __launch_bounds__(32, MINB) k_seq_pipe(PipeP Q) {
             xh2 = xh1;
             xh1 = xj;
             bh2 = bh1;
-            dh2 = dh1;
+            if (!UNI) dh2 = dh1;
             mkh2 = mkh1;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) rvh2[q] = rvh1[q];
+            for (int q = 0; q < 4; ++q)
+                if (!UNI) rvh2[q] = rvh1[q];
             bh1 = cu.b;
-            dh1 = cu.d;
+            if (!UNI) dh1 = cu.d;
             mkh1 = act ? cu.mk : 0u;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) rvh1[q] = SYMR ? cu.cc[q] : cu.rv[q];
+            for (int q = 0; q < 4; ++q)
+                if (!UNI) rvh1[q] = SYMR ? cu.cc[q] : cu.rv[q];
             if (lane == 0 && boundary) {
                 const int cn = c - 1;  // next step's residual column
                 if (cn >= 0 && cn < nx) {
-                    const size_t jp = (size_t)(r0 - 1) * nx + cn;
-                    pmk = __ldg(P.mask + jp);
-                    pb = __ldg(Q.b + jp);
-                    pd = UNI ? Q.du : __ldg(P.diag + jp);
+                    const long long ep = pbase + 32ll * (cn + 31);
+                    pmk = __ldg(Q.smask + ep);
+                    pb = __ldg(Q.sb + ep);
+                    if (!UNI) pd = __ldg(Q.sd + ep);
 #pragma unroll
                     for (int q = 0; q < 4; ++q)
-                        prv[q] = UNI ? Q.cu[q] : __ldg((SYMR ? P.c : Q.rowv) + (size_t)q * n + jp);
+                        if (!UNI) prv[q] = __ldg((SYMR ? Q.sc : Q.srow) + q * Q.sslot + ep);
                 }
             }
         }
