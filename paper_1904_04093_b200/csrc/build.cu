@@ -208,6 +208,12 @@ void Engine::build_dia_device(const int* ro_, const int* ci_, const double* v_) 
     phase("  dia: fill + facts kernels");
     symmetric = hf.asym == 0u;
     grid5 = gx > 0 && hf.wrap == 0u;
+    dia.full5nx = dia.full5ny = 0;
+    if (grid5 && symmetric && nnz == 5ll * n - 2ll * gx - 2ll * (n / gx) &&  // every in-grid entry present
+        !getenv("BGABP_NO_FULL5")) {                                          // (A/B knob)
+        dia.full5nx = gx;
+        dia.full5ny = n / gx;
+    }
     grid5_nx = gx;
     dia.uniform = 0;
     if (symmetric && n > 0) {  // constant-coefficient stencil (one bit pattern per slot and diagonal)
