@@ -14,22 +14,23 @@
 
 namespace bgabp {
 
-constexpr int kTmaTile = 64;  // nodes per warp tile (two per lane)
+constexpr int kTmaTile = 64;  // n must be a multiple of this (the largest tile below)
 
-template <int S>
-__host__ __device__ constexpr unsigned dia_tma_buf_bytes() {  // one buffer: S message rows, mask, b
-    return (unsigned)(S * kTmaTile * 16 + kTmaTile * 4 + kTmaTile * 8);
+// one buffer of a warp tile of 32 * NPL nodes (NPL per lane): S message rows, mask, b
+template <int S, int NPL>
+__host__ __device__ constexpr unsigned dia_tma_buf_bytes() {
+    return (unsigned)(32 * NPL * (S * 16 + 4 + 8));
 }
 
-template <int S, int WPB>
+template <int S, int NPL, int WPB>
 __host__ __device__ constexpr size_t dia_tma_smem() {
-    return (size_t)WPB * 2 * dia_tma_buf_bytes<S>() + (size_t)WPB * 2 * sizeof(unsigned long long);
+    return (size_t)WPB * 2 * dia_tma_buf_bytes<S, NPL>() + (size_t)WPB * 2 * sizeof(unsigned long long);
 }
 
 // SYM / UNIF / DELTA as in k_flood_solve_dia (no sharding, peers or damping on this path).
 // Requires n % kTmaTile == 0 (every tile full: the bulk copies stay 16-byte multiples).
-template <int S, bool DELTA, bool SYM, bool UNIF, int WPB>
-static __global__ void __launch_bounds__(32 * WPB, 2) k_flood_solve_dia_tma(DiaP P, const double* __restrict__ b,
+template <int S, bool DELTA, bool SYM, bool UNIF, int WPB, int NPL = 2, int MINB = 2>
+static __global__ void __launch_bounds__(32 * WPB, MINB) k_flood_solve_dia_tma(DiaP P, const double* __restrict__ b,
                                                                        double2* m0, double2* m1, double* x0,
                                                                        double* x1, Ctrl* ctrl,
                                                                        unsigned long long* spread) {
@@ -43,13 +44,14 @@ static __global__ void __launch_bounds__(32 * WPB, 2) k_flood_solve_dia_tma(DiaP
     const bool res = t >= 3;
     const int n = P.n;
     const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr unsigned kBuf = dia_tma_buf_bytes<S>();
+    constexpr unsigned kBuf = dia_tma_buf_bytes<S, NPL>();
+    constexpr int T = 32 * NPL;  // nodes per tile
     unsigned char* wbase = smem + (size_t)wl * 2 * kBuf;
     unsigned long long* bars =
         reinterpret_cast<unsigned long long*>(smem + (size_t)WPB * 2 * kBuf) + 2 * wl;
     auto msg_of = [&](int buf) { return reinterpret_cast<double2*>(wbase + (size_t)buf * kBuf); };
-    auto mask_of = [&](int buf) { return reinterpret_cast<uint32_t*>(msg_of(buf) + S * kTmaTile); };
-    auto b_of = [&](int buf) { return reinterpret_cast<double*>(mask_of(buf) + kTmaTile); };
+    auto mask_of = [&](int buf) { return reinterpret_cast<uint32_t*>(msg_of(buf) + S * T); };
+    auto b_of = [&](int buf) { return reinterpret_cast<double*>(mask_of(buf) + T); };
     if (lane == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
@@ -59,16 +61,16 @@ static __global__ void __launch_bounds__(32 * WPB, 2) k_flood_solve_dia_tma(DiaP
     // (deriving the mask of a full 5-point grid from (row, column), as the one-thread-per-node
     // step does, measured 0.4 % slower here: the staged mask is nearly free)
     constexpr bool full5 = false;
-    const int ntiles = n / kTmaTile;
+    const int ntiles = n / T;
     const int stride = gridDim.x * WPB;
     auto issue = [&](int tile, int buf) {  // lane 0: the tile's streams into buffer `buf`
-        const long long j0 = (long long)tile * kTmaTile;
-        mbar_arrive_tx(&bars[buf], full5 ? kBuf - kTmaTile * 4u : kBuf);
+        const long long j0 = (long long)tile * T;
+        mbar_arrive_tx(&bars[buf], full5 ? kBuf - T * 4u : kBuf);
 #pragma unroll
         for (int s = 0; s < S; ++s)
-            bulk_g2s(msg_of(buf) + s * kTmaTile, min + (long long)s * n + j0, kTmaTile * 16u, &bars[buf]);
-        if (!full5) bulk_g2s(mask_of(buf), P.mask + j0, kTmaTile * 4u, &bars[buf]);
-        bulk_g2s(b_of(buf), b + j0, kTmaTile * 8u, &bars[buf]);
+            bulk_g2s(msg_of(buf) + s * T, min + (long long)s * n + j0, T * 16u, &bars[buf]);
+        if (!full5) bulk_g2s(mask_of(buf), P.mask + j0, T * 4u, &bars[buf]);
+        bulk_g2s(b_of(buf), b + j0, T * 8u, &bars[buf]);
     };
     double rabs = 0.0, dmax = 0.0;
     int tile = blockIdx.x * WPB + wl, buf = 0;
@@ -82,10 +84,10 @@ static __global__ void __launch_bounds__(32 * WPB, 2) k_flood_solve_dia_tma(DiaP
         }
         // the residual's x(t-2) gathers and (general coefficients) the coefficient columns do not
         // depend on the staged data: issue them before waiting (mask-independent, indices clamped)
-        double xn[2][S], xjj[2], cc[2][S], dj[2];
+        double xn[NPL][S], xjj[NPL], cc[NPL][S], dj[NPL];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int j = tile * kTmaTile + 32 * h + lane;
+        for (int h = 0; h < NPL; ++h) {
+            const int j = tile * T + 32 * h + lane;
             xjj[h] = res ? __ldg(xr + j) : 0.0;
             dj[h] = UNIF ? P.du : __ldg(P.diag + j);
 #pragma unroll
@@ -103,9 +105,9 @@ static __global__ void __launch_bounds__(32 * WPB, 2) k_flood_solve_dia_tma(DiaP
         const uint32_t* smk = mask_of(buf);
         const double* sb = b_of(buf);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < NPL; ++h) {
             const int jl = 32 * h + lane;
-            const int j = tile * kTmaTile + jl;
+            const int j = tile * T + jl;
             uint32_t mk;
             if (full5) {  // slots -nx, -1, +1, +nx; structurally symmetric
                 const int row = j / P.full5nx, col = j - row * P.full5nx;
@@ -120,7 +122,7 @@ static __global__ void __launch_bounds__(32 * WPB, 2) k_flood_solve_dia_tma(DiaP
             double c[S];
 #pragma unroll
             for (int s = 0; s < S; ++s) {
-                in[s] = sm[s * kTmaTile + jl];
+                in[s] = sm[s * T + jl];
                 c[s] = (mk & (1u << (16 + s))) ? cc[h][s] : 0.0;
             }
             double sig = 0.0, acc = bj;

@@ -520,29 +520,33 @@ static void launch_sharded_step(Engine& E, unsigned g, bool dl) {
 
 // The bulk-copy staged step (dia_tma_kernels.cuh): persistent warps, one grid per SM count x
 // resident blocks.  BGABP_DIA_TMA=0 keeps the one-thread-per-node step (A/B).
-template <int S, bool DL, bool SYM, bool UNIF>
+template <int S, bool DL, bool SYM, bool UNIF, int WPB, int NPL, int MINB>
 static void launch_dia_tma_t(Engine& E) {
-    constexpr int WPB = 8;
-    constexpr size_t smem = dia_tma_smem<S, WPB>();
+    constexpr size_t smem = dia_tma_smem<S, NPL, WPB>();
+    auto kfn = k_flood_solve_dia_tma<S, DL, SYM, UNIF, WPB, NPL, MINB>;
     static int grid = 0;
     if (!grid) {
-        ck(cudaFuncSetAttribute(k_flood_solve_dia_tma<S, DL, SYM, UNIF, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem),
-           "dia tma smem");
+        ck(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "dia tma smem");
         int bps = 1, sms = 148;
-        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_flood_solve_dia_tma<S, DL, SYM, UNIF, WPB>, 32 * WPB,
-                                                         smem),
-           "occupancy");
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kfn, 32 * WPB, smem), "occupancy");
         ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, E.device), "sm count");
         grid = sms * std::max(bps, 1);
     }
-    k_flood_solve_dia_tma<S, DL, SYM, UNIF, WPB><<<grid, 32 * WPB, smem, E.st>>>(
-        E.dia, E.solve_b, E.d_msg[0], E.d_msg[1], E.d_xf, E.d_xf + E.n, E.d_ctrl, E.d_spread);
+    kfn<<<grid, 32 * WPB, smem, E.st>>>(E.dia, E.solve_b, E.d_msg[0], E.d_msg[1], E.d_xf, E.d_xf + E.n, E.d_ctrl,
+                                        E.d_spread);
+}
+
+// Two nodes per lane, 4 blocks of 4 warps per SM (16 warps, 124 registers).  Measured on config 2
+// (ms per step): 2 blocks of 8 warps 0.1075, 4 of 4 0.1072; one node per lane with 24 warps
+// (80 registers, small spills) 0.1092, with 32 warps (64 registers, spills) 0.1440.
+template <int S, bool DL>
+static void launch_dia_tma_v(Engine& E) {
+    launch_dia_tma_t<S, DL, true, true, 4, 2, 4>(E);
 }
 
 template <int S>
 static void launch_dia_tma_s(Engine& E, bool dl) {  // constant stencils only (see enqueue_fused_kernel)
-    if (dl) launch_dia_tma_t<S, true, true, true>(E); else launch_dia_tma_t<S, false, true, true>(E);
+    if (dl) launch_dia_tma_v<S, true>(E); else launch_dia_tma_v<S, false>(E);
 }
 
 static bool dia_tma_enabled() {

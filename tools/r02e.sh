@@ -1,9 +1,7 @@
-O=gpurun_out/r02y; mkdir -p $O
-timeout 2400 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/pytest_gpu.log 2>&1; tail -3 $O/pytest_gpu.log
-timeout 600 python bench.py --steps 20 --warmup 20 --no-cpu-baseline --no-schedules --no-tts > $O/b.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
-      --log-file $O/launches_config2.csv python bench.py --steps 20 --warmup 20 --no-cpu-baseline --no-schedules --no-tts > $O/ncu_launch.log 2>&1
-timeout 600 python tools/kernel_drivers.py flood > $O/drv.log 2>&1 && \
-ncu --set full --import-source on --clock-control none -k regex:k_flood_solve_dia -s 20 -c 1 -o $O/ncu_flood python tools/kernel_drivers.py flood > $O/ncu_flood.log 2>&1
-ncu -i $O/ncu_flood.ncu-rep --page raw --csv > $O/ncu_flood.raw.csv 2>/dev/null; rm -f $O/ncu_flood.ncu-rep
-tail -2 $O/ncu_flood.log
+O=gpurun_out/r02z; mkdir -p $O
+timeout 600 python -m pytest -q -x -p no:cacheprovider tests/test_gpu_gabp.py -k "solve or golden" > $O/pytest.log 2>&1; tail -1 $O/pytest.log
+for i in 1 2; do for v in 0 1 2 3; do
+  BGABP_DIA_TMA_V=$v timeout 300 python bench.py --steps 500 --warmup 20 --no-cpu-baseline --no-schedules --no-tts > $O/b2.log 2>&1
+  python -c "import json;d=json.loads([l for l in open('$O/b2.log') if l.startswith('{')][-1]);print('config2 V=$v', round(d['ms_per_step'],5), round(d['roofline']['us_per_launch'],2), round(d['e2e']['value']/1e9,1))"
+done; done
+for v in 1 2; do BGABP_DIA_TMA_V=$v timeout 600 python -m pytest -q -x -p no:cacheprovider tests/test_gpu_gabp.py -k "solve or golden" > $O/pytest$v.log 2>&1; tail -1 $O/pytest$v.log; done
