@@ -115,6 +115,10 @@ void Engine::launch_pipe(const double* b, double* x, int t0, int nsweeps, bool s
     // 164-register build of the constant-stencil kernel (12 warps per SM) ran 0.339 ms, and 0.325
     // ms with the lane-skewed operands (0.315 at 8 warps): the SM's warp-step rate stays at ~2.9
     // per us.  The lane-skewed operands took the general-coefficient kernel 0.393 -> 0.331 ms.
+    // Two rows per lane (strips of 64 rows, two independent node chains per step, bit-identical)
+    // ran 0.346 ms against 0.324 in the same run, and the spin / back-off of the progress polls
+    // (16 x 64 ns ... 0 x 1 us) made no difference: the rate does not follow the warp count, the
+    // chains per warp or the poll pressure.
     Q.gate = kPipeR;
     {  // b of this launch in the lane-skewed layout (the multigrid smoother passes a new residual)
         const int nx = grid5_nx, ny = n / grid5_nx;
