@@ -524,8 +524,11 @@ template <int S, bool DL, bool SYM, bool UNIF, int WPB, int NPL, int MINB>
 static void launch_dia_tma_t(Engine& E) {
     constexpr size_t smem = dia_tma_smem<S, NPL, WPB>();
     auto kfn = k_flood_solve_dia_tma<S, DL, SYM, UNIF, WPB, NPL, MINB>;
-    static int grid = 0;
+    static int grids[64] = {};  // per device: the attribute is set per device context
+    const int dev = std::min(std::max(E.device, 0), 63);
+    int& grid = grids[dev];
     if (!grid) {
+        DeviceGuard g(E.device);
         ck(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "dia tma smem");
         int bps = 1, sms = 148;
         ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kfn, 32 * WPB, smem), "occupancy");
