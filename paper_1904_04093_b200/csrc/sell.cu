@@ -146,7 +146,10 @@ void Engine::launch_sell_step(bool dl) {
         const unsigned g = nblk_host((long long)P.nchunks * 32);
         double2 *m0 = d_msg[0], *m1 = d_msg[1];
         double *x0 = d_xf, *x1 = d_xf + n;
-        if (!sell_reg && q < 3) {  // shared-memory staged (bulk async copies)
+        // shared-memory staged (bulk async copies) for chunks of <= 8 slot rows; wider chunks run
+        // the register kernel (a random 4M-node graph, chunks of 9-32 rows: 2.70 vs 2.89 ms per
+        // step staged -- 16 KB of staging per warp leaves 12 warps per SM for its random gathers)
+        if (!sell_reg && q < 1) {
 #define TMA_L(W_, P_, N_, G_) \
     launch_tma<W_, P_, N_>(P, sell_grid[G_], dl, symmetric, damp, solve_b, m0, m1, x0, x1, d_ctrl, d_spread, st)
             if (sell_variant == 0) {

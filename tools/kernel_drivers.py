@@ -8,6 +8,7 @@ families (kernels):
   flood3   config-3 solve steps              k_flood_solve_dia<4, nonsymmetric>
   sweep    per-sweep API on config 2         k_flood_dia, k_aggregate_dia, k_state_gather/scatter
   sell     csr7 (config 4 on SELL) steps     k_flood_solve_sell_tma
+  sellrand random DD graph on SELL steps     k_flood_solve_sell_tma / k_flood_solve_sell
   rb       red-black solve on config 2       k_rb_half, k_residual_dia
   seq      lexicographic solve on 2048^2     k_seq_pipe
   levels   greedy-coloured order, random DD  k_level_csr, k_residual_csr
@@ -59,6 +60,12 @@ def main():
     elif f == "sell":
         P = g.config_problem(4, size=a.n)
         print(f, steps(g.GabpEngine(P.A, g.Layout.Csr), P.b, g.Schedule.parallel_flood(), 12))
+    elif f == "sellrand":  # random diagonally dominant graph (bench --workload csr_random)
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        from bench import random_dd
+        n = a.n or (1 << 22)
+        ro, ci, v, b = random_dd(n, 6, 7)
+        print(f, steps(g.GabpEngine(g.SparseMatrix(n, ro, ci, v), g.Layout.Csr), b, g.Schedule.parallel_flood(), 12))
     elif f == "rb":
         N = a.n or 2048
         P = g.config_problem(2, size=N)
