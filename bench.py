@@ -93,15 +93,29 @@ class Clocks:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+SHARED_GPU = False  # ranks share a GPU (more ranks than visible GPUs): gloo, host-barrier shard steps
+
+
 def dist_setup():
+    """One process per GPU over NCCL.  With more ranks than visible GPUs (a plumbing check of the
+    multi-GPU mode on one device) the ranks share the GPUs round-robin, torch.distributed runs on
+    gloo, and the sharded solve uses host barriers instead of device-side waits between processes."""
+    global SHARED_GPU
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
         import torch
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        ndev = torch.cuda.device_count()
+        if ndev < world:
+            SHARED_GPU = True
+            local = local % max(ndev, 1)
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
 
 
@@ -117,7 +131,7 @@ def max_over_ranks(v, world, device="cuda"):
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device=device)
+    t = torch.tensor([v], dtype=torch.float64, device="cpu" if SHARED_GPU else device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -498,7 +512,7 @@ def run_sharded(args, world, rank, local):
     layouts = sh.ShardLayout.partition(n, halo, world, align=max(nx_in, 1))
     L = layouts[rank]
     shard = sh.GpuShard(sh.local_matrix(A_in, L), L, b_in[L.glo:L.ghi], device=f"cuda:{local}")
-    solver = sh.IpcSolve(shard, layouts)
+    solver = sh.IpcSolve(shard, layouts, host_barrier=SHARED_GPU)
     solver.connect()
     b_inf = float(np.abs(b_in).max())
     tol = 0.0 if args.config == 0 else 1e-8 * b_inf
