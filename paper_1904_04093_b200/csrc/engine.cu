@@ -463,7 +463,7 @@ void Engine::solve_begin(const double* b_dev, const bgabp_schedule& s, const bga
     if (solve_pipe) {  // pipelined lexicographic sweeps: x(0) = 0 in ring slot 0
         pipe_setup(true);
         pipe_reset();
-        ck(cudaMemsetAsync(d_xring, 0, sizeof(double) * std::max(n, 1), st), "memset ring");
+        ck(cudaMemsetAsync(d_xring, 0, sizeof(double) * (size_t)pipe_sn, st), "memset ring");
         pipe_next = 1;
     }
     cur = 0;
@@ -781,17 +781,15 @@ void Engine::solve_report(bgabp_report& rep, std::string& detail) {
 const double* Engine::solve_x() {
     if (solve_pipe) {
         const Ctrl& c = *h_ctrl;  // read by solve_report
-        const double* xs = d_xring + (size_t)(c.solx % kPipeR) * n;
-        if (c.status == BGABP_DIVERGED && c.detail_kind == 4 && n > 0) {
+        if (n == 0) return d_aux;
+        const int xs = c.solx % kPipeR;
+        if (c.status == BGABP_DIVERGED && c.detail_kind == 4) {
             // the reference's sweep stopped at visit position p: x(k) before it (and at it for an
             // edge pivot, whose x-stage ran), x(k-1) from there on; positions are node ids here
-            const double* xo = d_xring + (size_t)((c.solx + kPipeR - 1) % kPipeR) * n;
             const long long p = (long long)(c.detail_key >> 32) + ((c.detail_key & 0xffffffffu) ? 1 : 0);
-            k_compose_pivot_x<<<nblk(n), 256, 0, st>>>(xs, xo, d_aux, n, p);
-            ck(cudaGetLastError(), "compose x");
-            return d_aux;
+            return pipe_x_out(xs, (c.solx + kPipeR - 1) % kPipeR, p);
         }
-        return xs;
+        return pipe_x_out(xs, xs, (long long)n);
     }
     if (!solve_fused && solve_flood) {  // union-CSR flood: x(k) in slot k & 1 of d_xord
         const Ctrl& c = *h_ctrl;
@@ -985,8 +983,9 @@ int Engine::cold_sweeps_dev(const double* r_dev, const bgabp_schedule& s, int sw
         rb_build(s.nx);
         for (int k = 0; k < sweeps; ++k) launch_rb_sweep(r_dev, e_dev, k == 0, false, nullptr, MODE_PLAIN);
     } else {
-        for (int k = 0; k < 2; ++k)
-            ck(cudaMemsetAsync(d_msg[k], 0, sizeof(double2) * (size_t)std::max<long long>(nslots, 1), st), "memset");
+        if (!seq_applicable(s))  // the pipeline zeroes its own (lane-skewed) messages
+            for (int k = 0; k < 2; ++k)
+                ck(cudaMemsetAsync(d_msg[k], 0, sizeof(double2) * (size_t)std::max<long long>(nslots, 1), st), "memset");
         ck(cudaMemsetAsync(e_dev, 0, sizeof(double) * std::max(n, 1), st), "memset");
         cur = 0;
         if (n == 0 || sweeps <= 0) return BGABP_OK;

@@ -203,7 +203,9 @@ struct Engine {
     void launch_seq_sweep(const double* b, double2* msg, double* x, bool delta, unsigned long long* dslot, int mode,
                           long long xstride = 0);
     // pipelined lexicographic sweeps (seqpipe_kernels.cuh): many sweeps per launch
-    double* d_xring = nullptr;  // [kPipeR][n] x(t) of the solve
+    double* d_xring = nullptr;   // [kPipeR][pipe_sn] x(t) of the solve, lane-skewed
+    double2* d_pmsg = nullptr;   // [4][pipe_sn] the pipeline's in-slot messages, lane-skewed
+    const double* pipe_x_out(int slot, int oslot, long long p);  // natural-order x of a ring slot
     unsigned long long* d_pprog = nullptr;
     PipeRed* d_pred = nullptr;
     int* d_pint = nullptr;  // [0] ticket, [1] decided

@@ -42,10 +42,14 @@ void Engine::pipe_setup(bool ring) {
         d_pred = static_cast<PipeRed*>(dalloc(sizeof(PipeRed) * kPipeR));
         d_pint = static_cast<int*>(dalloc(sizeof(int) * 2));
     }
-    if (ring && !d_xring) d_xring = static_cast<double*>(dalloc(sizeof(double) * (size_t)kPipeR * std::max(n, 1)));
+    pipe_sn = (long long)strips * (grid5_nx + 31) * 32;
+    // messages and the x ring live in the lane-skewed layout for the whole launch (both start
+    // from zero: the solve's and a smoothing call's fresh state), so a strip's 32 lanes load and
+    // store one or two lines per array and step instead of 32 rows' sectors
+    if (!d_pmsg) d_pmsg = static_cast<double2*>(dalloc(sizeof(double2) * 4 * (size_t)pipe_sn));
+    if (ring && !d_xring) d_xring = static_cast<double*>(dalloc(sizeof(double) * (size_t)kPipeR * pipe_sn));
     if (!d_skb) {  // lane-skewed read-only operands, built once per handle (b: every launch)
         const int nx = grid5_nx, ny = n / grid5_nx, sstep = nx + 31;
-        pipe_sn = (long long)strips * sstep * 32;
         const unsigned g = std::min<unsigned>(nblk_host(pipe_sn), 148u * 16u);
         d_skmask = static_cast<uint32_t*>(dalloc(sizeof(uint32_t) * (size_t)pipe_sn));
         k_pipe_skew<uint32_t><<<g, 256, 0, st>>>(dia.mask, d_skmask, nx, ny, sstep, pipe_sn, 1, pipe_sn, n);
@@ -66,6 +70,7 @@ void Engine::pipe_setup(bool ring) {
 
 void Engine::pipe_reset() {
     const int np = kPipeR * pipe_strips;
+    ck(cudaMemsetAsync(d_pmsg, 0, sizeof(double2) * 4 * (size_t)pipe_sn, st), "memset pipeline messages");
     k_pipe_reset<<<std::max(1, std::min((np + 255) / 256, 256)), 256, 0, st>>>(d_pred, d_pprog, np, d_pint);
 }
 
@@ -75,7 +80,7 @@ void Engine::launch_pipe(const double* b, double* x, int t0, int nsweeps, bool s
     Q.P = SeqP{grid5_nx, n / grid5_nx, n, dia.mask, dia.c, dia.diag};
     Q.rowv = dia.rowv;
     Q.b = b;
-    Q.msg = d_msg[0];
+    Q.msg = d_pmsg;
     Q.x = x;
     Q.prog = d_pprog;
     Q.red = d_pred;
@@ -154,6 +159,24 @@ void Engine::launch_pipe(const double* b, double* x, int t0, int nsweeps, bool s
         k_pipe_failure<<<1, 1, 0, st>>>(d_ctrl, d_pred, t0, nsweeps);
     }
     ck(cudaGetLastError(), "pipelined sequential sweeps");
+}
+
+// x(t) of the pipelined solve out of its lane-skewed ring slot (natural order); on a pivot stop
+// node j < p takes xs, the rest xo (the reference's partly updated x)
+static __global__ void k_pipe_x_out(const double* __restrict__ xs, const double* __restrict__ xo,
+                                    double* __restrict__ out, int nx, int n, int sstep, long long p) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const int r = j / nx, c = j - r * nx, i = r & 31;
+    const long long e = (long long)(r >> 5) * sstep * 32 + 32ll * (c + i) + i;
+    out[j] = j < p ? xs[e] : xo[e];
+}
+
+const double* Engine::pipe_x_out(int slot, int oslot, long long p) {
+    k_pipe_x_out<<<nblk_host(n), 256, 0, st>>>(d_xring + (size_t)slot * pipe_sn, d_xring + (size_t)oslot * pipe_sn, d_aux,
+                                          grid5_nx, n, grid5_nx + 31, p);
+    ck(cudaGetLastError(), "pipeline x");
+    return d_aux;
 }
 
 }  // namespace bgabp

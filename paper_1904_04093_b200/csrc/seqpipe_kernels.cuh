@@ -41,8 +41,8 @@ struct PipeP {
     SeqP P;
     const double* rowv;  // [4][n] A_{j,j+off} (residual); == P.c when A is bit-symmetric
     const double* b;
-    double2* msg;
-    double* x;                 // SOLVE: ring [kPipeR][n]; smoothing: x of the last sweep
+    double2* msg;              // [4][sslot] in-slot messages, lane-skewed like the operands below
+    double* x;                 // SOLVE: ring [kPipeR][sslot], lane-skewed; smoothing: x of the last sweep (natural)
     unsigned long long* prog;  // [kPipeR][strips]
     PipeRed* red;              // [kPipeR]
     int* ticket;
@@ -119,9 +119,22 @@ struct PipeNode {
     double2 old[4];
 };
 
-// j: the node (natural index, for the messages); e: its lane-skewed index (read-only operands)
+// lane-skewed index of the out-slot node q of the node at skewed index e (lane `lane`): the
+// south node (r-1, c) is lane - 1 one step earlier (lane 0: lane 31 of the previous strip, step
+// c + 31), west / east the same lane one step earlier / later, north (r+1, c) lane + 1 one step
+// later (lane 31: lane 0 of the next strip, step c); ss = elements per strip (sstep * 32)
+__device__ __forceinline__ long long pipe_nbr(long long e, int q, int lane, long long ss) {
+    switch (q) {
+        case 0: return lane > 0 ? e - 33 : e - ss + 1023;
+        case 1: return e - 32;
+        case 2: return e + 32;
+        default: return lane < 31 ? e + 33 : e + ss - 1023;
+    }
+}
+
+// e: the node's lane-skewed index (messages and read-only operands)
 template <bool DELTA, bool SOLVE, bool SYMR, bool UNI>
-__device__ __forceinline__ void pipe_load(PipeNode& o, const PipeP& Q, int j, long long e, bool valid) {
+__device__ __forceinline__ void pipe_load(PipeNode& o, const PipeP& Q, int lane, long long e, bool valid) {
     o.mk = 0u;
     o.b = o.d = 0.0;
     o.inE = o.inN = make_double2(0.0, 0.0);
@@ -131,24 +144,22 @@ __device__ __forceinline__ void pipe_load(PipeNode& o, const PipeP& Q, int j, lo
         o.old[q] = make_double2(0.0, 0.0);
     }
     if (!valid) return;
-    const SeqP& P = Q.P;
-    const size_t n = (size_t)P.n;
     o.mk = __ldg(Q.smask + e);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         if (!UNI) o.cc[q] = __ldg(Q.sc + q * Q.sslot + e);
         if (SOLVE && !SYMR) o.rv[q] = __ldg(Q.srow + q * Q.sslot + e);
     }
-    o.inE = __ldcg(Q.msg + 2 * n + j);  // written by sweep t-1 on another SM
-    o.inN = __ldcg(Q.msg + 3 * n + j);
+    o.inE = __ldcg(Q.msg + 2 * Q.sslot + e);  // written by sweep t-1 on another SM
+    o.inN = __ldcg(Q.msg + 3 * Q.sslot + e);
     o.b = __ldg(Q.sb + e);
     if (!UNI) o.d = __ldg(Q.sd + e);
     if (DELTA) {  // previous-sweep values of this node's four out-slots (only this node writes them)
-        const long long nb[4] = {(long long)j - P.nx, (long long)j - 1, (long long)j + 1, (long long)j + P.nx};
+        const long long ss = (long long)Q.sstep * 32;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const long long k = nb[q] < 0 ? 0 : (nb[q] >= P.n ? P.n - 1 : nb[q]);
-            o.old[q] = __ldcg(Q.msg + (size_t)(3 - q) * n + k);
+        for (int q = 0; q < 4; ++q) {  // outside the grid (mask bit clear): any in-range element
+            const long long k = pipe_nbr(e, q, lane, ss);
+            o.old[q] = __ldcg(Q.msg + (size_t)(3 - q) * Q.sslot + (k < 0 ? 0 : (k >= Q.sslot ? Q.sslot - 1 : k)));
         }
     }
 }
@@ -252,7 +263,8 @@ static __global__ void __launch_bounds__(32, MINB) k_seq_pipe(PipeP Q) {
     const bool has_prev = t > 1;  // sweep 0 does not exist: its messages are the initial state
     const bool north_strip = strip + 1 < Q.strips && r0 + 31 + 1 < ny;
     const bool boundary = strip > 0 && r0 < ny;
-    double* xt = SOLVE ? Q.x + (size_t)slot * n : Q.x;
+    double* xt = SOLVE ? Q.x + (size_t)slot * Q.sslot : Q.x;
+    const long long ss = (long long)Q.sstep * 32;
     const bool write_x = SOLVE || t == Q.t0 + Q.nsweeps - 1;
     __shared__ double2 ring_m[kSeqRing];
     __shared__ double ring_x1[kSeqRing], ring_x2[kSeqRing];  // x(t) of rows r0-1, r0-2
@@ -270,7 +282,7 @@ static __global__ void __launch_bounds__(32, MINB) k_seq_pipe(PipeP Q) {
     // strip) at column c is pbase + 32 (c + 31)
     const long long ebase = (long long)strip * Q.sstep * 32 + lane;
     const long long pbase = (long long)(strip - 1) * Q.sstep * 32 + 31;
-    pipe_load<DELTA, SOLVE, SYMR, UNI>(cur, Q, r * nx, ebase, row_ok && lane == 0);
+    pipe_load<DELTA, SOLVE, SYMR, UNI>(cur, Q, lane, ebase, row_ok && lane == 0);
     double2 west = make_double2(0.0, 0.0), north_out = make_double2(0.0, 0.0);
     double dmax = 0.0, rmax = 0.0;
     // own-row history for the residual two columns behind: x, b, diag, mask, A row of c-1 / c-2
@@ -286,6 +298,7 @@ static __global__ void __launch_bounds__(32, MINB) k_seq_pipe(PipeP Q) {
         const int c = s - lane;
         const bool act = row_ok && c >= 0 && c < nx;
         const int j = r * nx + c;
+        const long long e = ebase + 32ll * s;
         // previous sweep far enough ahead for next step's prefetch (east: lane 0 is the most
         // demanding lane; north: lane 31 reads the next strip's first row)
         if (has_prev) {
@@ -303,7 +316,7 @@ static __global__ void __launch_bounds__(32, MINB) k_seq_pipe(PipeP Q) {
             }
         }
         // next node: the skewed operands of step s + 1 are one coalesced line per array
-        pipe_load<DELTA, SOLVE, SYMR, UNI>(nu, Q, j + 1, ebase + 32ll * (s + 1), row_ok && c + 1 >= 0 && c + 1 < nx);
+        pipe_load<DELTA, SOLVE, SYMR, UNI>(nu, Q, lane, e + 32, row_ok && c + 1 >= 0 && c + 1 < nx);
         double2 south;
         south.x = __shfl_up_sync(FULL, north_out.x, 1);
         south.y = __shfl_up_sync(FULL, north_out.y, 1);
@@ -315,12 +328,14 @@ static __global__ void __launch_bounds__(32, MINB) k_seq_pipe(PipeP Q) {
             v = __shfl_sync(FULL, v, 0);
             __syncwarp();
             v = min(min(v, nx), s + kSeqRing - 4);
-            const size_t base = (size_t)r0 * nx;
+            // skewed: row r0 column cc is lane 0 of this strip at step cc; rows r0-1 / r0-2 are
+            // lanes 31 / 30 of the previous strip at steps cc + 31 / cc + 30
+            const long long mb = (long long)strip * ss, xb = mb - ss;
             for (int cc = seen + lane; cc < v; cc += 32) {
-                ring_m[cc & (kSeqRing - 1)] = __ldcg(Q.msg + base + cc);
+                ring_m[cc & (kSeqRing - 1)] = __ldcg(Q.msg + mb + 32ll * cc);
                 if (SOLVE) {
-                    ring_x1[cc & (kSeqRing - 1)] = __ldcg(xt + base - nx + cc);
-                    ring_x2[cc & (kSeqRing - 1)] = r0 >= 2 ? __ldcg(xt + base - 2 * nx + cc) : 0.0;
+                    ring_x1[cc & (kSeqRing - 1)] = __ldcg(xt + xb + 32ll * (cc + 31) + 31);
+                    ring_x2[cc & (kSeqRing - 1)] = __ldcg(xt + xb + 32ll * (cc + 30) + 30);
                 }
             }
             __syncwarp();
@@ -373,7 +388,8 @@ static __global__ void __launch_bounds__(32, MINB) k_seq_pipe(PipeP Q) {
             west = out[2];
             nout = out[3];
             if (fabs(sig) < kPivotFloor) atomicMin(&Q.red[slot].opiv, pk);
-            if (write_x) xt[j] = xj;
+            if (SOLVE) xt[e] = xj;
+            else if (write_x) xt[j] = xj;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 if (!(mk & (1u << (16 + q)))) continue;
@@ -381,7 +397,7 @@ static __global__ void __launch_bounds__(32, MINB) k_seq_pipe(PipeP Q) {
                 if (DELTA)
                     dmax = fmax(dmax, fmax(nan_skip_abs(dsub(out[q].x, cu.old[q].x)),
                                            nan_skip_abs(dsub(out[q].y, cu.old[q].y))));
-                Q.msg[(size_t)(3 - q) * n + j + off[q]] = out[q];
+                Q.msg[(size_t)(3 - q) * Q.sslot + pipe_nbr(e, q, lane, ss)] = out[q];
             }
         }
         north_out = nout;
