@@ -385,7 +385,7 @@ def run_gpu(args, world, rank, local):
     if args.config == 2 and info["num_slots"] == 4 and not args.no_schedules:
         nxg = nx_in
         for name, sch, k in (("red_black", g.Schedule.red_black_grid(nxg, nxg), 128),
-                             ("sequential_pipelined", g.Schedule.sequential(), 256)):
+                             ("sequential_pipelined", g.Schedule.sequential(), 2048)):
             eng.solve_device_begin(b_dev.data_ptr(), sch, g.GabpOptions(tol=0.0, max_iter=k + 8))
             eng.solve_device_steps(4)
             torch.cuda.synchronize()

@@ -728,7 +728,11 @@ void Engine::solve_run_to_end() {
     read_ctrl();
     if (h_ctrl->done) return;
     const long long total = (long long)solve_max_iter + (solve_fused ? 2 : 1);
-    int chunk = 16, inflight = 0, oldest = 0;
+    // The pipelined sequential solve fills and drains its wavefront once per launch (~7 ms at
+    // 2048^2), while the sweeps of a launch that start after the decision exit at their gate
+    // check: it runs kPipeChunk sweeps per launch from the start.
+    const int cap = solve_pipe ? kPipeChunk : 512;
+    int chunk = solve_pipe ? kPipeChunk : 16, inflight = 0, oldest = 0;
     while (true) {
         while (inflight < 2 && steps_enqueued < total) {
             solve_steps((int)std::min<long long>(chunk, total - steps_enqueued));
@@ -736,7 +740,7 @@ void Engine::solve_run_to_end() {
             ck(cudaMemcpyAsync(&h_poll[sl], &d_ctrl->done, sizeof(int), cudaMemcpyDeviceToHost, st), "poll");
             ck(cudaEventRecord(poll_ev[sl], st), "event");
             ++inflight;
-            chunk = std::min(chunk * 2, 512);
+            chunk = std::min(chunk * 2, cap);
         }
         if (inflight == 0) throw CudaError("solve loop did not terminate");
         ck(cudaEventSynchronize(poll_ev[oldest]), "poll sync");

@@ -31,6 +31,7 @@
 namespace bgabp {
 
 constexpr int kPipeR = 64;
+constexpr int kPipeChunk = 4096;  // sweeps per launch of a pipelined solve (engine.cu solve_run_to_end)
 
 struct PipeRed {  // per-sweep reductions, ring slot t % kPipeR
     unsigned long long rmax, delta, opiv;
