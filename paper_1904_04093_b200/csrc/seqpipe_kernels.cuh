@@ -398,7 +398,13 @@ static __global__ void __launch_bounds__(32, MINB) k_seq_pipe(PipeP Q) {
                 if (DELTA)
                     dmax = fmax(dmax, fmax(nan_skip_abs(dsub(out[q].x, cu.old[q].x)),
                                            nan_skip_abs(dsub(out[q].y, cu.old[q].y))));
-                Q.msg[(size_t)(3 - q) * Q.sslot + pipe_nbr(e, q, lane, ss)] = out[q];
+                // east- and north-going messages are consumed inside the strip by this sweep (the
+                // `west` register, the south shuffle): only lane 31's north message crosses to the
+                // next strip through memory.  Nothing reads the launch's final messages (the solve
+                // and the smoothing calls start from zero and discard them), so the others are
+                // stored only where the message delta needs the previous sweep's values.
+                if (DELTA || q < 2 || (q == 3 && lane == 31))
+                    Q.msg[(size_t)(3 - q) * Q.sslot + pipe_nbr(e, q, lane, ss)] = out[q];
             }
         }
         north_out = nout;
