@@ -213,6 +213,32 @@ class Oracle:
         if self.has_assemble:
             sig["ref_assemble"] = (vp, [C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_char_p), _dp,
                                         _dp, _dp, _ip, _dp, C.c_char_p, C.c_size_t])
+        self.has_ref_full = hasattr(L, "ref_hier_create")
+        if self.has_ref_full:  # multigrid.cpp / classic.cpp / region_gabp.cpp over the Eigen stand-in
+            sig.update({
+                "ref_hier_create": (vp, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_char_p), _dp, C.c_int,
+                                         C.c_char_p, C.c_size_t]),
+                "ref_hier_free": (None, [vp]),
+                "ref_hier_num_levels": (C.c_int, [vp]),
+                "ref_hier_level_n": (C.c_int, [vp, C.c_int]),
+                "ref_hier_level_nx": (C.c_int, [vp, C.c_int]),
+                "ref_hier_level_frozen_ok": (C.c_int, [vp, C.c_int]),
+                "ref_hier_fine_rhs": (None, [vp, _dp, _dp]),
+                "ref_hier_vcycle": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, _dp, _dp, C.c_char_p, C.c_size_t]),
+                "ref_hier_cycle_flops": (C.c_double, [vp, C.c_int, C.c_int]),
+                "ref_hier_solve": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, _dp, C.c_double, C.c_int, C.c_double,
+                                             _dp, _dp, _ip, _ip, _dp, _ip, C.c_char_p, C.c_size_t]),
+                "ref_relax": (C.c_int, [C.c_int, vp, _dp, _dp, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_size_t]),
+                "ref_region_create": (vp, [vp, C.c_int, _ip, _ip, C.c_char_p, C.c_size_t]),
+                "ref_region_free": (None, [vp]),
+                "ref_region_num_edges": (C.c_int, [vp]),
+                "ref_region_state_size": (C.c_long, [vp, C.POINTER(C.c_long)]),
+                "ref_region_sweep": sig["orc_region_sweep"],
+                "ref_region_solve": sig["orc_region_solve"],
+                "ref_region_direct_message": sig["orc_region_direct_message"],
+                "ref_region_flops": (C.c_double, [vp, C.c_int]),
+                "ref_block_convergence": (C.c_double, [vp, C.c_int, _ip, _ip, C.c_int, _ip, _ip]),
+            })
         for name, (res, args) in sig.items():
             f = getattr(L, name)
             f.restype = res
@@ -440,6 +466,38 @@ class Oracle:
     def hierarchy(self, levels, nx, smoother):
         return _Hierarchy(self, levels, nx, smoother)
 
+    # ---- the reference's own multigrid.cpp / classic.cpp / region_gabp.cpp (reference build only;
+    # compiled over oracle/eigen_shim, see oracle/Makefile) ----------------------------------
+    def ref_hierarchy(self, problem, J1, J2, params, smoother):
+        """belief::Hierarchy(problem, J1, J2, params, smoother) (multigrid.cpp:74-109)."""
+        return _RefHierarchy(self, problem, J1, J2, params or {}, smoother)
+
+    def ref_region(self, A: Csr, large):
+        """belief::RegionGabpEngine over belief::build_two_layer_region_graph (region_gabp.cpp)."""
+        return _Region(self, A, large, prefix="ref_region")
+
+    def ref_relax(self, kind, A: Csr, b, x, sweeps, nx=0, ny=0):
+        """belief::relax (classic.cpp:99-146); kind = belief::RelaxKind (0 Jacobi, 1 GsLex, 2 GsRedBlack,
+        3 GsFourColor, 4 LineGsX, 5 LineGsY, 6 ZebraX, 7 AlternatingZebra)."""
+        x = f64(x).copy()
+        h = self._handle(A)
+        err = C.create_string_buffer(256)
+        rc = self.lib.ref_relax(kind, h, _d(f64(b)), _d(x), sweeps, nx, ny, err, 256)
+        self.lib.orc_matrix_free(h)
+        if rc != 1:
+            raise RuntimeError(err.value.decode())
+        return x
+
+    def ref_block_convergence(self, A: Csr, blocks, spectral=False):
+        """check_block_convergence (region_gabp.cpp:276-309): (rho, sufficient, singular_block)."""
+        offs, idx = _flatten_lists(blocks)
+        h = self._handle(A)
+        suf, sing = C.c_int(0), C.c_int(0)
+        rho = self.lib.ref_block_convergence(h, len(blocks), _i(offs), _i(idx), int(spectral), C.byref(suf),
+                                             C.byref(sing))
+        self.lib.orc_matrix_free(h)
+        return rho, bool(suf.value), sing.value
+
 
 class _Rng:
     def __init__(self, orc: Oracle, seed):
@@ -635,6 +693,65 @@ class _Hierarchy:
         return Report(st.value, it.value, hist[: hl.value].copy(), fl.value, x, det.value.decode())
 
 
+class _RefHierarchy:
+    """The reference's own belief::Hierarchy / v_cycle / mg_solve (multigrid.cpp), named problems only."""
+
+    def __init__(self, orc: Oracle, problem, J1, J2, params, smoother):
+        self.o = orc
+        keys = (C.c_char_p * max(1, len(params)))(*[k.encode() for k in params])
+        vals = f64(list(params.values()) or [0.0])
+        err = C.create_string_buffer(512)
+        self.h = orc.lib.ref_hier_create(problem.encode(), J1, J2, len(params), keys, _d(vals), smoother, err, 512)
+        if not self.h:
+            raise ValueError(err.value.decode())
+        self.n = orc.lib.ref_hier_level_n(self.h, 0)
+
+    def __del__(self):
+        try:
+            self.o.lib.ref_hier_free(self.h)
+        except Exception:
+            pass
+
+    @property
+    def num_levels(self):
+        return self.o.lib.ref_hier_num_levels(self.h)
+
+    def level_n(self, k):
+        return self.o.lib.ref_hier_level_n(self.h, k)
+
+    def frozen_ok(self, k):
+        return bool(self.o.lib.ref_hier_level_frozen_ok(self.h, k))
+
+    def fine_rhs(self):
+        b, e = np.zeros(self.n), np.zeros(self.n)
+        self.o.lib.ref_hier_fine_rhs(self.h, _d(b), _d(e))
+        return b, e
+
+    def v_cycle(self, pre, post, b, x, frozen=False):
+        x = f64(x).copy()
+        err = C.create_string_buffer(512)
+        rc = self.o.lib.ref_hier_vcycle(self.h, pre, post, int(frozen), _d(f64(b)), _d(x), err, 512)
+        if rc != 1:
+            raise RuntimeError(err.value.decode(), x)
+        return x
+
+    def cycle_flops_per_unknown(self, pre, post):
+        return self.o.lib.ref_hier_cycle_flops(self.h, pre, post)
+
+    def solve(self, pre, post, b, tol=2e-4, max_cycles=200, divergence_factor=1e6, frozen=False):
+        x = np.zeros(self.n)
+        hist = np.zeros(max_cycles + 1)
+        it, st, hl = C.c_int(0), C.c_int(0), C.c_int(0)
+        fl = C.c_double(0.0)
+        det = C.create_string_buffer(512)
+        rc = self.o.lib.ref_hier_solve(self.h, pre, post, int(frozen), _d(f64(b)), tol, max_cycles,
+                                       divergence_factor, _d(x), _d(hist), C.byref(it), C.byref(st), C.byref(fl),
+                                       C.byref(hl), det, 512)
+        if rc != 1:
+            raise RuntimeError(det.value.decode())
+        return Report(st.value, it.value, hist[: hl.value].copy(), fl.value, x, det.value.decode())
+
+
 def _flatten_lists(lists):
     offs = np.zeros(len(lists) + 1, np.int32)
     offs[1:] = np.cumsum([len(r) for r in lists])
@@ -646,29 +763,33 @@ class _Region:
     """Region GaBP restatement (region_gabp.cpp:30-198, region_restate.inc).  State is flat:
     Lambda blocks (row-major |l| x |l|) and m blocks per edge, in the engine's edge order."""
 
-    def __init__(self, orc: Oracle, A: Csr, large):
+    def __init__(self, orc: Oracle, A: Csr, large, prefix="orc_region"):
         self.o = orc
+        self.p = prefix  # "ref_region": the reference's own RegionGabpEngine (same flat state layout)
         offs, idx = _flatten_lists(large)
         h = orc._handle(A)
         err = C.create_string_buffer(512)
-        self.h = orc.lib.orc_region_create(h, len(large), _i(offs), _i(idx), err, 512)
+        self.h = self._f("create")(h, len(large), _i(offs), _i(idx), err, 512)
         orc.lib.orc_matrix_free(h)
         if not self.h:
             raise ValueError(err.value.decode())
         self.n = A.n
         ms = C.c_long(0)
-        self.lam_size = orc.lib.orc_region_state_size(self.h, C.byref(ms))
+        self.lam_size = self._f("state_size")(self.h, C.byref(ms))
         self.m_size = ms.value
+
+    def _f(self, name):
+        return getattr(self.o.lib, f"{self.p}_{name}")
 
     def __del__(self):
         try:
-            self.o.lib.orc_region_free(self.h)
+            self._f("free")(self.h)
         except Exception:
             pass
 
     @property
     def num_edges(self):
-        return self.o.lib.orc_region_num_edges(self.h)
+        return self._f("num_edges")(self.h)
 
     def edges(self):
         E = self.num_edges
@@ -691,7 +812,7 @@ class _Region:
     def sweep(self, b, lam, m, x, mode=0):
         """One sweep (mode 0 Sequential, 1 Flood), in place; returns (ok, err)."""
         err = C.create_string_buffer(512)
-        rc = self.o.lib.orc_region_sweep(self.h, _d(f64(b)), mode, _d(lam), _d(m), _d(x), err, 512)
+        rc = self._f("sweep")(self.h, _d(f64(b)), mode, _d(lam), _d(m), _d(x), err, 512)
         return rc == 1, err.value.decode()
 
     def solve(self, b, tol=2e-4, max_iter=10000, mode=0, divergence_factor=1e12):
@@ -699,17 +820,17 @@ class _Region:
         hist = np.zeros(max_iter + 1)
         it, st, fl = C.c_int(0), C.c_int(0), C.c_double(0)
         det = C.create_string_buffer(512)
-        self.o.lib.orc_region_solve(self.h, _d(f64(b)), tol, max_iter, mode, divergence_factor, _d(x), _d(hist),
+        self._f("solve")(self.h, _d(f64(b)), tol, max_iter, mode, divergence_factor, _d(x), _d(hist),
                                     C.byref(it), C.byref(st), C.byref(fl), det, 512)
         return Report(st.value, it.value, hist[: it.value + 1].copy(), fl.value, x, det.value.decode())
 
     def direct_message(self, b, lam, m, edge, nl=1):
         lo, mo = np.zeros(nl * nl), np.zeros(nl)
         err = C.create_string_buffer(512)
-        if self.o.lib.orc_region_direct_message(self.h, _d(f64(b)), _d(f64(lam)), _d(f64(m)), edge, _d(lo), _d(mo),
+        if self._f("direct_message")(self.h, _d(f64(b)), _d(f64(lam)), _d(f64(m)), edge, _d(lo), _d(mo),
                                                 err, 512) != 1:
             raise RuntimeError(err.value.decode())
         return lo, mo
 
     def flops(self, per_child=False):
-        return self.o.lib.orc_region_flops(self.h, int(per_child))
+        return self._f("flops")(self.h, int(per_child))
