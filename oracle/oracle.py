@@ -3,6 +3,8 @@
     Oracle.restatement()  -> oracle/liboracle.so          (own restatement, always available)
     Oracle.reference()    -> oracle/_ref/libbelief_ref.so  (reference sources compiled here;
                                                            None when it was never built)
+                             .ref_hierarchy / .ref_region / .ref_relax run the reference's own
+                             multigrid.cpp / region_gabp.cpp / classic.cpp (over oracle/eigen_shim)
 
 Only tests/, __graft_entry__.smoke() and bench.py's CPU legs import this module.  The CUDA
 product (paper_1904_04093_b200/) never does.

@@ -1,9 +1,12 @@
-// TEST INFRASTRUCTURE ONLY — C-ABI shim over the reference's own GaBP engine.
+// TEST INFRASTRUCTURE ONLY — C-ABI shim over the reference's own compiled sources.
 // Built by oracle/Makefile from the reference sources where they lie under
-// /root/reference/proj/core/src/{sparse,gabp,schedule,problems,analysis}.cpp (never copied into
-// this repo) into oracle/_ref/libbelief_ref.so (plus region.cpp, whose graph builder is Eigen-free).  multigrid.cpp and classic.cpp need Eigen, which
-// is absent, so the multigrid / Gauss-Seidel entry points run the Eigen-free restatement in
-// abi_impl.inc on top of the reference's compiled GabpEngine.
+// /root/reference/proj/core/src/*.cpp (all nine; never copied into this repo) into
+// oracle/_ref/libbelief_ref.so.  multigrid.cpp, classic.cpp and region_gabp.cpp include
+// <Eigen/Dense>, which is absent here: they compile over the minimal stand-in
+// oracle/eigen_shim/Eigen/Dense (see its header) and are exported below as ref_hier_*, ref_relax,
+// ref_region_*.  The orc_mg_* / orc_gs_sweeps / orc_region_* entry points of this library still run
+// the Eigen-free restatement in abi_impl.inc on top of the reference's compiled GabpEngine
+// (SURVEY.md §8(c)(i)-(ii)); tests/test_ref_full.py pins one to the other bit for bit.
 #include "belief/analysis.hpp"
 #include "belief/gabp.hpp"
 #include "belief/problems.hpp"

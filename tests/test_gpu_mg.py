@@ -4,7 +4,9 @@ Eigen-free CPU restatement of multigrid.cpp (over the reference's compiled GabpE
 checker.  Eigen's PartialPivLU is absent; the restatement's coarsest solve
 restates the GPU's documented arithmetic (partial-pivot LU -> explicit inverse -> 32-lane fma
 partial sums + xor butterfly, oracle/abi_impl.inc DenseLU), so whole V-cycles compare bit for bit:
-statuses, cycle counts, details, flop estimates, residual histories and x.
+statuses, cycle counts, details, flop estimates, residual histories and x.  Where oracle/_ref is
+built, test_mg_solve_matches_reference_multigrid_cpp compares with the reference's own
+multigrid.cpp (compiled over the Eigen stand-in with the same LU) directly, also bit for bit.
 """
 import numpy as np
 import pytest
@@ -182,6 +184,33 @@ def test_mg_solve_matches_cpu_restatement(orc, ref, golden, prob, J1, J2, sm, pr
     if key in meta["mg"]:
         rec = meta["mg"][key]
         assert (h.num_levels(), int(got.status), got.iterations) == (rec["levels"], rec["status"], rec["iterations"])
+
+
+@pytest.mark.parametrize("frozen", [False, True])
+@pytest.mark.parametrize("prob,J1,J2,sm,pre,post,params", MG_CASES + [("mixed", 5, 3, S.GabpFourColor, 0, 4, {})])
+def test_mg_solve_matches_reference_multigrid_cpp(ref, prob, J1, J2, sm, pre, post, params, frozen):
+    """The CUDA hierarchy against the reference's OWN belief::Hierarchy + mg_solve (multigrid.cpp
+    compiled where it lies over the Eigen stand-in, oracle/Makefile): level count after the
+    expansion probe, frozen flags, cycle flops, status, cycles, detail, flop estimate, the full
+    residual history and x, bit for bit."""
+    if ref is None or not ref.has_ref_full:
+        pytest.skip("oracle/_ref not built")
+    if frozen and int(sm) > 3:
+        pytest.skip("frozen applies to the GaBP smoothers")
+    hr = ref.ref_hierarchy(prob, J1, J2, params, int(sm))
+    b, _ = hr.fine_rhs()
+    tol = 1e-8 * np.abs(b).max()
+    want = hr.solve(pre, post, b, tol=tol, max_cycles=60, frozen=frozen)
+    h = g.Hierarchy(prob, J1, J2, params, sm)
+    assert h.fine_rhs().tobytes() == b.tobytes()
+    assert h.num_levels() == hr.num_levels
+    assert [h.level_frozen_ok(k) for k in range(h.num_levels())] == [hr.frozen_ok(k) for k in range(hr.num_levels)]
+    assert h.cycle_flops_per_unknown(g.CycleSpec(pre, post, sm)) == hr.cycle_flops_per_unknown(pre, post)
+    got = g.mg_solve(h, g.CycleSpec(pre, post, sm, frozen), b, g.MgSolveOptions(tol=tol, max_cycles=60))
+    assert (int(got.status), got.iterations, got.detail, got.flop_estimate) == (want.status, want.iterations,
+                                                                                want.detail, want.flop_estimate)
+    assert got.residual_history.tobytes() == want.residual_history.tobytes()
+    assert got.solution.tobytes() == want.solution.tobytes()
 
 
 @pytest.mark.parametrize("prob,sm,pre,post", [("poisson", S.GabpRedBlack, 1, 1), ("general", S.GabpRedBlack, 2, 2),

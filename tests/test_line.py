@@ -205,17 +205,33 @@ def _close(got, want, what, rtol=RTOL):
                                err_msg=what)
 
 
+def _checker(orc, ref, A, large):
+    """The reference's own RegionGabpEngine (region_gabp.cpp compiled over the Eigen stand-in) when
+    oracle/_ref is built, else its restatement (pinned to it bit for bit, tests/test_ref_full.py)."""
+    if ref is not None and ref.has_ref_full:
+        return ref.ref_region(A, large)
+    return orc.region(A, large)
+
+
+def _mg_checker(orc, ref, levels, nx):
+    """The reference's own GabpLine Hierarchy on the Poisson levels, else the restatement."""
+    if ref is not None and ref.has_ref_full:
+        J1 = int(np.log2(nx[0] + 1))
+        return ref.ref_hierarchy("poisson", J1, len(levels), {}, 4)
+    return orc.hierarchy(levels, nx, 4)
+
+
 GRIDS = [(6, 6, 0), (9, 5, 1), (1, 7, 2), (7, 1, 3), (33, 17, 4), (64, 48, 5)]
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("nx,ny,seed", GRIDS)
 @pytest.mark.parametrize("mode", [0, 1])
-def test_gpu_line_sweep_from_the_same_state(orc, nx, ny, seed, mode):
+def test_gpu_line_sweep_from_the_same_state(orc, ref, nx, ny, seed, mode):
     """Every sweep starts from the oracle's state: one sweep's messages and x, nonsymmetric grids."""
     A = _scaled_grid(orc, nx, ny, seed)
     b = np.random.RandomState(seed).uniform(-1, 1, A.n)
-    R = orc.region(A, orc.grid_lines(nx, ny))
+    R = _checker(orc, ref, A, orc.grid_lines(nx, ny))
     D = g.LineGabpEngine(g.SparseMatrix.of(A), nx, ny)
     assert D.num_edges == R.num_edges
     lr, mr = R.make_state()
@@ -231,13 +247,13 @@ def test_gpu_line_sweep_from_the_same_state(orc, nx, ny, seed, mode):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("mode", [0, 1])
-def test_gpu_line_sweep_long_lines(orc, mode):
+def test_gpu_line_sweep_long_lines(orc, ref, mode):
     """Rows longer than one 128-node warp tile and columns cut into many segments, so the scan
     carries between tiles and between segments are exercised (nonsymmetric, from the same state)."""
     nx, ny, seed = 160, 140, 7
     A = _scaled_grid(orc, nx, ny, seed)
     b = np.random.RandomState(seed).uniform(-1, 1, A.n)
-    R = orc.region(A, orc.grid_lines(nx, ny))
+    R = _checker(orc, ref, A, orc.grid_lines(nx, ny))
     D = g.LineGabpEngine(g.SparseMatrix.of(A), nx, ny)
     lr, mr = R.make_state()
     xr = np.zeros(A.n)
@@ -253,11 +269,11 @@ def test_gpu_line_sweep_long_lines(orc, mode):
 @pytest.mark.gpu
 @pytest.mark.parametrize("nx,ny", [(6, 6), (31, 17), (64, 64)])
 @pytest.mark.parametrize("mode", [0, 1])
-def test_gpu_line_sweeps_free_running(orc, nx, ny, mode):
+def test_gpu_line_sweeps_free_running(orc, ref, nx, ny, mode):
     """Twelve sweeps on their own state (Poisson, well conditioned): relative 1e-10 throughout."""
     A = orc.poisson5(nx, ny)
     b = orc.rng(nx + ny).vector(A.n)
-    R = orc.region(A, orc.grid_lines(nx, ny))
+    R = _checker(orc, ref, A, orc.grid_lines(nx, ny))
     D = g.LineGabpEngine(g.SparseMatrix.of(A), nx, ny)
     lr, mr = R.make_state()
     ld, md = D.make_state()
@@ -272,10 +288,10 @@ def test_gpu_line_sweeps_free_running(orc, nx, ny, mode):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("mode", [0, 1])
-def test_gpu_line_solve_matches_restatement(orc, mode):
+def test_gpu_line_solve_matches_restatement(orc, ref, mode):
     A = orc.poisson5(24, 20)
     b = orc.rng(8).vector(A.n)
-    R = orc.region(A, orc.grid_lines(24, 20))
+    R = _checker(orc, ref, A, orc.grid_lines(24, 20))
     D = g.LineGabpEngine(g.SparseMatrix.of(A), 24, 20)
     want = R.solve(b, tol=1e-10, mode=mode)
     got = D.solve(b, g.RegionSolveOptions(tol=1e-10, mode=mode))
@@ -286,21 +302,21 @@ def test_gpu_line_solve_matches_restatement(orc, mode):
 
 
 @pytest.mark.gpu
-def test_gpu_line_singular_local_system(orc):
+def test_gpu_line_singular_local_system(orc, ref):
     # row 0 of a 2x2 grid is [[1, 1], [1, 1]]: its local system is singular on the first sweep
     D2 = np.array([[1.0, 1.0, -0.5, 0.0], [1.0, 1.0, 0.0, -0.5], [-0.5, 0.0, 3.0, -1.0], [0.0, -0.5, -1.0, 3.0]])
     A = _csr_from_dense(orc, D2)
     b = np.ones(4)
-    want = orc.region(A, orc.grid_lines(2, 2)).solve(b)
+    want = _checker(orc, ref, A, orc.grid_lines(2, 2)).solve(b)
     got = g.LineGabpEngine(g.SparseMatrix.of(A), 2, 2).solve(b)
     assert want.status == 1 and want.detail.startswith("singular local system")
     assert (int(got.status), got.iterations, got.detail) == (want.status, want.iterations, want.detail)
 
 
 @pytest.mark.gpu
-def test_gpu_line_smoother_multigrid_matches_restatement(orc):
+def test_gpu_line_smoother_multigrid_matches_restatement(orc, ref):
     levels, nx, b = _poisson_levels((5, 4, 3))
-    want = orc.hierarchy(levels, nx, 4).solve(1, 1, b, tol=1e-9)
+    want = _mg_checker(orc, ref, levels, nx).solve(1, 1, b, tol=1e-9)
     H = g.Hierarchy("poisson", 5, 3, smoother=g.MgSmoother.GabpLine)
     got = g.mg_solve(H, g.CycleSpec(1, 1, g.MgSmoother.GabpLine), b, g.MgSolveOptions(tol=1e-9))
     assert (int(got.status), got.iterations) == (want.status, want.iterations)
@@ -317,10 +333,10 @@ def test_gpu_line_rejects_like_the_reference_on_the_device_path(orc):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("pre,post", [(2, 2), (0, 3), (3, 1)])
-def test_gpu_line_smoother_multi_sweep_cycles(orc, pre, post):
+def test_gpu_line_smoother_multi_sweep_cycles(orc, ref, pre, post):
     """Recorded factors for several sweeps per smoothing call (mean-only fast path)."""
     levels, nx, b = _poisson_levels((5, 4, 3))
-    want = orc.hierarchy(levels, nx, 4).solve(pre, post, b, tol=1e-9)
+    want = _mg_checker(orc, ref, levels, nx).solve(pre, post, b, tol=1e-9)
     H = g.Hierarchy("poisson", 5, 3, smoother=g.MgSmoother.GabpLine)
     got = g.mg_solve(H, g.CycleSpec(pre, post, g.MgSmoother.GabpLine), b, g.MgSolveOptions(tol=1e-9))
     assert (int(got.status), got.iterations) == (want.status, want.iterations)
