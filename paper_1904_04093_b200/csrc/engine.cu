@@ -250,16 +250,16 @@ void Engine::launch_aggregate(const double* b, const double2* msg, double* x, do
 }
 
 void Engine::launch_residual(const double* b, const double* x, double* r, unsigned long long* rmax, int mode,
-                             long long xstride) {
+                             long long xstride, int rb_nx, unsigned long long* rpart) {
     if (n == 0) return;
     const unsigned g = nblk(n);
     if (layout == BGABP_LAYOUT_DIA) {
         if (dia.uniform) {
-            DIA_SWITCH(S, k_residual_dia<SS, true, true><<<g, 256, 0, st>>>(dia, b, x, r, rmax, d_ctrl, mode, xstride));
+            DIA_SWITCH(S, k_residual_dia<SS, true, true><<<g, 256, 0, st>>>(dia, b, x, r, rmax, d_ctrl, mode, xstride, rb_nx, rpart));
         } else if (symmetric) {
-            DIA_SWITCH(S, k_residual_dia<SS, true><<<g, 256, 0, st>>>(dia, b, x, r, rmax, d_ctrl, mode, xstride));
+            DIA_SWITCH(S, k_residual_dia<SS, true><<<g, 256, 0, st>>>(dia, b, x, r, rmax, d_ctrl, mode, xstride, rb_nx, rpart));
         } else {
-            DIA_SWITCH(S, k_residual_dia<SS><<<g, 256, 0, st>>>(dia, b, x, r, rmax, d_ctrl, mode, xstride));
+            DIA_SWITCH(S, k_residual_dia<SS><<<g, 256, 0, st>>>(dia, b, x, r, rmax, d_ctrl, mode, xstride, rb_nx, rpart));
         }
     } else {
         k_residual_csr<<<g, 256, 0, st>>>(csr, b, x, r, rmax, d_ctrl, mode, xstride);

@@ -169,8 +169,11 @@ struct Engine {
     void launch_flood(const double* b, double2* m0, double2* m1, double* x, int mode, bool delta,
                       long long xstride = 0);
     void launch_aggregate(const double* b, const double2* msg, double* x, double* beta, unsigned long long* npiv);
+    // DIA only: rb_nx > 0, r written colour-compact for rb_smooth_add(r, ..., true); rpart, one
+    // max |r| per 256-node block (residual_blocks() entries) instead of the atomic into rmax
     void launch_residual(const double* b, const double* x, double* r, unsigned long long* rmax, int mode,
-                         long long xstride = 0);
+                         long long xstride = 0, int rb_nx = 0, unsigned long long* rpart = nullptr);
+    unsigned residual_blocks() const { return (unsigned)((n + 255) / 256); }
     void launch_levels(const Levels& L, const double* b, double2* msg, double* x, bool delta,
                        unsigned long long* dslot, int mode, long long xstride = 0);
     void launch_gs_levels(const Levels& L, const double* b, double* x);
@@ -192,7 +195,7 @@ struct Engine {
     int rb_pre_sweeps = 0;
     bool rb_pre_failed = false;
     bool rb_precompute(int sweeps);
-    void rb_smooth_add(const double* r, int sweeps, double* x);
+    void rb_smooth_add(const double* r, int sweeps, double* x, bool r_compact = false);
     // pipelined lexicographic sweep on 5-point grids (seq_kernels.cuh)
     bool grid5 = false;  // DIA offsets {-nx,-1,+1,+nx} with no wrap-around edges at row ends
     int grid5_nx = 0;

@@ -130,16 +130,38 @@ __global__ void k_mg_clear(Ctrl* const* c, int nl) {
     }
 }
 
-// out[0] = *rres (the stop test's residual bits) or 0; out[1] = min over halted levels of
-// (fail_seq << 32 | level), kNone if no level halted: the first failure in execution order
-__global__ void k_mg_summary(Ctrl* const* c, int nl, const unsigned long long* rres, unsigned long long* out) {
+// out[0] = the stop test's residual bits: *rres, or the max of the npart per-block values in
+// rpart (k_residual_dia's rpart), or 0; out[1] = min over halted levels of
+// (fail_seq << 32 | level), kNone if no level halted: the first failure in execution order.
+// One block of 1024 threads.
+__global__ void __launch_bounds__(1024) k_mg_summary(Ctrl* const* c, int nl, const unsigned long long* rres,
+                                                     const unsigned long long* rpart, int npart,
+                                                     unsigned long long* out) {
+    __shared__ unsigned long long part[32];
+    unsigned long long m = 0ull;
+    if (rpart) {
+        for (int i = threadIdx.x; i < npart; i += blockDim.x) {
+            const unsigned long long v = rpart[i];
+            m = v > m ? v : m;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long other = __shfl_xor_sync(0xffffffffu, m, o);
+            m = other > m ? other : m;
+        }
+        if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = m;
+        __syncthreads();
+    }
+    if (threadIdx.x != 0) return;
+    if (rpart)
+        for (int k = 1; k < (int)(blockDim.x >> 5); ++k) m = part[k] > m ? part[k] : m;
     unsigned long long best = kNone;
     for (int k = 0; k < nl; ++k)
         if (c[k]->halt) {
             const unsigned long long key = ((unsigned long long)(unsigned)c[k]->fail_seq << 32) | (unsigned)k;
             best = key < best ? key : best;
         }
-    out[0] = rres ? *rres : 0ull;
+    out[0] = rpart ? m : (rres ? *rres : 0ull);
     out[1] = best;
 }
 
@@ -167,6 +189,7 @@ struct bgmg {
     int seq = 0;
     Ctrl** d_ctrls = nullptr;               // every level's d_ctrl, for k_mg_clear / k_mg_summary
     unsigned long long* d_sum = nullptr;    // k_mg_summary output
+    unsigned long long* d_rpart = nullptr;  // per-block max |r| of the stop test's residual (DIA fine level)
     unsigned long long* h_sum = nullptr;    // pinned copy of it
     std::vector<CycleGraph> graphs;
     bool use_graphs = true;
@@ -203,6 +226,7 @@ struct bgmg {
             if (g.exec) cudaGraphExecDestroy(g.exec);
         if (d_ctrls) cudaFree(d_ctrls);
         if (d_sum) cudaFree(d_sum);
+        if (d_rpart) cudaFree(d_rpart);
         if (h_sum) cudaFreeHost(h_sum);
         levels.clear();
         if (d_inv) cudaFree(d_inv);
@@ -215,6 +239,13 @@ struct bgmg {
     Engine& E(int k) { return *levels[k].E; }
     int nl() const { return (int)levels.size(); }
 
+    // whether smooth(k, ..., sweeps, frozen) runs the recorded red-black sweeps (rb_smooth_add)
+    bool smooth_uses_rb(int k, int sweeps, bool frozen) {
+        Engine& L = E(k);
+        return sweeps > 0 && is_gabp(smoother) && !(frozen && levels[k].frozen_ok) &&
+               L.rb_applicable(levels[k].sched) && L.rb_ready && L.rb_pre_sweeps >= sweeps;
+    }
+
     // Hierarchy::smooth (multigrid.cpp:163-208)
     void smooth(int k, const double* b, double* x, int sweeps, bool frozen, bool have_r = false) {
         if (sweeps <= 0) return;
@@ -223,10 +254,12 @@ struct bgmg {
         const unsigned g = nblk_host(L.n);
         ++seq;
         if (is_gabp(smoother)) {
-            if (!have_r) L.launch_residual(b, x, L.d_r, nullptr, MODE_PLAIN);
-            if (!(frozen && levels[k].frozen_ok) && L.rb_applicable(levels[k].sched) && L.rb_ready &&
-                L.rb_pre_sweeps >= sweeps) {
-                L.rb_smooth_add(L.d_r, sweeps, x);  // recorded lambda/sigma, x += e fused
+            // the recorded red-black smoother reads r per colour: have the residual write it so
+            const bool rb = smooth_uses_rb(k, sweeps, frozen);
+            if (have_r && fine_r_compact != rb) have_r = false;
+            if (!have_r) L.launch_residual(b, x, L.d_r, nullptr, MODE_PLAIN, 0, rb ? levels[k].sched.nx : 0);
+            if (rb) {
+                L.rb_smooth_add(L.d_r, sweeps, x, true);  // recorded lambda/sigma, x += e fused
                 return;
             }
             if (frozen && levels[k].frozen_ok) {
@@ -300,7 +333,7 @@ struct bgmg {
     // first smoother failure of the last cycle, in execution order; "" if none (one summary read;
     // the per-level scan only when some level halted)
     std::string failure() {
-        k_mg_summary<<<1, 1, 0, st>>>(d_ctrls, nl(), nullptr, d_sum);
+        k_mg_summary<<<1, 32, 0, st>>>(d_ctrls, nl(), nullptr, nullptr, 0, d_sum);
         ck(cudaMemcpyAsync(h_sum, d_sum, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st), "D2H");
         ck(cudaStreamSynchronize(st), "sync");
         return h_sum[1] == kNone ? std::string() : failure_detail();
@@ -440,14 +473,29 @@ struct bgmg {
     // the stop test's residual r = b - A x also serves the next cycle's first smoothing call (same
     // x, same kernel): fine_r_for records which (b, x) it belongs to
     const double *fine_r_b = nullptr, *fine_r_x = nullptr;
+    bool fine_r_compact = false;  // ... stored colour-compact (the next pre-smoothing is recorded red-black)
+
+    // the stop test's residual, laid out for the pre-smoothing call of a following cycle.  On a
+    // DIA fine level max |r| is left as one value per block in d_rpart (true is returned; the
+    // summary kernel folds them), otherwise reduced into d_ctrl->red[2].
+    bool stop_test_residual(const bgmg_cycle* spec, const double* b, const double* x) {
+        Engine& L = E(0);
+        fine_r_compact = spec && smooth_uses_rb(0, spec->pre, spec->frozen != 0);
+        const bool parts = spec && L.layout == BGABP_LAYOUT_DIA && L.n > 0;
+        if (parts && !d_rpart)
+            ck(cudaMalloc(&d_rpart, sizeof(unsigned long long) * L.residual_blocks()), "malloc");
+        if (!parts) ck(cudaMemsetAsync(&L.d_ctrl->red[2], 0, sizeof(unsigned long long), st), "memset");
+        L.launch_residual(b, x, L.d_r, &L.d_ctrl->red[2], MODE_PLAIN, 0, fine_r_compact ? levels[0].sched.nx : 0,
+                          parts ? d_rpart : nullptr);
+        fine_r_b = b;
+        fine_r_x = x;
+        return parts;
+    }
 
     double residual_inf(const double* b, const double* x) {
         Engine& L = E(0);
         if (L.n == 0) return 0.0;
-        ck(cudaMemsetAsync(&L.d_ctrl->red[2], 0, sizeof(unsigned long long), st), "memset");
-        L.launch_residual(b, x, L.d_r, &L.d_ctrl->red[2], MODE_PLAIN);
-        fine_r_b = b;
-        fine_r_x = x;
+        stop_test_residual(nullptr, b, x);
         unsigned long long r;
         ck(cudaMemcpyAsync(&r, &L.d_ctrl->red[2], sizeof(r), cudaMemcpyDeviceToHost, st), "D2H");
         ck(cudaStreamSynchronize(st), "sync");
@@ -506,11 +554,9 @@ struct bgmg {
                 v_cycle_dev(spec, b, x);
             // stop test and failure summary in one read
             Engine& L = E(0);
-            ck(cudaMemsetAsync(&L.d_ctrl->red[2], 0, sizeof(unsigned long long), st), "memset");
-            L.launch_residual(b, x, L.d_r, &L.d_ctrl->red[2], MODE_PLAIN);
-            fine_r_b = b;
-            fine_r_x = x;
-            k_mg_summary<<<1, 1, 0, st>>>(d_ctrls, nl(), &L.d_ctrl->red[2], d_sum);
+            const bool parts = stop_test_residual(&spec, b, x);
+            k_mg_summary<<<1, 1024, 0, st>>>(d_ctrls, nl(), &L.d_ctrl->red[2], parts ? d_rpart : nullptr,
+                                             (int)L.residual_blocks(), d_sum);
             ck(cudaMemcpyAsync(h_sum, d_sum, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st), "D2H");
             ck(cudaStreamSynchronize(st), "sync");
             const double r = bits2d(h_sum[0]);

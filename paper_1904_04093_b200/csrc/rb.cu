@@ -126,24 +126,25 @@ bool Engine::rb_precompute(int sweeps) {
 }
 
 // e from `sweeps` cold red-black mean-only sweeps on A e = r, then x += e (multigrid.cpp:180-188)
-void Engine::rb_smooth_add(const double* r, int sweeps, double* x) {
+void Engine::rb_smooth_add(const double* r, int sweeps, double* x, bool r_compact) {
     if (n == 0 || sweeps <= 0) return;
     double* mR = reinterpret_cast<double*>(d_rbmsg);
     double* mB = mR + 4 * (size_t)rb.nR;
     const unsigned gr = nblk_host(rb.nR), gb = nblk_host(std::max(rb.nB, 1));
+    const int rc = r_compact ? 1 : 0;  // r as launch_residual(..., rb_nx) wrote it
     for (int s = 0; s < sweeps; ++s) {
         const bool first = s == 0, last = s + 1 == sweeps;
         const double* recR = rb_lamrec[s];
         const double* recB = rb_lamrec[s] + 4 * (size_t)rb.nR;
         const double* sR = rb_sigrec[s];
         const double* sB = rb_sigrec[s] + rb.nR;
-        if (first && last) k_rb_mean_half<0, true, true><<<gr, 256, 0, st>>>(rb, r, mR, mB, recR, sR, x);
-        else if (first) k_rb_mean_half<0, true, false><<<gr, 256, 0, st>>>(rb, r, mR, mB, recR, sR, x);
-        else if (last) k_rb_mean_half<0, false, true><<<gr, 256, 0, st>>>(rb, r, mR, mB, recR, sR, x);
-        else k_rb_mean_half<0, false, false><<<gr, 256, 0, st>>>(rb, r, mR, mB, recR, sR, x);
+        if (first && last) k_rb_mean_half<0, true, true><<<gr, 256, 0, st>>>(rb, r, mR, mB, recR, sR, x, rc);
+        else if (first) k_rb_mean_half<0, true, false><<<gr, 256, 0, st>>>(rb, r, mR, mB, recR, sR, x, rc);
+        else if (last) k_rb_mean_half<0, false, true><<<gr, 256, 0, st>>>(rb, r, mR, mB, recR, sR, x, rc);
+        else k_rb_mean_half<0, false, false><<<gr, 256, 0, st>>>(rb, r, mR, mB, recR, sR, x, rc);
         if (rb.nB > 0) {
-            if (last) k_rb_mean_half<1, false, true><<<gb, 256, 0, st>>>(rb, r, mB, mR, recB, sB, x);
-            else k_rb_mean_half<1, false, false><<<gb, 256, 0, st>>>(rb, r, mB, mR, recB, sB, x);
+            if (last) k_rb_mean_half<1, false, true><<<gb, 256, 0, st>>>(rb, r, mB, mR, recB, sB, x, rc);
+            else k_rb_mean_half<1, false, false><<<gb, 256, 0, st>>>(rb, r, mB, mR, recB, sB, x, rc);
         }
     }
 }

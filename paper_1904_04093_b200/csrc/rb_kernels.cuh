@@ -200,7 +200,8 @@ static __global__ void __launch_bounds__(256) k_rb_lambda_half(RbP P, double* la
 template <int COLOUR, bool FIRST, bool LAST>
 static __global__ void __launch_bounds__(256) k_rb_mean_half(RbP P, const double* __restrict__ r, double* m_mine,
                                                             double* m_other, const double* __restrict__ lam_rec,
-                                                            const double* __restrict__ sig_rec, double* __restrict__ x) {
+                                                            const double* __restrict__ sig_rec, double* __restrict__ x,
+                                                            int r_compact) {
     const int nc = COLOUR == 0 ? P.nR : P.nB, no = COLOUR == 0 ? P.nB : P.nR;
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nc) return;
@@ -208,7 +209,8 @@ static __global__ void __launch_bounds__(256) k_rb_mean_half(RbP P, const double
     const uint32_t mk = P.mask[COLOUR][q];
     // all loads issued before the mask is known (slot arrays are full size; the mask still
     // selects every term): predicated loads wait for the mask's DRAM round trip first
-    double acc = r[g], in[4], lam[4];
+    // r_compact: r is stored per colour (k_residual_dia rb_nx), this colour's half contiguous
+    double acc = r[r_compact ? (COLOUR ? P.nR : 0) + q : g], in[4], lam[4];
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
         in[s] = FIRST ? 0.0 : m_mine[s * nc + q];

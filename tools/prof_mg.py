@@ -28,3 +28,15 @@ rep = g.mg_solve_device(h, g.CycleSpec(2, 2, sm), b.data_ptr(), x.data_ptr(),
                         g.MgSolveOptions(tol=1e-8 * float(np.abs(levels[0].b).max()), max_cycles=a.cycles))
 torch.cuda.synchronize()
 print(rep.status, rep.iterations)
+if os.environ.get("PROF_MG_TIME"):
+    import time
+    tol_t = 1e-8 * float(np.abs(levels[0].b).max())
+    for _ in range(2):
+        x.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep = g.mg_solve_device(h, g.CycleSpec(2, 2, sm), b.data_ptr(), x.data_ptr(),
+                                g.MgSolveOptions(tol=tol_t, max_cycles=int(os.environ["PROF_MG_TIME"])))
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        print(f"timed: {rep.status} {rep.iterations} cycles, {dt:.4f} s, {1e3 * dt / max(rep.iterations, 1):.4f} ms/cycle")
