@@ -210,11 +210,15 @@ static __global__ void __launch_bounds__(256) k_rb_mean_half(RbP P, const double
     // all loads issued before the mask is known (slot arrays are full size; the mask still
     // selects every term): predicated loads wait for the mask's DRAM round trip first
     // r_compact: r is stored per colour (k_residual_dia rb_nx), this colour's half contiguous
+    // The black phase of the last sweep sends nothing: the call ends there and its messages are
+    // never read (every smoothing call starts cold), so neither the recorded lambda of that
+    // visit is loaded nor the four messages stored (64 of the phase's 150 B per node).
+    constexpr bool SEND = !(LAST && COLOUR == 1);
     double acc = r[r_compact ? (COLOUR ? P.nR : 0) + q : g], in[4], lam[4];
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
         in[s] = FIRST ? 0.0 : m_mine[s * nc + q];
-        lam[s] = __ldg(lam_rec + s * nc + q);
+        lam[s] = SEND ? __ldg(lam_rec + s * nc + q) : 0.0;
     }
     const double sg = LAST ? __ldg(sig_rec + q) : 1.0;
     const double xg = LAST ? x[g] : 0.0;
@@ -224,9 +228,11 @@ static __global__ void __launch_bounds__(256) k_rb_mean_half(RbP P, const double
         else acc = dadd(acc, in[s]);  // (adding a zero would turn acc = -0 into +0)
     }
     if (LAST) x[g] = dadd(xg, ddiv(acc, sg));
+    if (SEND) {
 #pragma unroll
-    for (int s = 0; s < 4; ++s)
-        if (mk & (1u << (16 + s))) m_other[(3 - s) * no + rb_other(g, s, P.nx)] = dmul(lam[s], dsub(acc, in[s]));
+        for (int s = 0; s < 4; ++s)
+            if (mk & (1u << (16 + s))) m_other[(3 - s) * no + rb_other(g, s, P.nx)] = dmul(lam[s], dsub(acc, in[s]));
+    }
 }
 
 // message state natural DIA [4][n] <-> colour-compact ([4][nR] reds, then [4][nB] blacks)
