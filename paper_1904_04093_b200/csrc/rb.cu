@@ -132,7 +132,12 @@ void Engine::rb_smooth_add(const double* r, int sweeps, double* x, bool r_compac
     double* mB = mR + 4 * (size_t)rb.nR;
     const unsigned gr = nblk_host(rb.nR), gb = nblk_host(std::max(rb.nB, 1));
     const int rc = r_compact ? 1 : 0;  // r as launch_residual(..., rb_nx) wrote it
-    for (int s = 0; s < sweeps; ++s) {
+    int s0 = 0;
+    if (sweeps >= 2 && rb.nB > 0) {  // sweep 1, both colours, one launch (k_rb_mean_first_pair)
+        k_rb_mean_first_pair<<<gb, 256, 0, st>>>(rb, r, mR, rb_lamrec[0], rc);
+        s0 = 1;
+    }
+    for (int s = s0; s < sweeps; ++s) {
         const bool first = s == 0, last = s + 1 == sweeps;
         const double* recR = rb_lamrec[s];
         const double* recB = rb_lamrec[s] + 4 * (size_t)rb.nR;

@@ -235,6 +235,52 @@ static __global__ void __launch_bounds__(256) k_rb_mean_half(RbP P, const double
     }
 }
 
+// The first sweep's red and black phases in one launch over the black nodes.  After a cold start
+// a red node's first messages depend on nothing but its own r (acc = r, every in-message zero),
+// so each black node forms its four in-messages itself from the neighbours' r and recorded
+// lambda (the same operations the red phase performs: r + 0 per in-slot, (acc - 0) * lambda) and
+// goes on as the black phase does.  The red phase's message stores and the black phase's
+// message loads (64 B per red-black pair) never reach memory; every recorded lambda entry of
+// the reds is still read exactly once, by the node it points to.  Sweeps >= 2 only (with one
+// sweep the red nodes' x += e needs its own visit).
+static __global__ void __launch_bounds__(256) k_rb_mean_first_pair(RbP P, const double* __restrict__ r,
+                                                                  double* m_red, const double* __restrict__ lam_rec,
+                                                                  int r_compact) {
+    const int nR = P.nR, nB = P.nB;
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nB) return;
+    const int g = rb_nat(P, q, 1);
+    const uint32_t mk = P.mask[1][q];
+    const double* __restrict__ lamR = lam_rec;                    // [4][nR]
+    const double* __restrict__ lamB = lam_rec + 4 * (size_t)nR;   // [4][nB]
+    const int off[4] = {-P.nx, -1, 1, P.nx};
+    double acc = r[r_compact ? nR + q : g], in[4], lam[4];
+    int kq[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {  // loads independent of the mask (indices clamped)
+        const int k = g + off[s];
+        const int kc = k < 0 ? 0 : (k > 2 * nR - 2 ? 2 * nR - 2 : k);  // clamped into the reds' natural range
+        kq[s] = kc >> 1;
+        const double rk = r[r_compact ? kq[s] : rb_nat(P, kq[s], 0)];
+        const uint32_t mkk = __ldg(P.mask[0] + kq[s]);
+        const double lk = __ldg(lamR + (size_t)(3 - s) * nR + kq[s]);
+        lam[s] = __ldg(lamB + (size_t)s * nB + q);
+        // the red neighbour's visit (k_rb_mean_half<0, FIRST>): acc = r (+ 0 per in-slot), message
+        // = lambda * (acc - 0)
+        double ak = rk;
+        if (mkk & 0xfu) ak = dadd(ak, 0.0);
+        in[s] = dmul(lk, dsub(ak, 0.0));
+    }
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        if (!(mk & (1u << s))) in[s] = 0.0;
+        else acc = dadd(acc, in[s]);
+    }
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+        if (mk & (1u << (16 + s))) m_red[(3 - s) * nR + rb_other(g, s, P.nx)] = dmul(lam[s], dsub(acc, in[s]));
+}
+
 // message state natural DIA [4][n] <-> colour-compact ([4][nR] reds, then [4][nB] blacks)
 template <bool TO_COMPACT>
 static __global__ void k_rb_convert(int n, int nR, int nx, double2* nat, double2* cmp) {
