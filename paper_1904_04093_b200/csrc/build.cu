@@ -208,6 +208,7 @@ void Engine::build_dia_device(const int* ro_, const int* ci_, const double* v_) 
     phase("  dia: fill + facts kernels");
     symmetric = hf.asym == 0u;
     grid5 = gx > 0 && hf.wrap == 0u;
+    grid5_full = grid5 && nnz == 5ll * n - 2ll * gx - 2ll * (n / gx);
     dia.full5nx = dia.full5ny = 0;
     if (grid5 && symmetric && nnz == 5ll * n - 2ll * gx - 2ll * (n / gx) &&  // every in-grid entry present
         !getenv("BGABP_NO_FULL5")) {                                          // (A/B knob)

@@ -199,6 +199,7 @@ struct Engine {
     // pipelined lexicographic sweep on 5-point grids (seq_kernels.cuh)
     bool grid5 = false;  // DIA offsets {-nx,-1,+1,+nx} with no wrap-around edges at row ends
     int grid5_nx = 0;
+    bool grid5_full = false;  // ... and every in-grid neighbour entry is present (both directions)
     int* d_progress = nullptr;
     bool seq_applicable(const bgabp_schedule& s) const {
         return grid5 && s.kind == BGABP_SCHED_SEQUENTIAL && n > 0;

@@ -1,5 +1,7 @@
 // Host side of the colour-compact red-black path (rb_kernels.cuh).
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "engine.h"
 
@@ -137,7 +139,14 @@ void Engine::rb_smooth_add(const double* r, int sweeps, double* x, bool r_compac
         k_rb_mean_first_pair<<<gb, 256, 0, st>>>(rb, r, mR, rb_lamrec[0], rc);
         s0 = 1;
     }
+    // the last sweep's two phases in one launch (k_rb_mean_last_pair) on full grids
+    static const bool pair_on = !(getenv("BGABP_RB_LAST_PAIR") && std::string(getenv("BGABP_RB_LAST_PAIR")) == "0");
+    const bool last_pair = pair_on && s0 == 1 && grid5_full && rb.nx >= 2;
     for (int s = s0; s < sweeps; ++s) {
+        if (last_pair && s + 1 == sweeps) {
+            k_rb_mean_last_pair<<<gb, 256, 0, st>>>(rb, r, mR, rb_lamrec[s], rb_sigrec[s], x, rc);
+            break;
+        }
         const bool first = s == 0, last = s + 1 == sweeps;
         const double* recR = rb_lamrec[s];
         const double* recB = rb_lamrec[s] + 4 * (size_t)rb.nR;

@@ -281,6 +281,60 @@ static __global__ void __launch_bounds__(256) k_rb_mean_first_pair(RbP P, const 
         if (mk & (1u << (16 + s))) m_red[(3 - s) * nR + rb_other(g, s, P.nx)] = dmul(lam[s], dsub(acc, in[s]));
 }
 
+// The last sweep's red and black phases in one launch over the black nodes (sweeps >= 2, grids
+// with every in-grid neighbour present).  The last black visit needs from each red neighbour k
+// only k's message to it, lambda * (acc_k - in_k), and acc_k is r_k plus k's four in-messages --
+// which are in memory (the previous black phase put them there) and shared by k's four black
+// neighbours through L1 / L2.  So each black node rebuilds its neighbours' accumulators (the red
+// visit's own operations in its own order), takes its four in-messages from them and finishes;
+// the red node's x += e is done by exactly one of its neighbours (the eastern one, else the
+// western: the pair is adjacent in x).  The red phase's message stores and this phase's message
+// loads, and the half-used sectors of two strided passes over x, never reach DRAM: 136 instead
+// of 232 B per red-black pair.
+static __global__ void __launch_bounds__(256) k_rb_mean_last_pair(RbP P, const double* __restrict__ r,
+                                                                 const double* __restrict__ m_red,
+                                                                 const double* __restrict__ lam_rec,
+                                                                 const double* __restrict__ sig_rec,
+                                                                 double* __restrict__ x, int r_compact) {
+    const int nR = P.nR, nB = P.nB;
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nB) return;
+    const int g = rb_nat(P, q, 1);
+    const uint32_t mk = P.mask[1][q];
+    const int off[4] = {-P.nx, -1, 1, P.nx};
+    double acc = r[r_compact ? nR + q : g];
+    const double sg = __ldg(sig_rec + nR + q), xg = x[g];
+    double in[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {  // loads independent of the masks (indices clamped)
+        const int k = g + off[s];
+        const int kc = k < 0 ? 0 : (k > 2 * nR - 2 ? 2 * nR - 2 : k);
+        const int kq = kc >> 1, kn = rb_nat(P, kq, 0);
+        const uint32_t mkk = __ldg(P.mask[0] + kq);
+        double ak = r[r_compact ? kq : kn];
+        const double lk = __ldg(lam_rec + (size_t)(3 - s) * nR + kq);
+        double ik[4];
+#pragma unroll
+        for (int s2 = 0; s2 < 4; ++s2) ik[s2] = m_red[(size_t)s2 * nR + kq];
+        const bool ew = s == 1 || s == 2;  // only an eastern / western neighbour can own k
+        const double sk = ew ? __ldg(sig_rec + kq) : 1.0, xk = ew ? x[kn] : 0.0;
+#pragma unroll
+        for (int s2 = 0; s2 < 4; ++s2) {  // k's visit (k_rb_mean_half<0, false, true>)
+            if (!(mkk & (1u << s2))) ik[s2] = 0.0;
+            else ak = dadd(ak, ik[s2]);
+        }
+        in[s] = dmul(lk, dsub(ak, ik[3 - s]));
+        // k's x += e: by its eastern neighbour (k's slot 2, reached from here as s = 1), else the western
+        if (ew && (mk & (1u << s)) && (s == 1 || !(mkk & (1u << 2)))) x[kn] = dadd(xk, ddiv(ak, sk));
+    }
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        if (!(mk & (1u << s))) in[s] = 0.0;
+        else acc = dadd(acc, in[s]);
+    }
+    x[g] = dadd(xg, ddiv(acc, sg));
+}
+
 // message state natural DIA [4][n] <-> colour-compact ([4][nR] reds, then [4][nB] blacks)
 template <bool TO_COMPACT>
 static __global__ void k_rb_convert(int n, int nR, int nx, double2* nat, double2* cmp) {
