@@ -305,27 +305,37 @@ static __global__ void __launch_bounds__(256) k_rb_mean_last_pair(RbP P, const d
     double acc = r[r_compact ? nR + q : g];
     const double sg = __ldg(sig_rec + nR + q), xg = x[g];
     double in[4];
+    // every load first (independent of the masks, indices clamped), then the arithmetic: the
+    // kernel is a gather of ~36 values per node, so what counts is how many are in flight
+    int kn[4];
+    uint32_t mkk[4];
+    double ak[4], lk[4], ik[4][4], sk[4], xk[4];
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {  // loads independent of the masks (indices clamped)
+    for (int s = 0; s < 4; ++s) {
         const int k = g + off[s];
         const int kc = k < 0 ? 0 : (k > 2 * nR - 2 ? 2 * nR - 2 : k);
-        const int kq = kc >> 1, kn = rb_nat(P, kq, 0);
-        const uint32_t mkk = __ldg(P.mask[0] + kq);
-        double ak = r[r_compact ? kq : kn];
-        const double lk = __ldg(lam_rec + (size_t)(3 - s) * nR + kq);
-        double ik[4];
+        const int kq = kc >> 1;
+        kn[s] = rb_nat(P, kq, 0);
+        mkk[s] = __ldg(P.mask[0] + kq);
+        ak[s] = r[r_compact ? kq : kn[s]];
+        lk[s] = __ldg(lam_rec + (size_t)(3 - s) * nR + kq);
 #pragma unroll
-        for (int s2 = 0; s2 < 4; ++s2) ik[s2] = m_red[(size_t)s2 * nR + kq];
+        for (int s2 = 0; s2 < 4; ++s2) ik[s][s2] = m_red[(size_t)s2 * nR + kq];
         const bool ew = s == 1 || s == 2;  // only an eastern / western neighbour can own k
-        const double sk = ew ? __ldg(sig_rec + kq) : 1.0, xk = ew ? x[kn] : 0.0;
+        sk[s] = ew ? __ldg(sig_rec + kq) : 1.0;
+        xk[s] = ew ? x[kn[s]] : 0.0;
+    }
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
 #pragma unroll
         for (int s2 = 0; s2 < 4; ++s2) {  // k's visit (k_rb_mean_half<0, false, true>)
-            if (!(mkk & (1u << s2))) ik[s2] = 0.0;
-            else ak = dadd(ak, ik[s2]);
+            if (!(mkk[s] & (1u << s2))) ik[s][s2] = 0.0;
+            else ak[s] = dadd(ak[s], ik[s][s2]);
         }
-        in[s] = dmul(lk, dsub(ak, ik[3 - s]));
+        in[s] = dmul(lk[s], dsub(ak[s], ik[s][3 - s]));
         // k's x += e: by its eastern neighbour (k's slot 2, reached from here as s = 1), else the western
-        if (ew && (mk & (1u << s)) && (s == 1 || !(mkk & (1u << 2)))) x[kn] = dadd(xk, ddiv(ak, sk));
+        if ((s == 1 || s == 2) && (mk & (1u << s)) && (s == 1 || !(mkk[s] & (1u << 2))))
+            x[kn[s]] = dadd(xk[s], ddiv(ak[s], sk[s]));
     }
 #pragma unroll
     for (int s = 0; s < 4; ++s) {

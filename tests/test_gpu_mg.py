@@ -153,7 +153,11 @@ def _oracle_for(ref, orc):
 MG_CASES = [("poisson", 5, 3, S.GabpRedBlack, 2, 2, {}), ("poisson", 5, 3, S.GabpSequential, 1, 1, {}),
             ("poisson", 5, 3, S.GabpFourColor, 1, 1, {}), ("poisson", 5, 3, S.GsRedBlack, 2, 2, {}),
             ("poisson", 5, 3, S.GabpFlood, 2, 2, {}), ("boundary-layer", 6, 6, S.GabpRedBlack, 5, 0, {"eps": 0.01}),
-            ("general", 6, 4, S.GabpRedBlack, 2, 2, {}), ("anisotropic", 6, 4, S.GabpSequential, 2, 2, {"eps": 1e-3})]
+            ("general", 6, 4, S.GabpRedBlack, 2, 2, {}), ("anisotropic", 6, 4, S.GabpSequential, 2, 2, {"eps": 1e-3}),
+            # recorded red-black smoothing with unequal sweep counts: one sweep (phase kernels), two
+            # (first-pair + last-pair launches), three and more (phase kernels in between)
+            ("general", 6, 4, S.GabpRedBlack, 3, 1, {}), ("poisson", 6, 3, S.GabpRedBlack, 1, 2, {}),
+            ("anisotropic", 5, 3, S.GabpRedBlack, 4, 3, {"eps": 1e-2})]
 
 
 @pytest.mark.parametrize("prob,J1,J2,sm,pre,post,params", MG_CASES)
