@@ -256,20 +256,25 @@ static __global__ void __launch_bounds__(256) k_rb_mean_first_pair(RbP P, const 
     const int off[4] = {-P.nx, -1, 1, P.nx};
     double acc = r[r_compact ? nR + q : g], in[4], lam[4];
     int kq[4];
+    uint32_t mkk[4];
+    double rk[4], lk[4];
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {  // loads independent of the mask (indices clamped)
+    for (int s = 0; s < 4; ++s) {  // every load first, independent of the masks (indices clamped)
         const int k = g + off[s];
         const int kc = k < 0 ? 0 : (k > 2 * nR - 2 ? 2 * nR - 2 : k);  // clamped into the reds' natural range
         kq[s] = kc >> 1;
-        const double rk = r[r_compact ? kq[s] : rb_nat(P, kq[s], 0)];
-        const uint32_t mkk = __ldg(P.mask[0] + kq[s]);
-        const double lk = __ldg(lamR + (size_t)(3 - s) * nR + kq[s]);
+        rk[s] = r[r_compact ? kq[s] : rb_nat(P, kq[s], 0)];
+        mkk[s] = __ldg(P.mask[0] + kq[s]);
+        lk[s] = __ldg(lamR + (size_t)(3 - s) * nR + kq[s]);
         lam[s] = __ldg(lamB + (size_t)s * nB + q);
+    }
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
         // the red neighbour's visit (k_rb_mean_half<0, FIRST>): acc = r (+ 0 per in-slot), message
         // = lambda * (acc - 0)
-        double ak = rk;
-        if (mkk & 0xfu) ak = dadd(ak, 0.0);
-        in[s] = dmul(lk, dsub(ak, 0.0));
+        double ak = rk[s];
+        if (mkk[s] & 0xfu) ak = dadd(ak, 0.0);
+        in[s] = dmul(lk[s], dsub(ak, 0.0));
     }
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
