@@ -134,14 +134,19 @@ void Engine::rb_smooth_add(const double* r, int sweeps, double* x, bool r_compac
     double* mB = mR + 4 * (size_t)rb.nR;
     const unsigned gr = nblk_host(rb.nR), gb = nblk_host(std::max(rb.nB, 1));
     const int rc = r_compact ? 1 : 0;  // r as launch_residual(..., rb_nx) wrote it
-    int s0 = 0;
-    if (sweeps >= 2 && rb.nB > 0) {  // sweep 1, both colours, one launch (k_rb_mean_first_pair)
-        k_rb_mean_first_pair<<<gb, 256, 0, st>>>(rb, r, mR, rb_lamrec[0], rc);
-        s0 = 1;
-    }
     // the last sweep's two phases in one launch (k_rb_mean_last_pair) on full grids
     static const bool pair_on = !(getenv("BGABP_RB_LAST_PAIR") && std::string(getenv("BGABP_RB_LAST_PAIR")) == "0");
-    const bool last_pair = pair_on && s0 == 1 && grid5_full && rb.nx >= 2;
+    const bool full = pair_on && grid5_full && rb.nx >= 2 && rb.nB > 0;
+    if (sweeps == 1 && full) {  // the whole call in one launch
+        k_rb_mean_first_pair<true><<<gb, 256, 0, st>>>(rb, r, mR, rb_lamrec[0], rc, rb_sigrec[0], x);
+        return;
+    }
+    int s0 = 0;
+    if (sweeps >= 2 && rb.nB > 0) {  // sweep 1, both colours, one launch (k_rb_mean_first_pair)
+        k_rb_mean_first_pair<false><<<gb, 256, 0, st>>>(rb, r, mR, rb_lamrec[0], rc, nullptr, nullptr);
+        s0 = 1;
+    }
+    const bool last_pair = full && s0 == 1;
     for (int s = s0; s < sweeps; ++s) {
         if (last_pair && s + 1 == sweeps) {
             k_rb_mean_last_pair<<<gb, 256, 0, st>>>(rb, r, mR, rb_lamrec[s], rb_sigrec[s], x, rc);

@@ -243,9 +243,14 @@ static __global__ void __launch_bounds__(256) k_rb_mean_half(RbP P, const double
 // message loads (64 B per red-black pair) never reach memory; every recorded lambda entry of
 // the reds is still read exactly once, by the node it points to.  Sweeps >= 2 only (with one
 // sweep the red nodes' x += e needs its own visit).
+// ONLY: a one-sweep call (V(1,1)) on a full grid: this pair is also the last one, so the black node
+// sends nothing and the x += e of itself and of the red neighbour it owns (k_rb_mean_last_pair's
+// rule) happen here; sig_rec / x are used only then.
+template <bool ONLY>
 static __global__ void __launch_bounds__(256) k_rb_mean_first_pair(RbP P, const double* __restrict__ r,
                                                                   double* m_red, const double* __restrict__ lam_rec,
-                                                                  int r_compact) {
+                                                                  int r_compact, const double* __restrict__ sig_rec,
+                                                                  double* __restrict__ x) {
     const int nR = P.nR, nB = P.nB;
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nB) return;
@@ -266,7 +271,15 @@ static __global__ void __launch_bounds__(256) k_rb_mean_first_pair(RbP P, const 
         rk[s] = r[r_compact ? kq[s] : rb_nat(P, kq[s], 0)];
         mkk[s] = __ldg(P.mask[0] + kq[s]);
         lk[s] = __ldg(lamR + (size_t)(3 - s) * nR + kq[s]);
-        lam[s] = __ldg(lamB + (size_t)s * nB + q);
+        lam[s] = ONLY ? 0.0 : __ldg(lamB + (size_t)s * nB + q);
+    }
+    double sk[4], xk[4];
+    const double sg = ONLY ? __ldg(sig_rec + nR + q) : 1.0, xg = ONLY ? x[g] : 0.0;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        const bool ew = ONLY && (s == 1 || s == 2);  // only an eastern / western neighbour can own k
+        sk[s] = ew ? __ldg(sig_rec + kq[s]) : 1.0;
+        xk[s] = ew ? x[rb_nat(P, kq[s], 0)] : 0.0;
     }
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
@@ -275,11 +288,17 @@ static __global__ void __launch_bounds__(256) k_rb_mean_first_pair(RbP P, const 
         double ak = rk[s];
         if (mkk[s] & 0xfu) ak = dadd(ak, 0.0);
         in[s] = dmul(lk[s], dsub(ak, 0.0));
+        if (ONLY && (s == 1 || s == 2) && (mk & (1u << s)) && (s == 1 || !(mkk[s] & (1u << 2))))
+            x[rb_nat(P, kq[s], 0)] = dadd(xk[s], ddiv(ak, sk[s]));
     }
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
         if (!(mk & (1u << s))) in[s] = 0.0;
         else acc = dadd(acc, in[s]);
+    }
+    if (ONLY) {
+        x[g] = dadd(xg, ddiv(acc, sg));
+        return;
     }
 #pragma unroll
     for (int s = 0; s < 4; ++s)

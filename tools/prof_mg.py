@@ -24,7 +24,8 @@ sm = {"rb": g.MgSmoother.GabpRedBlack, "gs": g.MgSmoother.GsRedBlack}[a.smoother
 h = g.Hierarchy.from_levels([p.A for p in levels], [p.nx for p in levels], sm)
 b = torch.tensor(levels[0].b, device="cuda")
 x = torch.zeros_like(b)
-rep = g.mg_solve_device(h, g.CycleSpec(2, 2, sm), b.data_ptr(), x.data_ptr(),
+SW = int(os.environ.get("PROF_MG_SWEEPS", "2"))
+rep = g.mg_solve_device(h, g.CycleSpec(SW, SW, sm), b.data_ptr(), x.data_ptr(),
                         g.MgSolveOptions(tol=1e-8 * float(np.abs(levels[0].b).max()), max_cycles=a.cycles))
 torch.cuda.synchronize()
 print(rep.status, rep.iterations)
@@ -35,7 +36,7 @@ if os.environ.get("PROF_MG_TIME"):
         x.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        rep = g.mg_solve_device(h, g.CycleSpec(2, 2, sm), b.data_ptr(), x.data_ptr(),
+        rep = g.mg_solve_device(h, g.CycleSpec(SW, SW, sm), b.data_ptr(), x.data_ptr(),
                                 g.MgSolveOptions(tol=tol_t, max_cycles=int(os.environ["PROF_MG_TIME"])))
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0

@@ -18,12 +18,18 @@ python tools/prof_mg.py --J 12 --sigma 2 --cycles 4 > $O/prof_mg.log 2>&1
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file $O/launches_mg.csv python tools/prof_mg.py --J 12 --sigma 2 --cycles 4 > $O/ncu_launches_mg.log 2>&1
 # the compact-r residual and the phase that reads it (fine level of config 5)
-timeout 900 ncu --set full --import-source on --clock-control none -k "regex:k_residual_dia" -s 2 -c 2 \
+timeout 900 ncu --set full --import-source on --clock-control none -k "regex:k_residual_dia" -s 0 -c 3 \
     -o $O/ncu_mgres python tools/prof_mg.py --J 12 --sigma 2 --cycles 3 > $O/ncu_mgres.log 2>&1
 ncu -i $O/ncu_mgres.ncu-rep --page raw --csv > $O/ncu_mgres.raw.csv 2>/dev/null
-timeout 900 ncu --set full --import-source on --clock-control none -k "regex:k_rb_mean_half" -s 0 -c 4 \
+# the two launches of a recorded V(2,2) smoothing call (first pair, last pair), fine level
+timeout 900 ncu --set full --import-source on --clock-control none -k "regex:k_rb_mean_(first|last)_pair" -s 0 -c 2 \
     -o $O/ncu_mgphase python tools/prof_mg.py --J 12 --sigma 2 --cycles 3 > $O/ncu_mgphase.log 2>&1
 ncu -i $O/ncu_mgphase.ncu-rep --page raw --csv > $O/ncu_mgphase.raw.csv 2>/dev/null
+# the phase kernels (V(3,3): the middle sweep runs them)
+PROF_MG_SWEEPS=3 python tools/prof_mg.py --J 12 --sigma 2 --cycles 2 > $O/prof_mg_v33.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k "regex:k_rb_mean_half" -s 0 -c 2 \
+    -o $O/ncu_mgphase3 env PROF_MG_SWEEPS=3 python tools/prof_mg.py --J 12 --sigma 2 --cycles 2 > $O/ncu_mgphase3.log 2>&1
+ncu -i $O/ncu_mgphase3.ncu-rep --page raw --csv > $O/ncu_mgphase3.raw.csv 2>/dev/null
 rm -f $O/*.ncu-rep
 tail -3 $O/pytest_gpu.log; tail -2 $O/smoke.log
 for f in $O/bench_*.log; do echo "== $f"; tail -c 400 $f; echo; done
