@@ -354,6 +354,10 @@ def run_gpu(args, world, rank, local):
     # a constant-coefficient stencil (config 2) runs the variant with the coefficients and the
     # diagonal as kernel parameters: it moves 32E + 28n, less than the SURVEY formula counts
     kernel_bytes = 32.0 * E + 28.0 * n if info.get("uniform_coefficients") else bytes_sweep
+    if info["layout"] == 1 and not info["symmetric_values"]:
+        # nonsymmetric stencils: the out-edge coefficient A_kj is read from row k's own entry (a line
+        # node k fetches for its residual), so only one coefficient array comes from DRAM
+        kernel_bytes = bytes_sweep - 8.0 * E
     traffic = None
     tp = os.path.join(ROOT, "profiles", "flood_traffic.json")
     if os.path.exists(tp):
@@ -421,7 +425,8 @@ def run_gpu(args, world, rank, local):
     formula = (("32*E + 28*n: messages 16 B/edge in + 16 B/edge out; b, x(t-2) read, x(t-1) write, mask per node "
                 "(coefficients are kernel parameters)") if info.get("uniform_coefficients") else
                "40*E + 24*n (B_sweep, SURVEY.md 8(d)) + 8*n (x read of the fused residual)"
-               + ("" if info["symmetric_values"] else " + 8*E (row coefficients of the residual)"))
+               + ("" if info["symmetric_values"] else " (the out-edge coefficients come from the neighbours' row "
+                  "entries through L1/L2, not DRAM; SURVEY's figure adds 8*E for them)"))
     extra = {}
     if info["layout"] == 2:
         # general sparsity: 44*E + 28*n counts 4 B of index per edge and per node
