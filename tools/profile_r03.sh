@@ -30,6 +30,12 @@ PROF_MG_SWEEPS=3 python tools/prof_mg.py --J 12 --sigma 2 --cycles 2 > $O/prof_m
 timeout 900 ncu --set full --import-source on --clock-control none -k "regex:k_rb_mean_half" -s 0 -c 2 \
     -o $O/ncu_mgphase3 env PROF_MG_SWEEPS=3 python tools/prof_mg.py --J 12 --sigma 2 --cycles 2 > $O/ncu_mgphase3.log 2>&1
 ncu -i $O/ncu_mgphase3.ncu-rep --page raw --csv > $O/ncu_mgphase3.raw.csv 2>/dev/null
+# config 3's nonsymmetric step (out-edge coefficients from the neighbours' row entries)
+timeout 900 python bench.py --workload config3 --steps 500 --warmup 20 --no-cpu-baseline > $O/bench_config3.log 2>&1; echo "exit $?" >> $O/bench_config3.log
+python tools/kernel_drivers.py flood3 > $O/drv_flood3.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k "regex:k_flood_solve_dia" -s 20 -c 1 \
+    -o $O/ncu_flood3 python tools/kernel_drivers.py flood3 > $O/ncu_flood3.log 2>&1
+ncu -i $O/ncu_flood3.ncu-rep --page raw --csv > $O/ncu_flood3.raw.csv 2>/dev/null
 rm -f $O/*.ncu-rep
 tail -3 $O/pytest_gpu.log; tail -2 $O/smoke.log
 for f in $O/bench_*.log; do echo "== $f"; tail -c 400 $f; echo; done
