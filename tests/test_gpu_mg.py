@@ -190,6 +190,43 @@ def test_mg_solve_matches_cpu_restatement(orc, ref, golden, prob, J1, J2, sm, pr
         assert (h.num_levels(), int(got.status), got.iterations) == (rec["levels"], rec["status"], rec["iterations"])
 
 
+@pytest.mark.parametrize("pre,post", [(1, 1), (2, 2), (3, 2)])
+def test_red_black_smoothing_on_a_grid_with_missing_couplings(orc, ref, pre, post):
+    """A 5-point grid whose fine level lacks a few couplings (both directions dropped): the recorded
+    red-black smoothing call then takes its general route -- first-pair launch by the masks, colour
+    phases, the silent last black phase -- instead of the full-grid pair launches.  Bit-identical
+    to the restated / reference V-cycle over the same matrices."""
+    import scipy.sparse as sp
+    from oracle.oracle import Csr
+    O = _oracle_for(ref, orc)
+    ps = [g.assemble("poisson", J, {}) for J in (5, 4, 3)]
+    A0 = ps[0].A
+    M = sp.csr_matrix((A0.values, A0.col_indices, A0.row_offsets), shape=(A0.n, A0.n)).tolil()
+    nx = ps[0].nx
+    for i in (0, 7, nx + 3, 5 * nx + 11, A0.n - 2):      # east couplings
+        M[i, i + 1] = 0.0
+        M[i + 1, i] = 0.0
+    for i in (2, 3 * nx + 9):                              # north couplings
+        M[i, i + nx] = 0.0
+        M[i + nx, i] = 0.0
+    M = M.tocsr()
+    M.eliminate_zeros()
+    M.sort_indices()
+    fine = g.SparseMatrix(A0.n, M.indptr.astype(np.int32), M.indices.astype(np.int32), M.data.astype(np.float64))
+    assert fine.nnz == A0.nnz - 14
+    levels = [fine, ps[1].A, ps[2].A]
+    nxs = [p.nx for p in ps]
+    b = ps[0].b
+    oh = O.hierarchy([Csr(A.n, A.row_offsets, A.col_indices, A.values) for A in levels], nxs, int(S.GabpRedBlack))
+    tol = 1e-8 * np.abs(b).max()
+    want = oh.solve(pre, post, b, tol=tol, max_cycles=40)
+    h = g.Hierarchy.from_levels(levels, nxs, S.GabpRedBlack)
+    got = g.mg_solve(h, g.CycleSpec(pre, post, S.GabpRedBlack), b, g.MgSolveOptions(tol=tol, max_cycles=40))
+    assert (int(got.status), got.iterations, got.detail) == (want.status, want.iterations, want.detail)
+    assert got.residual_history.tobytes() == want.residual_history.tobytes()
+    assert got.solution.tobytes() == want.solution.tobytes()
+
+
 @pytest.mark.parametrize("frozen", [False, True])
 @pytest.mark.parametrize("prob,J1,J2,sm,pre,post,params", MG_CASES + [("mixed", 5, 3, S.GabpFourColor, 0, 4, {})])
 def test_mg_solve_matches_reference_multigrid_cpp(ref, prob, J1, J2, sm, pre, post, params, frozen):
