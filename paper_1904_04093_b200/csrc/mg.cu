@@ -133,16 +133,29 @@ __global__ void k_mg_clear(Ctrl* const* c, int nl) {
 // out[0] = the stop test's residual bits: *rres, or the max of the npart per-block values in
 // rpart (k_residual_dia's rpart), or 0; out[1] = min over halted levels of
 // (fail_seq << 32 | level), kNone if no level halted: the first failure in execution order.
-// One block of 1024 threads.
+// With rpart: kMgSummaryBlocks blocks of 1024 threads fold the partials into out[0] by atomicMax
+// (the caller zeroes it first; one block alone is bound by a single SM's L2 bandwidth: 12-35 us
+// for the 65k partials of a 4095^2 level); block 0 also scans the levels.  Otherwise one block.
+constexpr int kMgSummaryBlocks = 16;
 __global__ void __launch_bounds__(1024) k_mg_summary(Ctrl* const* c, int nl, const unsigned long long* rres,
                                                      const unsigned long long* rpart, int npart,
                                                      unsigned long long* out) {
     __shared__ unsigned long long part[32];
     unsigned long long m = 0ull;
     if (rpart) {
-        for (int i = threadIdx.x; i < npart; i += blockDim.x) {
-            const unsigned long long v = rpart[i];
-            m = v > m ? v : m;
+        // 16 independent loads in flight per thread (one dependent L2 round trip per element made
+        // this 35 us for the 65k partials of a 4095^2 level)
+        constexpr int U = 4;
+        const int nthr = gridDim.x * blockDim.x;
+        for (int i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < npart; i0 += U * nthr) {
+            unsigned long long v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * nthr;
+                v[u] = i < npart ? __ldcg(rpart + i) : 0ull;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) m = v[u] > m ? v[u] : m;
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -152,16 +165,37 @@ __global__ void __launch_bounds__(1024) k_mg_summary(Ctrl* const* c, int nl, con
         if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = m;
         __syncthreads();
     }
+    if (blockIdx.x != 0) {  // the other blocks only fold their slice of the partials
+        if (threadIdx.x == 0) {
+            for (int k = 1; k < (int)(blockDim.x >> 5); ++k) m = part[k] > m ? part[k] : m;
+            if (m != 0ull) atomicMax(&out[0], m);
+        }
+        return;
+    }
+    if (threadIdx.x >= 32) return;
+    // the levels' halt words in parallel (lane k = level k, then levels k + 32, ...): one pair of
+    // dependent loads instead of nl of them in a row
+    unsigned long long best = kNone;
+    for (int k = threadIdx.x; k < nl; k += 32) {
+        const Ctrl* ck = c[k];
+        if (ck->halt) {
+            const unsigned long long key = ((unsigned long long)(unsigned)ck->fail_seq << 32) | (unsigned)k;
+            best = key < best ? key : best;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
+        best = other < best ? other : best;
+    }
     if (threadIdx.x != 0) return;
     if (rpart)
         for (int k = 1; k < (int)(blockDim.x >> 5); ++k) m = part[k] > m ? part[k] : m;
-    unsigned long long best = kNone;
-    for (int k = 0; k < nl; ++k)
-        if (c[k]->halt) {
-            const unsigned long long key = ((unsigned long long)(unsigned)c[k]->fail_seq << 32) | (unsigned)k;
-            best = key < best ? key : best;
-        }
-    out[0] = rpart ? m : (rres ? *rres : 0ull);
+    if (rpart) {
+        if (m != 0ull) atomicMax(&out[0], m);  // out[0] was zeroed before the residual launch
+    } else {
+        out[0] = rres ? *rres : 0ull;
+    }
     out[1] = best;
 }
 
@@ -484,6 +518,7 @@ struct bgmg {
         const bool parts = spec && L.layout == BGABP_LAYOUT_DIA && L.n > 0;
         if (parts && !d_rpart)
             ck(cudaMalloc(&d_rpart, sizeof(unsigned long long) * L.residual_blocks()), "malloc");
+        if (parts) ck(cudaMemsetAsync(d_sum, 0, sizeof(unsigned long long), st), "memset");  // k_mg_summary's max
         if (!parts) ck(cudaMemsetAsync(&L.d_ctrl->red[2], 0, sizeof(unsigned long long), st), "memset");
         L.launch_residual(b, x, L.d_r, &L.d_ctrl->red[2], MODE_PLAIN, 0, fine_r_compact ? levels[0].sched.nx : 0,
                           parts ? d_rpart : nullptr);
@@ -555,8 +590,9 @@ struct bgmg {
             // stop test and failure summary in one read
             Engine& L = E(0);
             const bool parts = stop_test_residual(&spec, b, x);
-            k_mg_summary<<<1, 1024, 0, st>>>(d_ctrls, nl(), &L.d_ctrl->red[2], parts ? d_rpart : nullptr,
-                                             (int)L.residual_blocks(), d_sum);
+            k_mg_summary<<<parts ? kMgSummaryBlocks : 1, 1024, 0, st>>>(d_ctrls, nl(), &L.d_ctrl->red[2],
+                                                                         parts ? d_rpart : nullptr,
+                                                                         (int)L.residual_blocks(), d_sum);
             ck(cudaMemcpyAsync(h_sum, d_sum, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st), "D2H");
             ck(cudaStreamSynchronize(st), "sync");
             const double r = bits2d(h_sum[0]);
