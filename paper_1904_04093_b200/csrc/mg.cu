@@ -352,8 +352,13 @@ struct bgmg {
         smooth(k, b, x, spec.pre, spec.frozen != 0, reuse);
         MgLevel& C = levels[k + 1];
         L.launch_residual(b, x, L.d_r, nullptr, MODE_PLAIN);
-        k_restrict<<<nblk_host(C.E->n), 256, 0, st>>>(L.d_r, levels[k].nx, C.d_b);
-        ck(cudaMemsetAsync(C.d_x, 0, sizeof(double) * std::max(C.E->n, 1), st), "memset");
+        const int mc = (levels[k].nx - 1) / 2;
+        if ((long long)mc * mc == C.E->n && C.E->n > 0) {  // the restriction also zeroes the coarse start vector
+            k_restrict<<<nblk_host(C.E->n), 256, 0, st>>>(L.d_r, levels[k].nx, C.d_b, C.d_x);
+        } else {
+            k_restrict<<<nblk_host(C.E->n), 256, 0, st>>>(L.d_r, levels[k].nx, C.d_b);
+            ck(cudaMemsetAsync(C.d_x, 0, sizeof(double) * std::max(C.E->n, 1), st), "memset");
+        }
         cycle(k + 1, spec, C.d_b, C.d_x);
         k_prolong_add<<<dim3(nblk_host(C.nx + 1), levels[k].nx), 256, 0, st>>>(C.d_x, C.nx, x, 0);
         smooth(k, b, x, spec.post, spec.frozen != 0);
