@@ -593,6 +593,15 @@ def time_to_solution(g, torch, args):
     del e3
     smoothers = (("gabp_red_black", g.MgSmoother.GabpRedBlack), ("gs_red_black", g.MgSmoother.GsRedBlack),
                  ("gabp_flood", g.MgSmoother.GabpFlood))
+    # warm-up: one small hierarchy and solve per smoother, so that the one-time costs of a process (the
+    # CUDA modules of the multigrid kernels load on first use: 0.1-1 s) are not charged to the first
+    # timed configuration
+    wl, wb = _mg_levels(g, 7, 1.0)
+    for _name, sm in smoothers:
+        wh = g.Hierarchy.from_levels([p.A for p in wl], [p.nx for p in wl], sm)
+        g.mg_solve(wh, g.CycleSpec(2, 2, sm), wb, g.MgSolveOptions(tol=1e-8 * float(np.abs(wb).max()), max_cycles=5))
+        del wh
+    torch.cuda.synchronize()
     for sigma in (1.0, 2.0):
         levels, b = _mg_levels(g, args.mg_J, sigma)
         tol = 1e-8 * float(np.abs(b).max())
@@ -640,6 +649,13 @@ def run_mg(args, world, rank, local):
                                   "K = exp(N(0, sigma^2)) per unknown, harmonic faces, rediscretised levels "
                                   "(K coarsened by arithmetic full weighting), rows scaled 1/h^2"},
            "gpu": {}, "cpu_reference": {}}
+    # warm-up (module loads of the multigrid kernels, see time_to_solution)
+    wl, wb = _mg_levels(g, 7, 1.0)
+    for sm in (g.MgSmoother.GabpRedBlack, g.MgSmoother.GsRedBlack, g.MgSmoother.GabpFlood):
+        wh = g.Hierarchy.from_levels([p.A for p in wl], [p.nx for p in wl], sm)
+        g.mg_solve(wh, g.CycleSpec(2, 2, sm), wb, g.MgSolveOptions(tol=1e-8 * float(np.abs(wb).max()), max_cycles=5))
+        del wh
+    torch.cuda.synchronize()
     for sigma in args.mg_sigmas:
         levels, b = _mg_levels(g, J, sigma)
         bd = torch.tensor(b, device="cuda")
