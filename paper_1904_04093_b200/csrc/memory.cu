@@ -21,7 +21,8 @@ namespace bgabp {
 // solve after another, the shards of a re-partitioned system -- reuses its blocks instead of
 // paying cudaFree / cudaMalloc and the driver's re-zeroing of freed pages (~0.15 s for a config-5
 // hierarchy).  Blocks stay whole cudaMalloc allocations (CUDA IPC of shard buffers works).
-// BGABP_NO_BLOCK_CACHE=1 frees immediately; at most 16 GB are held (all devices).
+// BGABP_NO_BLOCK_CACHE=1 frees immediately; at most BGABP_BLOCK_CACHE_GB (default 32) GB are held
+// (all devices).
 namespace {
 struct BlockCache {
     std::mutex mu;
@@ -29,7 +30,14 @@ struct BlockCache {
     std::map<void*, std::pair<int, size_t>> sizes;  // every block handed out, with its rounded size
     size_t held = 0;
     bool off = getenv("BGABP_NO_BLOCK_CACHE") != nullptr;
-    static constexpr size_t kMin = size_t(1) << 20, kGran = size_t(2) << 20, kCap = size_t(16) << 30;
+    static constexpr size_t kMin = size_t(1) << 20, kGran = size_t(2) << 20;
+    // idle blocks kept: 32 GB of the B200's 180 GB by default (a config-5 hierarchy holds ~12 GB, and
+    // a fresh cudaMalloc / cudaFree of its blocks costs 0.1-0.3 s); BGABP_BLOCK_CACHE_GB overrides
+    size_t kCap = [] {
+        const char* e = getenv("BGABP_BLOCK_CACHE_GB");
+        const long gb = e ? std::atol(e) : 32;
+        return size_t(gb < 0 ? 0 : gb) << 30;
+    }();
 };
 BlockCache& block_cache() {
     static BlockCache* c = new BlockCache();
@@ -104,7 +112,7 @@ void release_block(void* p) {
         if (it != C.sizes.end()) {
             const auto key = it->second;
             C.sizes.erase(it);
-            if (C.held + key.second <= BlockCache::kCap) {
+            if (C.held + key.second <= C.kCap) {
                 C.free_blocks.emplace(key, p);
                 C.held += key.second;
                 return;
